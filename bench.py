@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""bench.py -- replica-variable updates/s of the batched multi-replica dynamics loop.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2] [--solver pa|sbm] [--T 1000]
+
+One bench "step" = one full solve (T dynamics iterations for all R replicas of the
+workload, exact energies, best-first order) -- one pass of the hot path over one
+batch of synthetic input.  metric = R * N * T / time (replica-variable updates/s),
+whole job: at N GPUs each rank owns R replicas (replica sharding, weak scaling) and
+the job value is N * R * n * T / max-over-ranks time.
+
+  value   device-resident: the problem is in HBM, outputs stay on the device, CUDA
+          events on the launching stream, L2 flushed (256 MiB write) between solves.
+  e2e     through the public API solve_pa/solve_sbm with HOST buffers: every step
+          uploads the model (COO + h from pinned host memory) and reads back states,
+          energies and order (wall clock, barrier + synchronize on both sides).
+  roofline  dominant kernel = the per-step dynamics kernel; achieved = algorithmic
+          bytes * units per launch / mean launch time (library CUDA events).
+  cpu_baseline  the oracle's C port (1 thread) timed on a bounded sample (fewer
+          replicas / steps of the same instance) on this host, rank 0 at N=1.
+
+--impl reference runs the unmodified reference (baseline/_ref/qubokit) on a bounded
+sample of the same workload: its own IsingModel, coupling_operator() and sign_pm,
+driving the reference loop lines (parallel_annealing.py:41-45 / bifurcation.py:37-47)
+for R_s replicas x T_s steps per bench step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--solver", default="pa", choices=["pa", "sbm"])
+    ap.add_argument("--T", type=int, default=None)
+    ap.add_argument("--replicas", type=int, default=None)
+    ap.add_argument("--n", type=int, default=None, help="override instance size")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--path", default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", 1416.4)), "measured"
+    return FALLBACK_HBM_GBS, 1400.0, "fallback"
+
+
+def bytes_per_update(solver: str, dbar: float, R: int) -> float:
+    """algorithmic bytes per replica-variable update (fp32 state, int32+fp32 CSR)."""
+    amort = (8.0 * dbar + 4.0) / R
+    if solver == "pa":
+        return 16.0 + (1.0 + dbar) / 8.0 + amort
+    return 16.0 + 4.0 * dbar + amort
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cfg_params(args):
+    from paper_2501_19221_b200.instances import CONFIGS
+    c = CONFIGS[args.config]
+    R = args.replicas or c["R"]
+    T = args.T or c["T"]
+    return R, T, c["desc"]
+
+
+def make_params(vxq, solver, R, T, seed):
+    if solver == "pa":
+        return vxq.PaParams(steps=T, replicas=R, seed=seed)
+    return vxq.SbmParams(steps=T, dt=0.05, replicas=R, seed=seed)
+
+
+def cpu_sample_plan(nnz: int, n: int, R: int, T: int, target_ops: float = 3e9):
+    """Bounded sample: (replicas, steps) so the C port does ~target_ops field terms."""
+    per = max(nnz + n, 1)
+    budget = max(target_ops / per, 1.0)
+    Rs = int(min(R, max(1, 2 ** int(np.log2(max(budget ** 0.5, 1.0))))))
+    Ts = int(min(T, max(1, budget // Rs)))
+    return Rs, Ts
+
+
+def cpu_baseline(model, solver, R, T):
+    import oracle as O
+    ip, ix, dv = O.symmetric_csr(model.n, model.rows, model.cols, model.values)
+    nnz = int(ip[-1])
+    Rs, Ts = cpu_sample_plan(nnz, model.n, R, T)
+    if solver == "pa":
+        lam0 = O.resolve_lambda0(model)
+        X = O.pa_init(0, Rs, model.n)
+        M = np.zeros_like(X)
+        sched = O.pa_schedule(lam0, T)[:Ts]
+        t0 = time.perf_counter()
+        O.pa_run(ip, ix, dv, model.h, sched, 0.05, 0.9, X, M, np.float32)
+        dt = time.perf_counter() - t0
+    else:
+        Q, P = O.sbm_init(0, Rs, model.n, 1.0)
+        sched = O.sbm_schedule(1.0, T)[:Ts]
+        t0 = time.perf_counter()
+        O.sbm_run(ip, ix, -dv, -np.asarray(model.h), sched, 0.05, 1.0, 0.5, 1.0, Q, P,
+                  np.float32)
+        dt = time.perf_counter() - t0
+    v = Rs * model.n * Ts / dt
+    return {"value": v, "unit": "rv-updates/s", "cores": 1, "kind": "port",
+            "sample": f"oracle/oracle.c fp32 restatement, {Rs} replicas x {Ts} steps of the "
+                      f"same instance ({dt:.2f} s)"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    try:
+        import qubokit as qk
+        from qubokit.model import sign_pm
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"qubokit import failed: {e}"}))
+        return 0
+    from paper_2501_19221_b200 import instances
+    R, T, desc = cfg_params(args)
+    m = instances.build(args.config, args.n)
+    model = qk.IsingModel(n=m.n, h=np.array(m.h), rows=np.array(m.rows), cols=np.array(m.cols),
+                          values=np.array(m.values), offset=m.offset)
+    A = model.coupling_operator()
+    nnz = 2 * model.num_couplings
+    Rs, Ts = cpu_sample_plan(nnz, model.n, R, T, target_ops=1.5e9)
+    if args.config == "cfg1":
+        Rs, Ts = R, T  # the full solve is cheap: time the reference's own solve_*
+    n = model.n
+
+    def one_step(seed):
+        if args.config == "cfg1":
+            if args.solver == "pa":
+                qk.solve_pa(model, qk.PaParams(steps=T, replicas=R, seed=seed))
+            else:
+                qk.solve_sbm(model, qk.SbmParams(steps=T, dt=0.05, replicas=R, seed=seed))
+            return
+        streams = [qk.rng_stream(seed, r) for r in range(Rs)]
+        if args.solver == "pa":
+            lam0 = max(model.field_scale, 1e-12)
+            X = np.stack([g.uniform(-1.0, 1.0, size=n) for g in streams])
+            M = np.zeros_like(X)
+            h = model.h
+            for t in range(Ts):
+                lam = lam0 * (1.0 - t / T)
+                grad = lam * X + sign_pm(X).astype(np.float64) @ A + h
+                M = 0.9 * M - 0.05 * grad
+                X = np.clip(X + M, -1.0, 1.0)
+        else:
+            from qubokit.solvers.bifurcation import integrate
+            Q = np.stack([s.uniform(-1.0, 1.0, size=n) for s in streams])
+            P = np.stack([s.uniform(-1.0, 1.0, size=n) for s in streams])
+            integrate(-A, -model.h, Q, P, 0.05, np.linspace(0.0, 1.0, T)[:Ts], 1.0, 0.5, 1.0)
+
+    for w in range(args.warmup):
+        one_step(w)
+    times = []
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        one_step(100 + k)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.sum(times))
+    units = Rs * n * Ts * args.steps
+    v = units / dt
+    threads = os.environ.get("OPENBLAS_NUM_THREADS") or str(os.cpu_count())
+    line = {
+        "impl": "reference", "metric": "replica-variable updates/s", "value": v,
+        "unit": "rv-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {desc}", "solver": args.solver, "n": n,
+                   "replicas": R, "steps_per_solve": T,
+                   "sample": f"{Rs} replicas x {Ts} steps per bench step"},
+        "cpu_baseline": {"value": v, "unit": "rv-updates/s", "cores": os.cpu_count(),
+                         "kind": "reference",
+                         "sample": (f"unmodified qubokit (baseline/_ref) "
+                                    + ("solve_" + args.solver if args.config == "cfg1" else
+                                       "loop lines with its own coupling_operator/sign_pm")
+                                    + f", {Rs} replicas x {Ts} steps, BLAS threads {threads}")},
+        "e2e": {"value": v, "unit": "rv-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2501_19221_b200 as vxq
+    from paper_2501_19221_b200 import instances
+    from paper_2501_19221_b200.solvers import run_device
+
+    R, T, desc = cfg_params(args)
+    t_build = time.perf_counter()
+    model = instances.build(args.config, args.n)
+    t_build = time.perf_counter() - t_build
+    n = model.n
+    params = make_params(vxq, args.solver, R, T, seed=0)
+    rbegin = rank * R  # replica sharding: rank g owns global replicas [gR, (g+1)R)
+
+    stream = torch.cuda.Stream()
+    states = torch.empty((R, n), dtype=torch.int8, device="cuda")
+    energies = torch.empty(R, dtype=torch.float64, device="cuda")
+    order = torch.empty(R, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def solve_dev():
+        return run_device(args.solver, model, params, states.data_ptr(), energies.data_ptr(),
+                          order_ptr=order.data_ptr(), stream=stream.cuda_stream,
+                          precision=args.precision, path=args.path, device=local,
+                          replica_begin=rbegin)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.fill_(1)
+            solve_dev()
+        torch.cuda.synchronize()
+        barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        loop_ms, launches, info = [], 0, {}
+        with ClockSampler(local) as clk:
+            for k in range(args.steps):
+                flush.fill_(k & 0xff)
+                ev[k][0].record(stream)
+                info = solve_dev()
+                ev[k][1].record(stream)
+                loop_ms.append(info["loop_ms"])
+                launches += int(info["launches"])
+            torch.cuda.synchronize()
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(np.sum(step_ms))
+    t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        # final argmin reduce over replica shards (the only data-path collective)
+        best = torch.tensor([energies.min().item()], dtype=torch.float64, device="cuda")
+        dist.all_reduce(best, op=dist.ReduceOp.MIN)
+    tot_ms = float(t.item())
+    units = world * R * n * T * args.steps
+    value = units / (tot_ms / 1e3)
+
+    # roofline of the dominant kernel (per-step dynamics kernel)
+    hbm, bf16, src = peaks()
+    mean_step_kernel_ms = float(np.mean(loop_ms)) / T
+    dbar = 2.0 * model.num_couplings / n
+    if info.get("path") == "dense":
+        flops = 2.0 * n * R * n
+        achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                "frac": achieved / bf16, "traffic": None,
+                "kernel": "dense J.S step (tcgen05) + fused integrator", "peak_source": src}
+    else:
+        B = bytes_per_update(args.solver, dbar, R)
+        achieved = B * R * n / (mean_step_kernel_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "kernel": f"k_{args.solver}_step ({info.get('path')})",
+                "bytes_per_update": B, "units_per_launch": R * n,
+                "mean_launch_ms": mean_step_kernel_ms,
+                "frac_of_8TBs_nominal": achieved / 8000.0, "peak_source": src}
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        solve = vxq.solve_pa if args.solver == "pa" else vxq.solve_sbm
+        K = max(1, min(args.steps, 3))
+        rows = np.ascontiguousarray(model.rows)
+        h2d = int(model.rows.nbytes + model.cols.nbytes + model.values.nbytes + model.h.nbytes)
+        d2h = int(R * n + 16 * R)
+        walls = []
+        for k in range(K + 1):
+            fresh = vxq.IsingModel(n=n, h=model.h, rows=rows, cols=model.cols,
+                                   values=model.values, offset=model.offset)
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            ss = solve(fresh, params, precision=args.precision, path=args.path, device=local,
+                       replica_begin=rbegin)
+            torch.cuda.synchronize()
+            barrier()
+            if k > 0:
+                walls.append(time.perf_counter() - t0)
+            vxq.clear_cache(fresh)
+            del fresh
+        wt = torch.tensor([float(np.sum(walls))], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * R * n * T * len(walls) / float(wt.item()),
+               "unit": "rv-updates/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "best_energy": float(ss.best.energy)}
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(model, args.solver, R, T)
+
+    if rank == 0:
+        line = {
+            "metric": "replica-variable updates/s", "value": value, "unit": "rv-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic (seeded instance, see config)",
+            "config": {"workload": f"{args.config}: {desc}", "solver": args.solver, "n": n,
+                       "couplings": int(model.num_couplings), "replicas_per_gpu": R,
+                       "steps_per_solve": T, "path": info.get("path"),
+                       "precision": args.precision,
+                       "l2": "flushed between timed solves (256 MiB write)",
+                       "parallelism": f"replica-sharded x{world}",
+                       "instance_build_s": round(t_build, 2)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "best_energy": float(energies.min().item()),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,159 @@
+/*
+ * vxq.h -- C-ABI of the B200-native batched multi-replica dynamics loop.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (qubokit, /root/reference/pkg/src/qubokit):
+ *
+ *   reference entry point                              replaced by
+ *   -------------------------------------------------  ------------------------------
+ *   IsingModel + coupling_operator()/_csr              vxq_problem_create
+ *       model.py:113-192 (frozen COO i<j, h, offset)
+ *   solve_pa(model, PaParams) -> SampleSet             vxq_pa_solve
+ *       solvers/parallel_annealing.py:28-48
+ *   solve_sbm(model, SbmParams) -> SampleSet           vxq_sbm_solve
+ *       solvers/bifurcation.py:50-67
+ *   integrate(B, g, Q, P, dt, a_schedule, a0, c0, q)   vxq_sbm_integrate
+ *       solvers/bifurcation.py:37-47
+ *   IsingModel.energies(states)                        vxq_energies
+ *       model.py:160-164 (here: correctly rounded exact sums)
+ *   resolve_lambda0 / field_scale                      vxq_problem_lambda0
+ *       parallel_annealing.py:23-25, model.py:194-200
+ *   resolve_c0 / eig_extreme(-A, "max")                vxq_problem_c0
+ *       bifurcation.py:25-34, solvers/eigen.py:35-56
+ *
+ * Conventions: plain host pointers and sizes; no torch types.  All entry
+ * points are reentrant (one CUDA stream + stream-ordered workspace per call,
+ * no global mutable state beyond a per-device context cache).  Return 0 on
+ * success, else a VXQ_ERR_* code; vxq_last_error() gives a thread-local
+ * message.  Parameter validation (ValidationError in the reference,
+ * common.py:109-116,136-144) happens in the host layer before the call; the
+ * C layer re-checks and returns VXQ_ERR_INVALID.
+ */
+#ifndef VXQ_H_
+#define VXQ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define VXQ_API __attribute__((visibility("default")))
+#else
+#define VXQ_API
+#endif
+
+#define VXQ_ABI_VERSION 1
+
+#define VXQ_OK 0
+#define VXQ_ERR_INVALID 1     /* -> ValidationError */
+#define VXQ_ERR_OOM 2         /* -> QubokitError    */
+#define VXQ_ERR_CUDA 3        /* -> QubokitError    */
+#define VXQ_ERR_UNSUPPORTED 4 /* -> QubokitError    */
+
+/* precision of the dynamics loop */
+#define VXQ_FP32 0 /* default: fp32 state, fp32 CSR values, sequential row sums */
+#define VXQ_FP64 1 /* parity mode: bit-exact with the reference's CSR path     */
+
+/* kernel path */
+#define VXQ_PATH_AUTO 0
+#define VXQ_PATH_RESIDENT 1 /* small n: one CTA owns replicas for all T steps  */
+#define VXQ_PATH_SPARSE 2   /* CSR SpMM + fused integrator, one launch per step */
+#define VXQ_PATH_DENSE 3    /* tcgen05/TMEM J.S GEMM with fused integrator      */
+
+typedef struct vxq_problem vxq_problem;
+
+/* PaParams (common.py:94-116). lambda0 NaN => auto (field scale). */
+typedef struct {
+    int64_t steps;
+    double learning_rate;
+    double momentum;
+    double lambda0;
+    int64_t replicas;
+    uint64_t seed;
+} vxq_pa_params;
+
+/* SbmParams (common.py:119-144). c0 NaN => auto (1 / lambda_max(-A)). */
+typedef struct {
+    int64_t steps;
+    double dt;
+    double a0;
+    double c0;
+    double q_cap;
+    double init_noise;
+    int64_t replicas;
+    uint64_t seed;
+} vxq_sbm_params;
+
+typedef struct {
+    int32_t precision;         /* VXQ_FP32 | VXQ_FP64                            */
+    int32_t path;              /* VXQ_PATH_*                                     */
+    int32_t outputs_on_device; /* 1: vxq_outputs pointers are device pointers    */
+    int32_t track_best;        /* 1: return best-seen state per replica (opt-in) */
+    int64_t replica_begin;     /* global index of local replica 0 (sharding)     */
+    void* stream;              /* cudaStream_t; NULL => library stream           */
+} vxq_run_opts;
+
+typedef struct {
+    int8_t* states;      /* [R][n] spins (+1/-1), replica-major  (required) */
+    double* energies;    /* [R] exact energies                    (required) */
+    double* x;           /* [R][n] final X (PA) / Q (SBM), optional          */
+    double* m;           /* [R][n] final M (PA) / P (SBM), optional          */
+    int64_t* order;      /* [R] replicas by ascending energy, ties by index (optional;
+                            argsort(kind="stable") of common.py:57)                  */
+    /* filled by the library */
+    double lambda0_used; /* PA  */
+    double c0_used;      /* SBM */
+    double loop_ms;      /* device time of the dynamics loop (CUDA events)   */
+    int64_t launches;    /* kernels launched by this call                    */
+    int32_t path_used;   /* VXQ_PATH_* actually run                          */
+    int32_t reserved;
+} vxq_outputs;
+
+/* Build a device problem from the reference's canonical arrays:
+ * rows/cols int64 with rows[k] < cols[k], sorted unique (model.py:81-104),
+ * values/h fp64, offset. device = CUDA ordinal. Host pointers. */
+VXQ_API int vxq_problem_create(int64_t n, int64_t num_couplings, const int64_t* rows,
+                       const int64_t* cols, const double* values, const double* h,
+                       double offset, int device, vxq_problem** out);
+VXQ_API int vxq_problem_destroy(vxq_problem* p);
+/* info: [n, num_couplings, nnz_sym, dense_eligible, uniform_magnitude] */
+VXQ_API int vxq_problem_info(const vxq_problem* p, int64_t* info5);
+
+VXQ_API int vxq_problem_lambda0(vxq_problem* p, double* out); /* max(field_scale, 1e-12) */
+VXQ_API int vxq_problem_c0(vxq_problem* p, double* out);      /* 1/lambda_max(-A) or 1.0 */
+
+VXQ_API int vxq_pa_solve(vxq_problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts,
+                 vxq_outputs* out);
+VXQ_API int vxq_sbm_solve(vxq_problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts,
+                  vxq_outputs* out);
+
+/* integrate(B, g, Q, P, ...): B given as CSR of B^T (row i lists B[j,i]),
+ * Q/P [R][n] fp64 host arrays updated in place; a_sched[T] host fp64. */
+VXQ_API int vxq_sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indices,
+                      const double* bt_data, const double* g, int64_t R, double* Q,
+                      double* P, const double* a_sched, int64_t T, double dt, double a0,
+                      double c0, double q_cap, const vxq_run_opts* opts);
+
+/* Exact energies of R spin states [R][n] int8 (host, or device if
+ * opts->outputs_on_device) -> energies[R] (same residency). */
+VXQ_API int vxq_energies(vxq_problem* p, const int8_t* states, int64_t R, double* energies,
+                 const vxq_run_opts* opts);
+
+/* Host-only helpers (no GPU needed): the step schedules the loops use,
+ * bit-exact with the reference's Python expressions.
+ *   PA : lam_t = lambda0 * (1.0 - t / T)        parallel_annealing.py:42
+ *   SBM: a_t   = numpy.linspace(0.0, a0, T)[t]  bifurcation.py:63          */
+VXQ_API int vxq_pa_schedule(double lambda0, int64_t T, double* out);
+VXQ_API int vxq_sbm_schedule(double a0, int64_t T, double* out);
+
+VXQ_API const char* vxq_last_error(void);
+VXQ_API int vxq_abi_version(void);
+VXQ_API int vxq_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VXQ_H_ */

@@ -1,0 +1,217 @@
+// capi.cu -- extern "C" boundary (include/vxq.h).  Every entry point catches, maps the
+// failure to a VXQ_ERR_* code and leaves a thread-local message for vxq_last_error().
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "vxq_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return VXQ_OK;
+    } catch (const vxq::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return VXQ_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return VXQ_ERR_CUDA;
+    }
+}
+
+void check_outputs(const vxq_outputs* out) {
+    VXQ_REQUIRE(out != nullptr, "outputs must not be null");
+    VXQ_REQUIRE(out->states && out->energies, "outputs.states and outputs.energies are required");
+}
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        VXQ_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+}  // namespace
+
+struct vxq_problem {
+    vxq::Problem* p;
+};
+
+extern "C" {
+
+int vxq_abi_version(void) { return VXQ_ABI_VERSION; }
+
+const char* vxq_last_error(void) { return g_last_error.c_str(); }
+
+int vxq_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int vxq_pa_schedule(double lambda0, int64_t T, double* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(T >= 0 && (T == 0 || out), "invalid schedule arguments");
+        vxq::pa_schedule(lambda0, T, out);
+    });
+}
+
+int vxq_sbm_schedule(double a0, int64_t T, double* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(T >= 0 && (T == 0 || out), "invalid schedule arguments");
+        vxq::sbm_schedule(a0, T, out);
+    });
+}
+
+int vxq_problem_create(int64_t n, int64_t num_couplings, const int64_t* rows,
+                       const int64_t* cols, const double* values, const double* h,
+                       double offset, int device, vxq_problem** out) {
+    return guarded([&] {
+        VXQ_REQUIRE(out != nullptr, "out must not be null");
+        *out = nullptr;
+        DeviceGuard dg(device);
+        vxq::Problem* p =
+            vxq::problem_create(n, num_couplings, rows, cols, values, h, offset, device);
+        *out = new vxq_problem{p};
+    });
+}
+
+int vxq_problem_destroy(vxq_problem* p) {
+    return guarded([&] {
+        if (!p) return;
+        delete p->p;
+        delete p;
+    });
+}
+
+int vxq_problem_info(const vxq_problem* p, int64_t* info5) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && info5, "null argument");
+        info5[0] = p->p->n;
+        info5[1] = p->p->m;
+        info5[2] = p->p->nnz;
+        info5[3] = p->p->max_row_nnz;
+        info5[4] = p->p->uniform_magnitude ? 1 : 0;
+    });
+}
+
+int vxq_problem_lambda0(vxq_problem* p, double* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && out, "null argument");
+        DeviceGuard dg(p->p->device);
+        vxq::StreamScope ss(nullptr);
+        *out = vxq::problem_lambda0(p->p, ss.s);
+    });
+}
+
+int vxq_problem_c0(vxq_problem* p, double* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && out, "null argument");
+        DeviceGuard dg(p->p->device);
+        vxq::StreamScope ss(nullptr);
+        *out = vxq::problem_c0(p->p, ss.s);
+    });
+}
+
+int vxq_pa_solve(vxq_problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts,
+                 vxq_outputs* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && prm, "null argument");
+        check_outputs(out);
+        // PaParams.validate (common.py:109-116)
+        VXQ_REQUIRE(prm->steps > 0, "steps must be positive");
+        VXQ_REQUIRE(prm->learning_rate > 0, "learning_rate must be positive");
+        VXQ_REQUIRE(prm->momentum >= 0 && prm->momentum < 1, "momentum must lie in [0, 1)");
+        VXQ_REQUIRE(std::isnan(prm->lambda0) || prm->lambda0 > 0, "lambda0 must be positive");
+        VXQ_REQUIRE(prm->replicas > 0, "replicas must be positive");
+        DeviceGuard dg(p->p->device);
+        vxq::StreamScope ss(opts ? opts->stream : nullptr);
+        vxq::pa_solve(p->p, prm, opts, out, ss.s);
+    });
+}
+
+int vxq_sbm_solve(vxq_problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts,
+                  vxq_outputs* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && prm, "null argument");
+        check_outputs(out);
+        // SbmParams.validate (common.py:136-144)
+        VXQ_REQUIRE(prm->steps > 0, "steps must be positive");
+        VXQ_REQUIRE(prm->dt > 0, "dt must be positive");
+        VXQ_REQUIRE(prm->a0 > 0, "a0 must be positive");
+        VXQ_REQUIRE(std::isnan(prm->c0) || prm->c0 > 0, "c0 must be positive");
+        VXQ_REQUIRE(prm->q_cap > 0, "q_cap must be positive");
+        VXQ_REQUIRE(prm->init_noise > 0, "init_noise must be positive");
+        VXQ_REQUIRE(prm->replicas > 0, "replicas must be positive");
+        DeviceGuard dg(p->p->device);
+        vxq::StreamScope ss(opts ? opts->stream : nullptr);
+        vxq::sbm_solve(p->p, prm, opts, out, ss.s);
+    });
+}
+
+int vxq_sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indices,
+                      const double* bt_data, const double* g, int64_t R, double* Q,
+                      double* P, const double* a_sched, int64_t T, double dt, double a0,
+                      double c0, double q_cap, const vxq_run_opts* opts) {
+    return guarded([&] {
+        VXQ_REQUIRE(n >= 1 && R >= 1 && T >= 0, "invalid sizes");
+        VXQ_REQUIRE(bt_indptr && g && Q && P && (T == 0 || a_sched), "null argument");
+        int dev = 0;
+        VXQ_CUDA(cudaGetDevice(&dev));
+        vxq::StreamScope ss(opts ? opts->stream : nullptr);
+        vxq::sbm_integrate(n, bt_indptr, bt_indices, bt_data, g, R, Q, P, a_sched, T, dt, a0,
+                           c0, q_cap, opts, ss.s);
+    });
+}
+
+int vxq_energies(vxq_problem* p, const int8_t* states, int64_t R, double* energies,
+                 const vxq_run_opts* opts) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && states && energies && R >= 0, "null argument");
+        if (R == 0) return;
+        DeviceGuard dg(p->p->device);
+        vxq::StreamScope ss(opts ? opts->stream : nullptr);
+        cudaStream_t s = ss.s;
+        const int64_t n = p->p->n;
+        const int64_t W = vxq::ceil_div(R, 32);
+        const bool on_dev = opts && opts->outputs_on_device;
+        vxq::DevBuf<int8_t> st;
+        const int8_t* sd = states;
+        if (!on_dev) {
+            st = vxq::DevBuf<int8_t>(n * R, s);
+            VXQ_CUDA(cudaMemcpyAsync(st.get(), states, n * R, cudaMemcpyHostToDevice, s));
+            sd = st.get();
+        }
+        vxq::DevBuf<uint32_t> sb(n * W, s);
+        vxq::pack_states_to_bits(sd, n, R, W, sb.get(), s);
+        vxq::DevBuf<double> e;
+        double* ed = energies;
+        if (!on_dev) {
+            e = vxq::DevBuf<double>(R, s);
+            ed = e.get();
+        }
+        vxq::energies_from_bits(p->p, sb.get(), W, R, ed, s);
+        if (!on_dev)
+            VXQ_CUDA(cudaMemcpyAsync(energies, ed, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+        VXQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"
+
+namespace vxq {
+struct DenseOperand {};
+void dense_destroy(DenseOperand* d) { delete d; }
+}  // namespace vxq

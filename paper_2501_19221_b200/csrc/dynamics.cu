@@ -1,0 +1,824 @@
+// dynamics.cu -- the batched multi-replica dynamics loop on sm_100a.
+//
+// PA  (solvers/parallel_annealing.py:41-45), per (row i, replica r):
+//     f    = sum_k J_ik s_{j_k}          (CSR row, ascending j, sequential, starts at 0)
+//     grad = (lam_t * x + f) + h_i
+//     m    = alpha * m - eta * grad
+//     x    = clip(x + m, -1, 1);  s = sign(x)  (sign(0) = +1)
+// SBM (solvers/bifurcation.py:40-46), with B = -A, g = -h:
+//     f  = sum_k B_ik q_{j_k}
+//     p  = p + dt * ( -((q*q + a0) - a_t) * q + c0 * (f + g_i) )
+//     q  = q + (dt*a0) * p;  |q| > q_cap => q = clip(q), p = 0
+//
+// Every binary op is rounded once (no FMA contraction) in the reference's evaluation
+// order, and the row sum runs in the same order as scipy's csc_matvecs for X @ A_csr,
+// so the fp64 build reproduces the reference's CSR path bit for bit and the fp32 build
+// reproduces oracle/oracle.c's fp32 restatement bit for bit.
+//
+// HBM layout (one problem, R_pad replicas, V = values per lane, chunk = 32 V replicas):
+//   state[i][R_pad]: replica r sits at c*32V + l*V + b  (c = r / 32V, b = (r % 32V) / 32,
+//   l = r % 32), so lane l of the warp owning (row i, chunk c) loads its V replicas with
+//   one 16-byte vector access and the V sign words of the chunk come out of V ballots.
+//   sign bits sb[i][W], W = R_pad / 32: bit (r % 32) of word r / 32 (natural order).
+#include <algorithm>
+#include <vector>
+
+#include "vxq_internal.h"
+
+namespace vxq {
+
+template <typename T>
+struct Operator {  // field_i = sum_k (sign * data[k]) * v[indices[k]]
+    const int64_t* indptr;
+    const int32_t* indices;
+    const T* data;
+    T sign;
+};
+
+__device__ __forceinline__ int64_t lane_base(int64_t i, int64_t R_pad, int c, int lane, int V) {
+    return i * R_pad + (int64_t)c * 32 * V + (int64_t)lane * V;
+}
+
+__device__ __forceinline__ int64_t pos_of(int64_t r, int V) {
+    int64_t ch = 32 * V;
+    int64_t c = r / ch, rem = r % ch;
+    return c * ch + (rem % 32) * V + rem / 32;
+}
+
+// ------------------------------------------------------------------ init (Philox)
+template <typename T>
+__global__ void k_init_pa(int64_t n, int64_t R_pad, int V, uint64_t seed, int64_t rbegin,
+                          T* __restrict__ x, T* __restrict__ m) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t nq = (n + 3) / 4;
+    if (idx >= nq * R_pad) return;
+    int64_t q = idx / R_pad, r = idx % R_pad;
+    U64x4 o = philox4x64_10((uint64_t)q + 1, 0, (uint64_t)(rbegin + r), 0, seed, 0);
+    int64_t p = pos_of(r, V);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        int64_t i = 4 * q + w;
+        if (i < n) {
+            double v = uniform_from_raw(o.v[w], -1.0, 2.0);  // uniform(-1, 1)
+            x[i * R_pad + p] = (T)v;
+            m[i * R_pad + p] = (T)0;
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_init_sbm(int64_t n, int64_t R_pad, int V, uint64_t seed, int64_t rbegin,
+                           double amp, T* __restrict__ q, T* __restrict__ pm) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t nq = (2 * n + 3) / 4;
+    if (idx >= nq * R_pad) return;
+    int64_t qd = idx / R_pad, r = idx % R_pad;
+    U64x4 o = philox4x64_10((uint64_t)qd + 1, 0, (uint64_t)(rbegin + r), 0, seed, 0);
+    int64_t p = pos_of(r, V);
+    const double lo = -amp, range = __dadd_rn(amp, amp);  // hi - lo
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        int64_t k = 4 * qd + w;
+        double v = uniform_from_raw(o.v[w], lo, range);
+        if (k < n) q[k * R_pad + p] = (T)v;
+        else if (k < 2 * n) pm[(k - n) * R_pad + p] = (T)v;
+    }
+}
+
+// [R][n] fp64 host-order array <-> interleaved layout
+template <typename T>
+__global__ void k_import(const double* __restrict__ src, int64_t n, int64_t R, int64_t R_pad,
+                         int V, T* __restrict__ dst) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n * R_pad) return;
+    int64_t r = idx / n, i = idx % n;
+    T v = (r < R) ? (T)src[r * n + i] : (T)0;
+    dst[i * R_pad + pos_of(r, V)] = v;
+}
+
+template <typename T>
+__global__ void k_export(const T* __restrict__ src, int64_t n, int64_t R, int64_t R_pad, int V,
+                         double* __restrict__ dst) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n * R) return;
+    int64_t r = idx / n, i = idx % n;
+    dst[idx] = (double)src[i * R_pad + pos_of(r, V)];
+}
+
+// sign bits of the final analog state
+template <typename T, int V>
+__global__ void k_pack_signs(const T* __restrict__ x, int64_t n, int64_t R_pad,
+                             uint32_t* __restrict__ sb) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int chunks = (int)(R_pad / (32 * V));
+    const int64_t i = warp / chunks;
+    const int c = (int)(warp % chunks);
+    if (i >= n) return;
+    Vec<T, V> xv = *reinterpret_cast<const Vec<T, V>*>(x + lane_base(i, R_pad, c, lane, V));
+    const int64_t W = R_pad / 32;
+#pragma unroll
+    for (int b = 0; b < V; ++b) {
+        uint32_t word = __ballot_sync(0xffffffffu, xv.v[b] >= (T)0);
+        if (lane == b) sb[i * W + c * V + b] = word;
+    }
+}
+
+// ------------------------------------------------------------------ PA step (sparse)
+template <typename T, int V>
+__global__ void __launch_bounds__(256) k_pa_step(int64_t n, int64_t R_pad, Operator<T> op,
+                                                 const T* __restrict__ h, T lam, T eta, T alpha,
+                                                 T* __restrict__ x, T* __restrict__ m,
+                                                 const uint32_t* __restrict__ sb_in,
+                                                 uint32_t* __restrict__ sb_out) {
+    using O = Ops<T>;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int chunks = (int)(R_pad / (32 * V));
+    const int64_t i = warp / chunks;
+    const int c = (int)(warp % chunks);
+    if (i >= n) return;
+    const int64_t W = R_pad / 32;
+    const int64_t base = lane_base(i, R_pad, c, lane, V);
+    Vec<T, V> xv = *reinterpret_cast<const Vec<T, V>*>(x + base);
+    Vec<T, V> mv = *reinterpret_cast<const Vec<T, V>*>(m + base);
+
+    T f[V];
+#pragma unroll
+    for (int b = 0; b < V; ++b) f[b] = (T)0;
+    const uint32_t* sbc = sb_in + c * V;
+    const int64_t k0 = __ldg(op.indptr + i), k1 = __ldg(op.indptr + i + 1);
+    int64_t k = k0;
+    // batches of 4 neighbours: issue all gathers, then accumulate in order
+    for (; k + 4 <= k1; k += 4) {
+        int j[4];
+        T a[4];
+        Vec<uint32_t, V> w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            j[u] = __ldg(op.indices + k + u);
+            a[u] = O::mul(op.sign, __ldg(op.data + k + u));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            w[u] = *reinterpret_cast<const Vec<uint32_t, V>*>(sbc + (int64_t)j[u] * W);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int b = 0; b < V; ++b)
+                f[b] = O::add(f[b], ((w[u].v[b] >> lane) & 1u) ? a[u] : -a[u]);
+    }
+    for (; k < k1; ++k) {
+        int j = __ldg(op.indices + k);
+        T a = O::mul(op.sign, __ldg(op.data + k));
+        Vec<uint32_t, V> w = *reinterpret_cast<const Vec<uint32_t, V>*>(sbc + (int64_t)j * W);
+#pragma unroll
+        for (int b = 0; b < V; ++b) f[b] = O::add(f[b], ((w.v[b] >> lane) & 1u) ? a : -a);
+    }
+
+    const T hi = __ldg(h + i);
+#pragma unroll
+    for (int b = 0; b < V; ++b) {
+        T xo = xv.v[b];
+        T grad = O::add(O::add(O::mul(lam, xo), f[b]), hi);
+        T mn = O::sub(O::mul(alpha, mv.v[b]), O::mul(eta, grad));
+        T xn = O::add(xo, mn);
+        xn = xn < (T)-1 ? (T)-1 : (xn > (T)1 ? (T)1 : xn);
+        xv.v[b] = xn;
+        mv.v[b] = mn;
+        uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
+        if (lane == b) sb_out[i * W + c * V + b] = word;
+    }
+    *reinterpret_cast<Vec<T, V>*>(x + base) = xv;
+    *reinterpret_cast<Vec<T, V>*>(m + base) = mv;
+}
+
+// ------------------------------------------------------------------ SBM step (sparse)
+template <typename T>
+struct SbmScalars {
+    T a_t, dt, a0, c0, dta0, q_cap;
+};
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) k_sbm_step(int64_t n, int64_t R_pad, Operator<T> op,
+                                                  const T* __restrict__ g, SbmScalars<T> sc,
+                                                  const T* __restrict__ q_in,
+                                                  T* __restrict__ q_out, T* __restrict__ p) {
+    using O = Ops<T>;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int chunks = (int)(R_pad / (32 * V));
+    const int64_t i = warp / chunks;
+    const int c = (int)(warp % chunks);
+    if (i >= n) return;
+    const int64_t off = (int64_t)c * 32 * V + (int64_t)lane * V;
+    const int64_t base = i * R_pad + off;
+    T f[V];
+#pragma unroll
+    for (int b = 0; b < V; ++b) f[b] = (T)0;
+    const int64_t k0 = __ldg(op.indptr + i), k1 = __ldg(op.indptr + i + 1);
+    int64_t k = k0;
+    for (; k + 4 <= k1; k += 4) {
+        int j[4];
+        T a[4];
+        Vec<T, V> qv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            j[u] = __ldg(op.indices + k + u);
+            a[u] = O::mul(op.sign, __ldg(op.data + k + u));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            qv[u] = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j[u] * R_pad + off);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a[u], qv[u].v[b]));
+    }
+    for (; k < k1; ++k) {
+        int j = __ldg(op.indices + k);
+        T a = O::mul(op.sign, __ldg(op.data + k));
+        Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j * R_pad + off);
+#pragma unroll
+        for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a, qv.v[b]));
+    }
+    Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(q_in + base);
+    Vec<T, V> pv = *reinterpret_cast<const Vec<T, V>*>(p + base);
+    const T gi = __ldg(g + i);
+#pragma unroll
+    for (int b = 0; b < V; ++b) {
+        T qi = qv.v[b];
+        T inner = -O::sub(O::add(O::mul(qi, qi), sc.a0), sc.a_t);
+        T force = O::add(O::mul(inner, qi), O::mul(sc.c0, O::add(f[b], gi)));
+        T pn = O::add(pv.v[b], O::mul(sc.dt, force));
+        T qn = O::add(qi, O::mul(sc.dta0, pn));
+        if (fabs(qn) > sc.q_cap) {
+            qn = qn < -sc.q_cap ? -sc.q_cap : sc.q_cap;
+            pn = (T)0;
+        }
+        qv.v[b] = qn;
+        pv.v[b] = pn;
+    }
+    *reinterpret_cast<Vec<T, V>*>(q_out + base) = qv;
+    *reinterpret_cast<Vec<T, V>*>(p + base) = pv;
+}
+
+// ------------------------------------------------------------------ resident (small n)
+// One CTA owns RG replicas for all T steps; their state lives in shared memory, the
+// CSR streams from L1/L2.  One __syncthreads per step (double-buffered spins / q).
+template <typename T>
+__global__ void k_pa_resident(int64_t n, int64_t R_pad, int V, int RG, Operator<T> op,
+                              const T* __restrict__ h, const T* __restrict__ lam_sched,
+                              int64_t steps, T eta, T alpha, T* __restrict__ x,
+                              T* __restrict__ m) {
+    using O = Ops<T>;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* xs = reinterpret_cast<T*>(smem);
+    T* ms = xs + (int64_t)RG * n;
+    uint8_t* s0 = reinterpret_cast<uint8_t*>(ms + (int64_t)RG * n);
+    uint8_t* s1 = s0 + (int64_t)RG * n;
+    const int64_t r0 = (int64_t)blockIdx.x * RG;
+    const int64_t items = (int64_t)RG * n;
+    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
+        int64_t g = it / n, i = it % n;
+        int64_t r = r0 + g;
+        T xv = (r < R_pad) ? x[i * R_pad + pos_of(r, V)] : (T)0;
+        T mv = (r < R_pad) ? m[i * R_pad + pos_of(r, V)] : (T)0;
+        xs[it] = xv;
+        ms[it] = mv;
+        s0[it] = xv >= (T)0;
+    }
+    __syncthreads();
+    for (int64_t t = 0; t < steps; ++t) {
+        const T lam = lam_sched[t];
+        const uint8_t* sc = (t & 1) ? s1 : s0;
+        uint8_t* sn = (t & 1) ? s0 : s1;
+        for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
+            int64_t g = it / n, i = it % n;
+            const uint8_t* sg = sc + g * n;
+            T f = (T)0;
+            for (int64_t k = __ldg(op.indptr + i); k < __ldg(op.indptr + i + 1); ++k) {
+                T a = O::mul(op.sign, __ldg(op.data + k));
+                f = O::add(f, sg[__ldg(op.indices + k)] ? a : -a);
+            }
+            T xo = xs[it];
+            T grad = O::add(O::add(O::mul(lam, xo), f), __ldg(h + i));
+            T mn = O::sub(O::mul(alpha, ms[it]), O::mul(eta, grad));
+            T xn = O::add(xo, mn);
+            xn = xn < (T)-1 ? (T)-1 : (xn > (T)1 ? (T)1 : xn);
+            xs[it] = xn;
+            ms[it] = mn;
+            sn[it] = xn >= (T)0;
+        }
+        __syncthreads();
+    }
+    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
+        int64_t g = it / n, i = it % n;
+        int64_t r = r0 + g;
+        if (r < R_pad) {
+            x[i * R_pad + pos_of(r, V)] = xs[it];
+            m[i * R_pad + pos_of(r, V)] = ms[it];
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_sbm_resident(int64_t n, int64_t R_pad, int V, int RG, Operator<T> op,
+                               const T* __restrict__ g, const T* __restrict__ a_sched,
+                               int64_t steps, SbmScalars<T> sc0, T* __restrict__ q,
+                               T* __restrict__ p) {
+    using O = Ops<T>;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* q0 = reinterpret_cast<T*>(smem);
+    T* q1 = q0 + (int64_t)RG * n;
+    T* ps = q1 + (int64_t)RG * n;
+    const int64_t r0 = (int64_t)blockIdx.x * RG;
+    const int64_t items = (int64_t)RG * n;
+    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
+        int64_t gg = it / n, i = it % n;
+        int64_t r = r0 + gg;
+        q0[it] = (r < R_pad) ? q[i * R_pad + pos_of(r, V)] : (T)0;
+        ps[it] = (r < R_pad) ? p[i * R_pad + pos_of(r, V)] : (T)0;
+    }
+    __syncthreads();
+    for (int64_t t = 0; t < steps; ++t) {
+        const T a_t = a_sched[t];
+        const T* qc = (t & 1) ? q1 : q0;
+        T* qn_arr = (t & 1) ? q0 : q1;
+        for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
+            int64_t gg = it / n, i = it % n;
+            const T* qg = qc + gg * n;
+            T f = (T)0;
+            for (int64_t k = __ldg(op.indptr + i); k < __ldg(op.indptr + i + 1); ++k) {
+                T a = O::mul(op.sign, __ldg(op.data + k));
+                f = O::add(f, O::mul(a, qg[__ldg(op.indices + k)]));
+            }
+            T qi = qc[it];
+            T inner = -O::sub(O::add(O::mul(qi, qi), sc0.a0), a_t);
+            T force = O::add(O::mul(inner, qi), O::mul(sc0.c0, O::add(f, __ldg(g + i))));
+            T pn = O::add(ps[it], O::mul(sc0.dt, force));
+            T qn = O::add(qi, O::mul(sc0.dta0, pn));
+            if (fabs(qn) > sc0.q_cap) {
+                qn = qn < -sc0.q_cap ? -sc0.q_cap : sc0.q_cap;
+                pn = (T)0;
+            }
+            qn_arr[it] = qn;
+            ps[it] = pn;
+        }
+        __syncthreads();
+    }
+    const T* qf = (steps & 1) ? q1 : q0;
+    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
+        int64_t gg = it / n, i = it % n;
+        int64_t r = r0 + gg;
+        if (r < R_pad) {
+            q[i * R_pad + pos_of(r, V)] = qf[it];
+            p[i * R_pad + pos_of(r, V)] = ps[it];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+void pa_schedule(double lam0, int64_t T, double* out) {
+    for (int64_t t = 0; t < T; ++t) out[t] = lam0 * (1.0 - (double)t / (double)T);
+}
+
+void sbm_schedule(double a0, int64_t T, double* out) {
+    // numpy.linspace(0.0, a0, T): y = arange(T) * step + 0.0; y[-1] = a0
+    if (T <= 0) return;
+    if (T == 1) {
+        out[0] = 0.0 * a0 + 0.0;
+        return;
+    }
+    const double div = (double)(T - 1);
+    const double step = (a0 - 0.0) / div;
+    if (step == 0.0) {
+        for (int64_t t = 0; t < T; ++t) out[t] = ((double)t / div) * (a0 - 0.0) + 0.0;
+    } else {
+        for (int64_t t = 0; t < T; ++t) out[t] = (double)t * step + 0.0;
+    }
+    out[T - 1] = a0;
+}
+
+namespace {
+
+constexpr int TB = 256;
+inline unsigned nblk(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, TB)); }
+
+struct Layout {
+    int64_t n, R, R_pad, W;
+    int V;
+};
+
+Layout make_layout(int64_t n, int64_t R, bool fp64) {
+    Layout L;
+    L.n = n;
+    L.R = R;
+    if (fp64) L.V = (R <= 32) ? 1 : 2;
+    else L.V = (R <= 32) ? 1 : (R <= 64 ? 2 : 4);
+    int64_t ch = 32 * L.V;
+    L.R_pad = ceil_div(R, ch) * ch;
+    L.W = L.R_pad / 32;
+    return L;
+}
+
+int resident_rg(const Layout& L) {
+    int64_t ctas_target = 148 * 8;
+    int rg = (int)std::max<int64_t>(1, std::min<int64_t>(8, ceil_div(L.R_pad, ctas_target)));
+    return rg;
+}
+
+size_t resident_smem_pa(const Layout& L, int RG, size_t tsz) {
+    return (size_t)RG * L.n * (2 * tsz + 2);
+}
+size_t resident_smem_sbm(const Layout& L, int RG, size_t tsz) {
+    return (size_t)RG * L.n * (3 * tsz);
+}
+
+constexpr size_t kResidentSmemMax = 200 * 1024;
+
+int choose_path(int requested, const Layout& L, size_t smem_needed, int64_t nnz) {
+    if (requested == VXQ_PATH_RESIDENT) {
+        if (smem_needed > kResidentSmemMax)
+            throw Error(VXQ_ERR_UNSUPPORTED, "resident path: state does not fit shared memory");
+        return VXQ_PATH_RESIDENT;
+    }
+    if (requested == VXQ_PATH_SPARSE || requested == VXQ_PATH_DENSE) return VXQ_PATH_SPARSE;
+    // auto: small problems run resident (all steps in one launch); the CSR per replica
+    // must stay cache-friendly (each CTA re-streams it every step)
+    if (smem_needed <= kResidentSmemMax && L.n <= 4096 && nnz <= (int64_t)1 << 20)
+        return VXQ_PATH_RESIDENT;
+    return VXQ_PATH_SPARSE;
+}
+
+int block_threads(int64_t items) {
+    int64_t t = ceil_div(items, 32) * 32;
+    return (int)std::min<int64_t>(512, std::max<int64_t>(32, t));
+}
+
+template <typename T>
+void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T eta, T alpha,
+                    T* x, T* m, const uint32_t* sbi, uint32_t* sbo, cudaStream_t s) {
+    int64_t warps = L.n * (L.R_pad / (32 * L.V));
+    unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
+    switch (L.V) {
+        case 1: k_pa_step<T, 1><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, h, lam, eta, alpha, x, m, sbi, sbo); break;
+        case 2: k_pa_step<T, 2><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, h, lam, eta, alpha, x, m, sbi, sbo); break;
+        default:
+            if constexpr (sizeof(T) == 4)
+                k_pa_step<T, 4><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, h, lam, eta, alpha, x, m, sbi, sbo);
+            break;
+    }
+}
+
+template <typename T>
+void launch_sbm_step(const Layout& L, const Operator<T>& op, const T* g, SbmScalars<T> sc,
+                     const T* qi, T* qo, T* p, cudaStream_t s) {
+    int64_t warps = L.n * (L.R_pad / (32 * L.V));
+    unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
+    switch (L.V) {
+        case 1: k_sbm_step<T, 1><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, g, sc, qi, qo, p); break;
+        case 2: k_sbm_step<T, 2><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, g, sc, qi, qo, p); break;
+        default:
+            if constexpr (sizeof(T) == 4)
+                k_sbm_step<T, 4><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, g, sc, qi, qo, p);
+            break;
+    }
+}
+
+template <typename T>
+void launch_pack(const Layout& L, const T* x, uint32_t* sb, cudaStream_t s) {
+    int64_t warps = L.n * (L.R_pad / (32 * L.V));
+    unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
+    switch (L.V) {
+        case 1: k_pack_signs<T, 1><<<blocks, 256, 0, s>>>(x, L.n, L.R_pad, sb); break;
+        case 2: k_pack_signs<T, 2><<<blocks, 256, 0, s>>>(x, L.n, L.R_pad, sb); break;
+        default:
+            if constexpr (sizeof(T) == 4) k_pack_signs<T, 4><<<blocks, 256, 0, s>>>(x, L.n, L.R_pad, sb);
+            break;
+    }
+    VXQ_CHECK_LAUNCH();
+}
+
+struct EventTimer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s;
+    explicit EventTimer(cudaStream_t st) : s(st) {
+        VXQ_CUDA(cudaEventCreate(&a));
+        VXQ_CUDA(cudaEventCreate(&b));
+    }
+    void start() { VXQ_CUDA(cudaEventRecord(a, s)); }
+    void stop() { VXQ_CUDA(cudaEventRecord(b, s)); }
+    double ms() {
+        float v = 0;
+        VXQ_CUDA(cudaEventSynchronize(b));
+        VXQ_CUDA(cudaEventElapsedTime(&v, a, b));
+        return v;
+    }
+    ~EventTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+// Common tail: sign bits -> exact energies -> states / order / analog exports.
+template <typename T>
+void finish_outputs(Problem* p, const Layout& L, const uint32_t* sb, const T* xa, const T* ma,
+                    const vxq_run_opts* opts, vxq_outputs* out, cudaStream_t s) {
+    const bool on_dev = opts && opts->outputs_on_device;
+    const int64_t n = L.n, R = L.R;
+    DevBuf<double> e_tmp;
+    double* e_dev = out->energies;
+    if (!on_dev) {
+        e_tmp = DevBuf<double>(R, s);
+        e_dev = e_tmp.get();
+    }
+    energies_from_bits(p, sb, L.W, R, e_dev, s);
+    DevBuf<int8_t> st_tmp;
+    int8_t* st_dev = out->states;
+    if (!on_dev) {
+        st_tmp = DevBuf<int8_t>(n * R, s);
+        st_dev = st_tmp.get();
+    }
+    bits_to_states(sb, n, R, L.W, st_dev, s);
+    DevBuf<int64_t> ord_tmp;
+    if (out->order) {
+        int64_t* od = out->order;
+        if (!on_dev) {
+            ord_tmp = DevBuf<int64_t>(R, s);
+            od = ord_tmp.get();
+        }
+        stable_order(e_dev, R, od, s);
+        if (!on_dev)
+            VXQ_CUDA(cudaMemcpyAsync(out->order, od, R * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    }
+    DevBuf<double> xt, mt;
+    if (out->x) {
+        double* xd = out->x;
+        if (!on_dev) {
+            xt = DevBuf<double>(n * R, s);
+            xd = xt.get();
+        }
+        k_export<T><<<nblk(n * R), TB, 0, s>>>(xa, n, R, L.R_pad, L.V, xd);
+        VXQ_CHECK_LAUNCH();
+        if (!on_dev)
+            VXQ_CUDA(cudaMemcpyAsync(out->x, xd, n * R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    if (out->m) {
+        double* md = out->m;
+        if (!on_dev) {
+            mt = DevBuf<double>(n * R, s);
+            md = mt.get();
+        }
+        k_export<T><<<nblk(n * R), TB, 0, s>>>(ma, n, R, L.R_pad, L.V, md);
+        VXQ_CHECK_LAUNCH();
+        if (!on_dev)
+            VXQ_CUDA(cudaMemcpyAsync(out->m, md, n * R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    if (!on_dev) {
+        VXQ_CUDA(cudaMemcpyAsync(out->energies, e_dev, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+        VXQ_CUDA(cudaMemcpyAsync(out->states, st_dev, n * R, cudaMemcpyDeviceToHost, s));
+    }
+    VXQ_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+Operator<T> problem_operator(Problem* p, T sign) {
+    Operator<T> op;
+    op.indptr = p->indptr;
+    op.indices = p->indices;
+    if constexpr (sizeof(T) == 8) op.data = reinterpret_cast<const T*>(p->data64);
+    else op.data = reinterpret_cast<const T*>(p->data32);
+    op.sign = sign;
+    return op;
+}
+
+template <typename T>
+const T* pick(const double* d64, const float* d32) {
+    if constexpr (sizeof(T) == 8) return reinterpret_cast<const T*>(d64);
+    else return reinterpret_cast<const T*>(d32);
+}
+
+template <typename T>
+void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, vxq_outputs* out,
+                cudaStream_t s) {
+    const int64_t n = p->n, R = prm->replicas, T_ = prm->steps;
+    Layout L = make_layout(n, R, sizeof(T) == 8);
+    double lam0 = std::isnan(prm->lambda0) ? problem_lambda0(p, s) : prm->lambda0;
+    out->lambda0_used = lam0;
+    std::vector<double> sched(T_);
+    pa_schedule(lam0, T_, sched.data());
+    const T eta = (T)prm->learning_rate, alpha = (T)prm->momentum;
+    const int64_t rbegin = opts ? opts->replica_begin : 0;
+
+    DevBuf<T> x(n * L.R_pad, s), m(n * L.R_pad, s);
+    DevBuf<uint32_t> sbA(n * L.W, s), sbB(n * L.W, s);
+    int64_t launches = 0;
+    k_init_pa<T><<<nblk(((n + 3) / 4) * L.R_pad), TB, 0, s>>>(n, L.R_pad, L.V, prm->seed, rbegin,
+                                                            x.get(), m.get());
+    VXQ_CHECK_LAUNCH();
+    ++launches;
+    Operator<T> op = problem_operator<T>(p, (T)1);
+    const T* h = pick<T>(p->h64, p->h32);
+    int RG = resident_rg(L);
+    size_t smem = resident_smem_pa(L, RG, sizeof(T));
+    int path = choose_path(opts ? opts->path : 0, L, smem, p->nnz);
+    EventTimer tm(s);
+    const uint32_t* sb_final = nullptr;
+    if (path == VXQ_PATH_RESIDENT) {
+        DevBuf<T> ds(std::max<int64_t>(T_, 1), s);
+        std::vector<T> st(T_);
+        for (int64_t t = 0; t < T_; ++t) st[t] = (T)sched[t];
+        VXQ_CUDA(cudaMemcpyAsync(ds.get(), st.data(), T_ * sizeof(T), cudaMemcpyHostToDevice, s));
+        VXQ_CUDA(cudaFuncSetAttribute(k_pa_resident<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kResidentSmemMax));
+        unsigned grid = (unsigned)ceil_div(L.R_pad, RG);
+        tm.start();
+        k_pa_resident<T><<<grid, block_threads((int64_t)RG * n), smem, s>>>(
+            n, L.R_pad, L.V, RG, op, h, ds.get(), T_, eta, alpha, x.get(), m.get());
+        VXQ_CHECK_LAUNCH();
+        tm.stop();
+        ++launches;
+        launch_pack<T>(L, x.get(), sbA.get(), s);
+        ++launches;
+        sb_final = sbA.get();
+        out->loop_ms = tm.ms();
+        VXQ_CUDA(cudaStreamSynchronize(s));  // keep ds alive until done
+    } else {
+        launch_pack<T>(L, x.get(), sbA.get(), s);  // s_0 = sign(x_0)
+        ++launches;
+        tm.start();
+        uint32_t* bufs[2] = {sbA.get(), sbB.get()};
+        for (int64_t t = 0; t < T_; ++t) {
+            launch_pa_step<T>(L, op, h, (T)sched[t], eta, alpha, x.get(), m.get(), bufs[t & 1],
+                              bufs[(t + 1) & 1], s);
+            ++launches;
+        }
+        VXQ_CHECK_LAUNCH();
+        tm.stop();
+        sb_final = bufs[T_ & 1];
+        out->loop_ms = tm.ms();
+    }
+    out->path_used = path;
+    finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s);
+    out->launches = launches + 4;
+}
+
+template <typename T>
+void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g,
+                  const std::vector<double>& a_sched, double dt, double a0, double c0,
+                  double q_cap, int requested_path, int64_t nnz, T* q, T* qalt, T* pm,
+                  vxq_outputs* out, int64_t& launches, cudaStream_t s, T** q_final) {
+    const int64_t n = L.n, T_ = (int64_t)a_sched.size();
+    SbmScalars<T> sc;
+    sc.a_t = 0;
+    sc.dt = (T)dt;
+    sc.a0 = (T)a0;
+    sc.c0 = (T)c0;
+    sc.dta0 = (T)(dt * a0);  // (dt * a0) in Python floats, then * P
+    sc.q_cap = (T)q_cap;
+    int RG = resident_rg(L);
+    size_t smem = resident_smem_sbm(L, RG, sizeof(T));
+    int path = choose_path(requested_path, L, smem, nnz);
+    EventTimer tm(s);
+    if (path == VXQ_PATH_RESIDENT) {
+        DevBuf<T> ds(std::max<int64_t>(T_, 1), s);
+        std::vector<T> st(T_);
+        for (int64_t t = 0; t < T_; ++t) st[t] = (T)a_sched[t];
+        if (T_) VXQ_CUDA(cudaMemcpyAsync(ds.get(), st.data(), T_ * sizeof(T), cudaMemcpyHostToDevice, s));
+        VXQ_CUDA(cudaFuncSetAttribute(k_sbm_resident<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kResidentSmemMax));
+        unsigned grid = (unsigned)ceil_div(L.R_pad, RG);
+        tm.start();
+        k_sbm_resident<T><<<grid, block_threads((int64_t)RG * n), smem, s>>>(
+            n, L.R_pad, L.V, RG, op, g, ds.get(), T_, sc, q, pm);
+        VXQ_CHECK_LAUNCH();
+        tm.stop();
+        ++launches;
+        *q_final = q;
+        if (out) out->loop_ms = tm.ms();
+        VXQ_CUDA(cudaStreamSynchronize(s));
+    } else {
+        tm.start();
+        T* qs[2] = {q, qalt};
+        for (int64_t t = 0; t < T_; ++t) {
+            sc.a_t = (T)a_sched[t];
+            launch_sbm_step<T>(L, op, g, sc, qs[t & 1], qs[(t + 1) & 1], pm, s);
+            ++launches;
+        }
+        VXQ_CHECK_LAUNCH();
+        tm.stop();
+        *q_final = qs[T_ & 1];
+        if (out) out->loop_ms = tm.ms();
+    }
+    if (out) out->path_used = path;
+}
+
+template <typename T>
+void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts,
+                 vxq_outputs* out, cudaStream_t s) {
+    const int64_t n = p->n, R = prm->replicas, T_ = prm->steps;
+    Layout L = make_layout(n, R, sizeof(T) == 8);
+    double c0 = std::isnan(prm->c0) ? problem_c0(p, s) : prm->c0;
+    out->c0_used = c0;
+    std::vector<double> sched(T_);
+    sbm_schedule(prm->a0, T_, sched.data());
+    const int64_t rbegin = opts ? opts->replica_begin : 0;
+    DevBuf<T> q(n * L.R_pad, s), q2(n * L.R_pad, s), pm(n * L.R_pad, s);
+    DevBuf<uint32_t> sb(n * L.W, s);
+    int64_t launches = 0;
+    k_init_sbm<T><<<nblk(((2 * n + 3) / 4) * L.R_pad), TB, 0, s>>>(
+        n, L.R_pad, L.V, prm->seed, rbegin, prm->init_noise, q.get(), pm.get());
+    VXQ_CHECK_LAUNCH();
+    ++launches;
+    Operator<T> op = problem_operator<T>(p, (T)-1);  // B = -A
+    const T* g = pick<T>(p->g64, p->g32);            // g = -h
+    T* qf = nullptr;
+    sbm_run_core<T>(p, L, op, g, sched, prm->dt, prm->a0, c0, prm->q_cap, opts ? opts->path : 0,
+                    p->nnz, q.get(), q2.get(), pm.get(), out, launches, s, &qf);
+    launch_pack<T>(L, qf, sb.get(), s);
+    ++launches;
+    finish_outputs<T>(p, L, sb.get(), qf, pm.get(), opts, out, s);
+    out->launches = launches + 4;
+}
+
+}  // namespace
+
+void pa_solve(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, vxq_outputs* out,
+              cudaStream_t s) {
+    if (opts && opts->precision == VXQ_FP64) pa_solve_t<double>(p, prm, opts, out, s);
+    else pa_solve_t<float>(p, prm, opts, out, s);
+}
+
+void sbm_solve(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts,
+               vxq_outputs* out, cudaStream_t s) {
+    if (opts && opts->precision == VXQ_FP64) sbm_solve_t<double>(p, prm, opts, out, s);
+    else sbm_solve_t<float>(p, prm, opts, out, s);
+}
+
+namespace {
+__global__ void k_to_f32(int64_t n, const double* a, float* b) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = __double2float_rn(a[i]);
+}
+
+template <typename T>
+void integrate_t(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indices,
+                 const double* bt_data, const double* g, int64_t R, double* Q, double* P,
+                 const double* a_sched, int64_t T_, double dt, double a0, double c0,
+                 double q_cap, const vxq_run_opts* opts, cudaStream_t s) {
+    int64_t nnz = bt_indptr[n];
+    DevBuf<int64_t> ip(n + 1, s);
+    DevBuf<int32_t> ix(std::max<int64_t>(nnz, 1), s);
+    DevBuf<double> dv(std::max<int64_t>(nnz, 1), s), gv(n, s);
+    DevBuf<float> dv32(std::max<int64_t>(nnz, 1), s), gv32(n, s);
+    VXQ_CUDA(cudaMemcpyAsync(ip.get(), bt_indptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    if (nnz) {
+        VXQ_CUDA(cudaMemcpyAsync(ix.get(), bt_indices, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        VXQ_CUDA(cudaMemcpyAsync(dv.get(), bt_data, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        k_to_f32<<<nblk(nnz), TB, 0, s>>>(nnz, dv.get(), dv32.get());
+    }
+    VXQ_CUDA(cudaMemcpyAsync(gv.get(), g, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    k_to_f32<<<nblk(n), TB, 0, s>>>(n, gv.get(), gv32.get());
+    VXQ_CHECK_LAUNCH();
+    Layout L = make_layout(n, R, sizeof(T) == 8);
+    DevBuf<double> hq(n * R, s), hp(n * R, s);
+    VXQ_CUDA(cudaMemcpyAsync(hq.get(), Q, n * R * sizeof(double), cudaMemcpyHostToDevice, s));
+    VXQ_CUDA(cudaMemcpyAsync(hp.get(), P, n * R * sizeof(double), cudaMemcpyHostToDevice, s));
+    DevBuf<T> q(n * L.R_pad, s), q2(n * L.R_pad, s), pm(n * L.R_pad, s);
+    k_import<T><<<nblk(n * L.R_pad), TB, 0, s>>>(hq.get(), n, R, L.R_pad, L.V, q.get());
+    k_import<T><<<nblk(n * L.R_pad), TB, 0, s>>>(hp.get(), n, R, L.R_pad, L.V, pm.get());
+    VXQ_CHECK_LAUNCH();
+    Operator<T> op;
+    op.indptr = ip.get();
+    op.indices = ix.get();
+    op.data = pick<T>(dv.get(), dv32.get());
+    op.sign = (T)1;
+    std::vector<double> sched(a_sched, a_sched + T_);
+    int64_t launches = 0;
+    T* qf = nullptr;
+    int req = opts ? opts->path : 0;
+    sbm_run_core<T>(nullptr, L, op, pick<T>(gv.get(), gv32.get()), sched, dt, a0, c0, q_cap, req,
+                    nnz, q.get(), q2.get(), pm.get(), nullptr, launches, s, &qf);
+    k_export<T><<<nblk(n * R), TB, 0, s>>>(qf, n, R, L.R_pad, L.V, hq.get());
+    k_export<T><<<nblk(n * R), TB, 0, s>>>(pm.get(), n, R, L.R_pad, L.V, hp.get());
+    VXQ_CHECK_LAUNCH();
+    VXQ_CUDA(cudaMemcpyAsync(Q, hq.get(), n * R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    VXQ_CUDA(cudaMemcpyAsync(P, hp.get(), n * R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    VXQ_CUDA(cudaStreamSynchronize(s));
+}
+}  // namespace
+
+void sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indices,
+                   const double* bt_data, const double* g, int64_t R, double* Q, double* P,
+                   const double* a_sched, int64_t T_, double dt, double a0, double c0,
+                   double q_cap, const vxq_run_opts* opts, cudaStream_t s) {
+    if (opts && opts->precision == VXQ_FP64)
+        integrate_t<double>(n, bt_indptr, bt_indices, bt_data, g, R, Q, P, a_sched, T_, dt, a0,
+                            c0, q_cap, opts, s);
+    else
+        integrate_t<float>(n, bt_indptr, bt_indices, bt_data, g, R, Q, P, a_sched, T_, dt, a0,
+                           c0, q_cap, opts, s);
+}
+
+}  // namespace vxq

@@ -1,0 +1,588 @@
+// problem.cu -- device-resident Ising problem: symmetric CSR build, lambda0, c0.
+//
+// Replaces IsingModel.coupling_operator()/_csr (model.py:166-192),
+// field_scale (model.py:194-200) and resolve_c0/eig_extreme (bifurcation.py:25-34,
+// solvers/eigen.py:35-56).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "vxq_internal.h"
+
+namespace vxq {
+
+Problem::~Problem() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    void* ptrs[] = {indptr, indices, data64, data32, lower_count, h64, h32, g64,
+                    g32,    coo_i,   coo_j,  coef_fx, h_fx};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    extern void dense_destroy(DenseOperand*);
+    if (dense) dense_destroy(dense);
+    cudaSetDevice(prev);
+}
+
+namespace {
+
+__global__ void k_validate_coo(int64_t n, int64_t m, const int64_t* rows, const int64_t* cols,
+                               const double* values, int* err) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    int64_t i = rows[k], j = cols[k];
+    int e = 0;
+    if (!(i >= 0 && i < j && j < n)) e |= 1;
+    if (k > 0) {
+        int64_t pi = rows[k - 1], pj = cols[k - 1];
+        if (!(pi < i || (pi == i && pj < j))) e |= 2;
+    }
+    if (!isfinite(values[k])) e |= 4;
+    if (e) atomicOr(err, e);
+}
+
+__global__ void k_count_deg(int64_t m, const int64_t* rows, const int64_t* cols, int32_t* deg_up,
+                            int32_t* deg_lo, int32_t* ci, int32_t* cj) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    int32_t i = (int32_t)rows[k], j = (int32_t)cols[k];
+    atomicAdd(deg_up + i, 1);
+    atomicAdd(deg_lo + j, 1);
+    ci[k] = i;
+    cj[k] = j;
+}
+
+__global__ void k_row_total(int64_t n, const int32_t* up, const int32_t* lo, int64_t* tot) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) tot[i] = (int64_t)up[i] + lo[i];
+    if (i == n) tot[i] = 0;
+}
+
+__global__ void k_iota(int64_t m, int32_t* v) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < m) v[k] = (int32_t)k;
+}
+
+// upper part of row i: COO range in order -> after the lower part
+__global__ void k_fill_upper(int64_t m, const int32_t* ci, const int32_t* cj, const double* val,
+                             const int64_t* indptr, const int32_t* deg_lo,
+                             const int64_t* ustart, int32_t* indices, double* data) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    int32_t i = ci[k];
+    int64_t pos = indptr[i] + deg_lo[i] + (k - ustart[i]);
+    indices[pos] = cj[k];
+    data[pos] = val[k];
+}
+
+// lower part of row c: stable-sorted by column -> ascending row index
+__global__ void k_fill_lower(int64_t m, const int32_t* sorted_cols, const int32_t* perm,
+                             const int32_t* ci, const double* val, const int64_t* indptr,
+                             const int64_t* lstart, int32_t* indices, double* data) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    int32_t c = sorted_cols[p];
+    int32_t k = perm[p];
+    int64_t pos = indptr[c] + (p - lstart[c]);
+    indices[pos] = ci[k];
+    data[pos] = val[k];
+}
+
+__global__ void k_convert(int64_t nnz, const double* d64, float* d32) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < nnz) d32[k] = __double2float_rn(d64[k]);
+}
+
+__global__ void k_fields(int64_t n, const double* h, float* h32, double* g64, float* g32) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v = h[i];
+    h32[i] = __double2float_rn(v);
+    g64[i] = -v;
+    g32[i] = -__double2float_rn(v);
+}
+
+__global__ void k_abs_minmax(int64_t m, const double* v, unsigned long long* mn,
+                             unsigned long long* mx) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v[k]));
+    atomicMin(mn, b);
+    atomicMax(mx, b);
+}
+
+// ---- exact fixed-point encoding of coefficients ----
+// value = mant * 2^e with mant a 53-bit integer; lowest/highest set bit exponents.
+__device__ __forceinline__ bool decompose(double v, uint64_t& mant, int& e) {
+    uint64_t b = (uint64_t)__double_as_longlong(v);
+    int E = (int)((b >> 52) & 0x7ff);
+    mant = b & ((1ULL << 52) - 1);
+    if (E == 0) {
+        e = -1074;
+    } else {
+        mant |= (1ULL << 52);
+        e = E - 1075;
+    }
+    return mant != 0;
+}
+
+__global__ void k_exp_range(int64_t cnt, const double* v, int* lo, int* hi) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    uint64_t mant;
+    int e;
+    if (!decompose(v[k], mant, e)) return;
+    int low = e + (__ffsll((long long)mant) - 1);
+    int high = e + (63 - __clzll((long long)mant));
+    atomicMin(lo, low);
+    atomicMax(hi, high);
+}
+
+__device__ void encode_fx(double v, int e_low, int L, uint32_t* out) {
+    uint64_t mant;
+    int e;
+    uint32_t limb[kMaxLimbs + 3];
+    for (int q = 0; q < L; ++q) limb[q] = 0;
+    if (decompose(v, mant, e)) {
+        int s = e - e_low;  // >= 0
+        int q0 = s >> 5, sh = s & 31;
+        // mant << sh spans up to 85 bits -> 3 limbs
+        unsigned __int128 w = ((unsigned __int128)mant) << sh;
+        for (int t = 0; t < 3; ++t) {
+            int q = q0 + t;
+            if (q < L) limb[q] = (uint32_t)(w >> (32 * t));
+        }
+        if (v < 0) {  // two's complement negate over L limbs
+            uint64_t carry = 1;
+            for (int q = 0; q < L; ++q) {
+                uint64_t t = (uint64_t)(uint32_t)~limb[q] + carry;
+                limb[q] = (uint32_t)t;
+                carry = t >> 32;
+            }
+        }
+    }
+    for (int q = 0; q < L; ++q) out[q] = limb[q];
+}
+
+__global__ void k_encode(int64_t cnt, const double* v, int e_low, int L, uint32_t* out) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < cnt) encode_fx(v[k], e_low, L, out + k * L);
+}
+
+__global__ void k_encode_scalar(double v, int e_low, int L, uint32_t* out) {
+    encode_fx(v, e_low, L, out);
+}
+
+// field_scale: |h_i| + sum_{j>i asc} |J| + sum_{j<i asc} |J|  (np.add.at over rows, then cols)
+__global__ void k_field_scale(int64_t n, const int64_t* indptr, const int32_t* lower_count,
+                              const double* data, const double* h,
+                              unsigned long long* maxbits) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double acc = 0.0;
+    if (i < n) {
+        acc = fabs(h[i]);
+        int64_t b = indptr[i], mid = b + lower_count[i], e = indptr[i + 1];
+        for (int64_t k = mid; k < e; ++k) acc = __dadd_rn(acc, fabs(data[k]));
+        for (int64_t k = b; k < mid; ++k) acc = __dadd_rn(acc, fabs(data[k]));
+    }
+    // non-negative doubles order like their bit patterns
+    unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+        bits = other > bits ? other : bits;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(maxbits, bits);
+}
+
+constexpr int TB = 256;
+inline unsigned nblk(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, TB)); }
+
+__global__ void k_widen(int64_t n, const int32_t* a, int64_t* b) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+    if (i == n) b[i] = 0;
+}
+void widen_i32_i64(int64_t n, const int32_t* a, int64_t* b, cudaStream_t s) {
+    k_widen<<<nblk(n + 1), TB, 0, s>>>(n, a, b);
+    VXQ_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t* cols,
+                        const double* values, const double* h, double offset, int device) {
+    VXQ_REQUIRE(n >= 1, "model needs at least one variable");
+    VXQ_REQUIRE(n < (1LL << 31) - 1, "n must be < 2^31");
+    VXQ_REQUIRE(m >= 0 && m < (1LL << 31) - 1, "num_couplings must be in [0, 2^31)");
+    VXQ_REQUIRE(m == 0 || (rows && cols && values), "null coupling arrays");
+    VXQ_REQUIRE(std::isfinite(offset), "offset must be finite");
+    int ndev = 0;
+    VXQ_CUDA(cudaGetDeviceCount(&ndev));
+    VXQ_REQUIRE(device >= 0 && device < ndev, "invalid CUDA device ordinal");
+    VXQ_CUDA(cudaSetDevice(device));
+
+    Problem* P = new Problem();
+    try {
+        P->device = device;
+        P->n = n;
+        P->m = m;
+        P->nnz = 2 * m;
+        P->offset = offset;
+        cudaStream_t s;
+        VXQ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct SG {
+            cudaStream_t s;
+            ~SG() { cudaStreamDestroy(s); }
+        } sg{s};
+
+        const int64_t nnz = 2 * m;
+        VXQ_CUDA(cudaMalloc(&P->indptr, (n + 1) * sizeof(int64_t)));
+        VXQ_CUDA(cudaMalloc(&P->indices, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
+        VXQ_CUDA(cudaMalloc(&P->data64, std::max<int64_t>(nnz, 1) * sizeof(double)));
+        VXQ_CUDA(cudaMalloc(&P->data32, std::max<int64_t>(nnz, 1) * sizeof(float)));
+        VXQ_CUDA(cudaMalloc(&P->lower_count, n * sizeof(int32_t)));
+        VXQ_CUDA(cudaMalloc(&P->h64, n * sizeof(double)));
+        VXQ_CUDA(cudaMalloc(&P->h32, n * sizeof(float)));
+        VXQ_CUDA(cudaMalloc(&P->g64, n * sizeof(double)));
+        VXQ_CUDA(cudaMalloc(&P->g32, n * sizeof(float)));
+        VXQ_CUDA(cudaMalloc(&P->coo_i, std::max<int64_t>(m, 1) * sizeof(int32_t)));
+        VXQ_CUDA(cudaMalloc(&P->coo_j, std::max<int64_t>(m, 1) * sizeof(int32_t)));
+
+        // fields
+        if (h) {
+            VXQ_CUDA(cudaMemcpyAsync(P->h64, h, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        } else {
+            VXQ_CUDA(cudaMemsetAsync(P->h64, 0, n * sizeof(double), s));
+        }
+        k_fields<<<nblk(n), TB, 0, s>>>(n, P->h64, P->h32, P->g64, P->g32);
+        VXQ_CHECK_LAUNCH();
+
+        DevBuf<int32_t> deg_up(n, s), deg_lo(n, s);
+        DevBuf<int64_t> tot(n + 1, s), ustart(n + 1, s), lstart(n + 1, s), up64(n + 1, s),
+            lo64(n + 1, s);
+        VXQ_CUDA(cudaMemsetAsync(deg_up.get(), 0, n * sizeof(int32_t), s));
+        VXQ_CUDA(cudaMemsetAsync(deg_lo.get(), 0, n * sizeof(int32_t), s));
+        DevBuf<double> dval(std::max<int64_t>(m, 1), s);
+        DevBuf<int32_t> err(1, s);
+        VXQ_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(int), s));
+        if (m > 0) {
+            DevBuf<int64_t> drows(m, s), dcols(m, s);
+            VXQ_CUDA(cudaMemcpyAsync(drows.get(), rows, m * sizeof(int64_t),
+                                     cudaMemcpyHostToDevice, s));
+            VXQ_CUDA(cudaMemcpyAsync(dcols.get(), cols, m * sizeof(int64_t),
+                                     cudaMemcpyHostToDevice, s));
+            VXQ_CUDA(cudaMemcpyAsync(dval.get(), values, m * sizeof(double),
+                                     cudaMemcpyHostToDevice, s));
+            k_validate_coo<<<nblk(m), TB, 0, s>>>(n, m, drows.get(), dcols.get(), dval.get(),
+                                                  err.get());
+            VXQ_CHECK_LAUNCH();
+            int herr = 0;
+            VXQ_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+            VXQ_CUDA(cudaStreamSynchronize(s));
+            VXQ_REQUIRE(!(herr & 1), "couplings must satisfy 0 <= i < j < n");
+            VXQ_REQUIRE(!(herr & 2), "couplings must be sorted and unique by (i, j)");
+            VXQ_REQUIRE(!(herr & 4), "non-finite coupling value");
+            k_count_deg<<<nblk(m), TB, 0, s>>>(m, drows.get(), dcols.get(), deg_up.get(),
+                                               deg_lo.get(), P->coo_i, P->coo_j);
+            VXQ_CHECK_LAUNCH();
+        }
+        VXQ_CUDA(cudaMemcpyAsync(P->lower_count, deg_lo.get(), n * sizeof(int32_t),
+                                 cudaMemcpyDeviceToDevice, s));
+        k_row_total<<<nblk(n + 1), TB, 0, s>>>(n, deg_up.get(), deg_lo.get(), tot.get());
+        VXQ_CHECK_LAUNCH();
+        // scans (int32 degrees widened into int64 scans)
+        widen_i32_i64(n, deg_up.get(), up64.get(), s);
+        widen_i32_i64(n, deg_lo.get(), lo64.get(), s);
+        size_t tmp_bytes = 0, need = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, need, tot.get(), P->indptr, n + 1, s);
+        tmp_bytes = std::max(tmp_bytes, need);
+        cub::DeviceScan::ExclusiveSum(nullptr, need, up64.get(), ustart.get(), n + 1, s);
+        tmp_bytes = std::max(tmp_bytes, need);
+        DevBuf<int32_t> sorted_cols(std::max<int64_t>(m, 1), s), perm_in(std::max<int64_t>(m, 1), s),
+            perm(std::max<int64_t>(m, 1), s);
+        int end_bit = 1;
+        while ((1LL << end_bit) < n) ++end_bit;
+        if (m > 0) {
+            cub::DeviceRadixSort::SortPairs(nullptr, need, P->coo_j, sorted_cols.get(),
+                                            perm_in.get(), perm.get(), (int)m, 0, end_bit, s);
+            tmp_bytes = std::max(tmp_bytes, need);
+        }
+        DevBuf<uint8_t> tmp(std::max<size_t>(tmp_bytes, 1), s);
+        need = tmp_bytes;
+        VXQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), need, tot.get(), P->indptr, n + 1, s));
+        need = tmp_bytes;
+        VXQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), need, up64.get(), ustart.get(), n + 1, s));
+        need = tmp_bytes;
+        VXQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), need, lo64.get(), lstart.get(), n + 1, s));
+        if (m > 0) {
+            k_iota<<<nblk(m), TB, 0, s>>>(m, perm_in.get());
+            VXQ_CHECK_LAUNCH();
+            need = tmp_bytes;
+            VXQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), need, P->coo_j, sorted_cols.get(),
+                                                     perm_in.get(), perm.get(), (int)m, 0,
+                                                     end_bit, s));
+            k_fill_upper<<<nblk(m), TB, 0, s>>>(m, P->coo_i, P->coo_j, dval.get(), P->indptr,
+                                                deg_lo.get(), ustart.get(), P->indices,
+                                                P->data64);
+            VXQ_CHECK_LAUNCH();
+            k_fill_lower<<<nblk(m), TB, 0, s>>>(m, sorted_cols.get(), perm.get(), P->coo_i,
+                                                dval.get(), P->indptr, lstart.get(), P->indices,
+                                                P->data64);
+            VXQ_CHECK_LAUNCH();
+            k_convert<<<nblk(nnz), TB, 0, s>>>(nnz, P->data64, P->data32);
+            VXQ_CHECK_LAUNCH();
+        }
+        // max row length (dispatch heuristics)
+        {
+            DevBuf<int64_t> mx(1, s);
+            need = 0;
+            cub::DeviceReduce::Max(nullptr, need, tot.get(), mx.get(), n, s);
+            DevBuf<uint8_t> t2(std::max<size_t>(need, 1), s);
+            VXQ_CUDA(cub::DeviceReduce::Max(t2.get(), need, tot.get(), mx.get(), n, s));
+            VXQ_CUDA(cudaMemcpyAsync(&P->max_row_nnz, mx.get(), sizeof(int64_t),
+                                     cudaMemcpyDeviceToHost, s));
+        }
+        // uniform magnitude (+-c couplings, e.g. SK)
+        if (m > 0) {
+            DevBuf<unsigned long long> mm(2, s);
+            unsigned long long init[2] = {~0ULL, 0ULL};
+            VXQ_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
+            k_abs_minmax<<<nblk(m), TB, 0, s>>>(m, dval.get(), mm.get(), mm.get() + 1);
+            VXQ_CHECK_LAUNCH();
+            unsigned long long res[2];
+            VXQ_CUDA(cudaMemcpyAsync(res, mm.get(), sizeof(res), cudaMemcpyDeviceToHost, s));
+            VXQ_CUDA(cudaStreamSynchronize(s));
+            double a, b;
+            memcpy(&a, &res[0], 8);
+            memcpy(&b, &res[1], 8);
+            P->uniform_magnitude = (a == b) && a > 0;
+            P->magnitude = b;
+        }
+        // exact-energy encoding
+        {
+            DevBuf<int> rng(2, s);
+            int init[2] = {1 << 20, -(1 << 20)};
+            VXQ_CUDA(cudaMemcpyAsync(rng.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
+            if (m > 0) k_exp_range<<<nblk(m), TB, 0, s>>>(m, dval.get(), rng.get(), rng.get() + 1);
+            k_exp_range<<<nblk(n), TB, 0, s>>>(n, P->h64, rng.get(), rng.get() + 1);
+            DevBuf<double> doff(1, s);
+            VXQ_CUDA(cudaMemcpyAsync(doff.get(), &P->offset, sizeof(double),
+                                     cudaMemcpyHostToDevice, s));
+            k_exp_range<<<1, 1, 0, s>>>(1, doff.get(), rng.get(), rng.get() + 1);
+            VXQ_CHECK_LAUNCH();
+            int res[2];
+            VXQ_CUDA(cudaMemcpyAsync(res, rng.get(), sizeof(res), cudaMemcpyDeviceToHost, s));
+            VXQ_CUDA(cudaStreamSynchronize(s));
+            if (res[0] > res[1]) {  // all coefficients zero
+                res[0] = 0;
+                res[1] = 0;
+            }
+            P->e_low = res[0];
+            int span = res[1] - res[0] + 1;  // bits of the largest |coefficient|
+            int L = (span + 1 + 31) / 32 + (span % 32 > 29 ? 1 : 0);
+            L = std::max(L, 2);
+            if (L > kMaxLimbs) {
+                P->energy_ok = false;
+                L = kMaxLimbs;
+            }
+            P->limbs = L;
+            VXQ_CUDA(cudaMalloc(&P->coef_fx, std::max<int64_t>(m, 1) * L * sizeof(uint32_t)));
+            VXQ_CUDA(cudaMalloc(&P->h_fx, n * L * sizeof(uint32_t)));
+            if (P->energy_ok) {
+                if (m > 0) k_encode<<<nblk(m), TB, 0, s>>>(m, dval.get(), P->e_low, L, P->coef_fx);
+                k_encode<<<nblk(n), TB, 0, s>>>(n, P->h64, P->e_low, L, P->h_fx);
+                DevBuf<uint32_t> ofx(L, s);
+                k_encode_scalar<<<1, 1, 0, s>>>(P->offset, P->e_low, L, ofx.get());
+                VXQ_CHECK_LAUNCH();
+                VXQ_CUDA(cudaMemcpyAsync(P->offset_fx, ofx.get(), L * sizeof(uint32_t),
+                                         cudaMemcpyDeviceToHost, s));
+            }
+        }
+        VXQ_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+        delete P;
+        throw;
+    }
+    return P;
+}
+
+double problem_lambda0(Problem* p, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(p->mu);
+    if (!std::isnan(p->lambda0)) return p->lambda0;
+    DevBuf<unsigned long long> mx(1, s);
+    VXQ_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned long long), s));
+    k_field_scale<<<nblk(p->n), TB, 0, s>>>(p->n, p->indptr, p->lower_count, p->data64, p->h64,
+                                            mx.get());
+    VXQ_CHECK_LAUNCH();
+    unsigned long long bits = 0;
+    VXQ_CUDA(cudaMemcpyAsync(&bits, mx.get(), sizeof(bits), cudaMemcpyDeviceToHost, s));
+    VXQ_CUDA(cudaStreamSynchronize(s));
+    double fs;
+    memcpy(&fs, &bits, 8);
+    p->lambda0 = std::max(fs, 1e-12);  // parallel_annealing.py:25
+    return p->lambda0;
+}
+
+double problem_c0(Problem* p, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(p->mu);
+    if (!std::isnan(p->c0)) return p->c0;
+    double c0 = 1.0;  // bifurcation.py:31-34
+    if (p->m > 0) {
+        double lam = lanczos_lambda_max(p->n, p->indptr, p->indices, p->data64, -1.0, s);
+        c0 = lam > 1e-12 ? 1.0 / lam : 1.0;
+    }
+    p->c0 = c0;
+    return c0;
+}
+
+// ------------------------------------------------------------------ Lanczos
+namespace {
+
+// y = sign * A x (warp per row)
+__global__ void k_spmv(int64_t n, const int64_t* indptr, const int32_t* indices,
+                       const double* data, double sign, const double* x, double* y) {
+    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    double acc = 0.0;
+    for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32)
+        acc += data[k] * x[indices[k]];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[row] = sign * acc;
+}
+
+constexpr int RB = 512;  // reduction blocks (fixed => deterministic)
+
+__global__ void k_dot_partial(int64_t n, const double* a, const double* b, double* part) {
+    __shared__ double sh[TB];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)TB + threadIdx.x; i < n; i += (int64_t)TB * gridDim.x)
+        acc += a[i] * b[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = TB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void k_sum_partials(int nb, const double* part, double* out) {
+    __shared__ double sh[TB];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nb; i += TB) acc += part[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = TB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+// w = w - alpha v - beta vprev  (alpha, beta device scalars)
+__global__ void k_axpy2(int64_t n, double* w, const double* v, const double* vp,
+                        const double* alpha, const double* beta) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) w[i] = w[i] - (*alpha) * v[i] - (*beta) * vp[i];
+}
+
+__global__ void k_scale_into(int64_t n, const double* w, const double* nrm2, double* v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = w[i] / sqrt(*nrm2);
+}
+
+__global__ void k_start_vec(int64_t n, double* v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    U64x4 o = philox4x64_10((uint64_t)i + 1, 0, 0x5eed, 0, 0x1a2b3c4dULL, 0);
+    v[i] = uniform_from_raw(o.v[0], -1.0, 2.0);
+}
+
+// largest eigenvalue of the k x k symmetric tridiagonal (alpha, beta) by bisection
+__device__ int sturm_count(int k, const double* a, const double* b, double x) {
+    int c = 0;
+    double q = a[0] - x;
+    if (q < 0) ++c;
+    for (int i = 1; i < k; ++i) {
+        double d = (q == 0.0) ? 1e-300 : q;
+        q = a[i] - x - b[i - 1] * b[i - 1] / d;
+        if (q < 0) ++c;
+    }
+    return c;  // eigenvalues < x
+}
+
+__global__ void k_tridiag_max(int k, const double* a, const double* b, double* out) {
+    double lo = 1e300, hi = -1e300;
+    for (int i = 0; i < k; ++i) {
+        double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < k - 1 ? fabs(b[i]) : 0.0);
+        lo = fmin(lo, a[i] - r);
+        hi = fmax(hi, a[i] + r);
+    }
+    for (int it = 0; it < 200; ++it) {
+        double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        if (sturm_count(k, a, b, mid) >= k) hi = mid;  // all eigenvalues < mid
+        else lo = mid;
+    }
+    *out = hi;
+}
+
+}  // namespace
+
+double lanczos_lambda_max(int64_t n, const int64_t* indptr, const int32_t* indices,
+                          const double* data, double sign, cudaStream_t s) {
+    const int kmax = (int)std::min<int64_t>(n, 600);
+    DevBuf<double> v0(n, s), v1(n, s), w(n, s), part(RB, s), alpha(kmax + 1, s),
+        beta(kmax + 1, s), nrm(1, s), theta(1, s);
+    double* vp = v0.get();
+    double* v = v1.get();
+    VXQ_CUDA(cudaMemsetAsync(vp, 0, n * sizeof(double), s));
+    VXQ_CUDA(cudaMemsetAsync(beta.get(), 0, (kmax + 1) * sizeof(double), s));
+    k_start_vec<<<nblk(n), TB, 0, s>>>(n, w.get());
+    k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get());
+    k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), nrm.get());
+    k_scale_into<<<nblk(n), TB, 0, s>>>(n, w.get(), nrm.get(), v);
+    VXQ_CHECK_LAUNCH();
+    DevBuf<double> zero(1, s);
+    VXQ_CUDA(cudaMemsetAsync(zero.get(), 0, sizeof(double), s));
+    double prev_theta = NAN, th = 0.0;
+    int k = 0;
+    const unsigned spmv_blocks = (unsigned)ceil_div(n * 32, TB);
+    for (k = 0; k < kmax; ++k) {
+        k_spmv<<<spmv_blocks, TB, 0, s>>>(n, indptr, indices, data, sign, v, w.get());
+        k_dot_partial<<<RB, TB, 0, s>>>(n, v, w.get(), part.get());
+        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), alpha.get() + k);
+        k_axpy2<<<nblk(n), TB, 0, s>>>(n, w.get(), v, vp, alpha.get() + k,
+                                       k > 0 ? beta.get() + k - 1 : zero.get());
+        k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get());
+        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), nrm.get());
+        VXQ_CHECK_LAUNCH();
+        double h_nrm2 = 0;
+        VXQ_CUDA(cudaMemcpyAsync(&h_nrm2, nrm.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+        VXQ_CUDA(cudaStreamSynchronize(s));
+        double bk = std::sqrt(h_nrm2);
+        VXQ_CUDA(cudaMemcpyAsync(beta.get() + k, &bk, sizeof(double), cudaMemcpyHostToDevice, s));
+        bool last = (k + 1 == kmax) || !(bk > 1e-12);
+        if (last || (k + 1) % 10 == 0) {
+            k_tridiag_max<<<1, 1, 0, s>>>(k + 1, alpha.get(), beta.get(), theta.get());
+            VXQ_CHECK_LAUNCH();
+            VXQ_CUDA(cudaMemcpyAsync(&th, theta.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+            VXQ_CUDA(cudaStreamSynchronize(s));
+            if (last) break;
+            if (!std::isnan(prev_theta) &&
+                std::fabs(th - prev_theta) <= 1e-13 * std::max(1.0, std::fabs(th)))
+                break;
+            prev_theta = th;
+        }
+        // v_{k+1} = w / beta_k ; rotate
+        std::swap(vp, v);  // vp <- v_k
+        k_scale_into<<<nblk(n), TB, 0, s>>>(n, w.get(), nrm.get(), v);
+        VXQ_CHECK_LAUNCH();
+    }
+    VXQ_CUDA(cudaStreamSynchronize(s));
+    return th;
+}
+
+}  // namespace vxq

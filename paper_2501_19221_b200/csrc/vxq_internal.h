@@ -1,0 +1,135 @@
+// vxq_internal.h -- internal types shared by the vxq translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <mutex>
+#include <vector>
+
+#include "vxq_common.cuh"
+
+namespace vxq {
+
+// Maximum 32-bit limbs of the exact fixed-point energy accumulator.
+constexpr int kMaxLimbs = 8;
+
+struct DenseOperand;  // dense tcgen05 path (dense_tc.cu)
+
+// A device-resident Ising problem (the reference's IsingModel, model.py:113-200).
+struct Problem {
+    int device = 0;
+    int64_t n = 0, m = 0, nnz = 0;
+    double offset = 0.0;
+
+    // symmetric coupling CSR, ascending columns per row (both triangles, zero diagonal)
+    int64_t* indptr = nullptr;     // [n+1]
+    int32_t* indices = nullptr;    // [nnz]
+    double* data64 = nullptr;      // [nnz]
+    float* data32 = nullptr;       // [nnz]
+    int32_t* lower_count = nullptr;  // [n] entries with j < i in row i
+    double* h64 = nullptr;         // [n]
+    float* h32 = nullptr;          // [n]
+    double* g64 = nullptr;         // [n]  -h  (SBM drive, bifurcation.py:57)
+    float* g32 = nullptr;          // [n]
+    int32_t* coo_i = nullptr;      // [m] couplings i<j (energy evaluation)
+    int32_t* coo_j = nullptr;      // [m]
+
+    // exact energy: every coefficient as an L-limb two's-complement integer * 2^e_low
+    int limbs = 0;
+    int e_low = 0;
+    uint32_t* coef_fx = nullptr;   // [m][limbs]
+    uint32_t* h_fx = nullptr;      // [n][limbs]
+    uint32_t offset_fx[kMaxLimbs] = {0};
+    bool energy_ok = true;         // false if the dynamic range exceeds kMaxLimbs*32 bits
+
+    int64_t max_row_nnz = 0;
+    bool uniform_magnitude = false;  // all |J_ij| equal (e.g. SK +-1/sqrt(N))
+    double magnitude = 0.0;
+
+    std::mutex mu;  // guards the lazy caches below
+    double lambda0 = NAN;
+    double c0 = NAN;
+    DenseOperand* dense = nullptr;
+
+    ~Problem();
+};
+
+// run-scoped stream holder
+struct StreamScope {
+    cudaStream_t s = nullptr;
+    bool owned = false;
+    explicit StreamScope(void* user) {
+        if (user) {
+            s = (cudaStream_t)user;
+        } else {
+            VXQ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            owned = true;
+        }
+    }
+    ~StreamScope() {
+        if (owned && s) cudaStreamDestroy(s);
+    }
+};
+
+// stream-ordered device buffer
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t count = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t n, cudaStream_t st) : count(n), s(st) {
+        if (n) VXQ_CUDA(cudaMallocAsync((void**)&p, n * sizeof(T), st));
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count), s(o.s) { o.p = nullptr; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        release();
+        p = o.p; count = o.count; s = o.s; o.p = nullptr;
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+    }
+    T* get() const { return p; }
+};
+
+// ---- problem.cu
+Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t* cols,
+                        const double* values, const double* h, double offset, int device);
+double problem_lambda0(Problem* p, cudaStream_t s);
+double problem_c0(Problem* p, cudaStream_t s);
+// Lanczos lambda_max of the operator w_ij = sign * data[k] (row i lists field weights)
+double lanczos_lambda_max(int64_t n, const int64_t* indptr, const int32_t* indices,
+                          const double* data, double sign, cudaStream_t s);
+
+// ---- energy.cu
+// energies of bit-packed spins sb[n][W] (bit (r%32) of word r/32) for replicas r < R
+void energies_from_bits(Problem* p, const uint32_t* sb, int64_t W, int64_t R,
+                        double* energies_dev, cudaStream_t s);
+void pack_states_to_bits(const int8_t* states_dev, int64_t n, int64_t R, int64_t W,
+                         uint32_t* sb, cudaStream_t s);
+void bits_to_states(const uint32_t* sb, int64_t n, int64_t R, int64_t W, int8_t* states_dev,
+                    cudaStream_t s);
+void stable_order(const double* energies_dev, int64_t R, int64_t* order_dev, cudaStream_t s);
+
+// ---- dynamics.cu
+void pa_solve(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, vxq_outputs* out,
+              cudaStream_t s);
+void sbm_solve(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts,
+               vxq_outputs* out, cudaStream_t s);
+void sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indices,
+                   const double* bt_data, const double* g, int64_t R, double* Q, double* P,
+                   const double* a_sched, int64_t T_, double dt, double a0, double c0,
+                   double q_cap, const vxq_run_opts* opts, cudaStream_t s);
+
+// ---- host schedules (bit-exact with the reference's Python expressions)
+void pa_schedule(double lam0, int64_t T, double* out);   // lam0 * (1.0 - t / T)
+void sbm_schedule(double a0, int64_t T, double* out);    // np.linspace(0.0, a0, T)
+
+}  // namespace vxq

@@ -1,0 +1,125 @@
+"""Device-resident problems: one ``vxq_problem`` per (model object, device).
+
+The reference caches its coupling operator on the frozen model
+(``cached_property _matrix/_csr``, model.py:166-183); here the device CSR and
+the exact-energy encoding are cached the same way, keyed on model identity, and
+released when the model is garbage collected.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .errors import ValidationError
+
+_cache: dict[tuple[int, int], "DeviceProblem"] = {}
+_cache_lock = threading.Lock()
+
+
+class DeviceProblem:
+    """Owns one vxq_problem handle."""
+
+    def __init__(self, model, device: int = 0):
+        L = _lib.load()
+        _lib.require_gpu()
+        n = int(model.n)
+        rows = np.ascontiguousarray(model.rows, dtype=np.int64)
+        cols = np.ascontiguousarray(model.cols, dtype=np.int64)
+        vals = np.ascontiguousarray(model.values, dtype=np.float64)
+        h = np.ascontiguousarray(model.h, dtype=np.float64)
+        if h.shape != (n,):
+            raise ValidationError(f"field vector has shape {h.shape}, expected ({n},)")
+        handle = ctypes.c_void_p()
+        _lib.check(L.vxq_problem_create(n, int(vals.shape[0]), _lib.ptr(rows), _lib.ptr(cols),
+                                        _lib.ptr(vals), _lib.ptr(h), float(model.offset),
+                                        int(device), ctypes.byref(handle)))
+        self.handle = handle
+        self.n = n
+        self.device = device
+        self._finalizer = weakref.finalize(self, L.vxq_problem_destroy, handle)
+
+    def info(self) -> dict:
+        out = np.zeros(5, dtype=np.int64)
+        _lib.check(_lib.load().vxq_problem_info(self.handle, _lib.ptr(out)))
+        return {"n": int(out[0]), "num_couplings": int(out[1]), "nnz": int(out[2]),
+                "max_row_nnz": int(out[3]), "uniform_magnitude": bool(out[4])}
+
+    def lambda0(self) -> float:
+        v = ctypes.c_double()
+        _lib.check(_lib.load().vxq_problem_lambda0(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def c0(self) -> float:
+        v = ctypes.c_double()
+        _lib.check(_lib.load().vxq_problem_c0(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def close(self):
+        self._finalizer()
+
+
+def get_problem(model, device: int = 0, cache: bool = True) -> DeviceProblem:
+    if not cache:
+        return DeviceProblem(model, device)
+    key = (id(model), device)
+    with _cache_lock:
+        dp = _cache.get(key)
+        if dp is not None:
+            return dp
+    dp = DeviceProblem(model, device)
+    with _cache_lock:
+        existing = _cache.get(key)
+        if existing is not None:
+            dp.close()
+            return existing
+        _cache[key] = dp
+    try:
+        weakref.finalize(model, _drop, key)
+    except TypeError:  # model type without weakref support: keep until clear_cache()
+        pass
+    return dp
+
+
+def _drop(key):
+    with _cache_lock:
+        dp = _cache.pop(key, None)
+    if dp is not None:
+        dp.close()
+
+
+def clear_cache(model=None):
+    """Release cached device problems (all, or those of one model)."""
+    with _cache_lock:
+        keys = [k for k in _cache if model is None or k[0] == id(model)]
+        dps = [_cache.pop(k) for k in keys]
+    for dp in dps:
+        dp.close()
+
+
+def energies(model, states, device: int = 0) -> np.ndarray:
+    """Exact energies of (R, n) spin states on the GPU (vxq_energies)."""
+    S = np.asarray(states)
+    if S.ndim == 1:
+        S = S[None, :]
+    if S.ndim != 2 or S.shape[1] != model.n:
+        raise ValidationError(f"states must have shape (R, {model.n}), got {S.shape}")
+    S = np.ascontiguousarray(np.where(S >= 0, 1, -1).astype(np.int8))
+    dp = get_problem(model, device)
+    out = np.empty(S.shape[0], dtype=np.float64)
+    opts = _lib.RunOptsC()
+    _lib.check(_lib.load().vxq_energies(dp.handle, _lib.ptr(S), S.shape[0], _lib.ptr(out),
+                                        ctypes.byref(opts)))
+    return out
+
+
+def lambda0(model, device: int = 0) -> float:
+    return get_problem(model, device).lambda0()
+
+
+def c0(model, device: int = 0) -> float:
+    return get_problem(model, device).c0()

@@ -1,0 +1,117 @@
+"""Synthetic instances of the BASELINE.json configurations (seeded, vectorised).
+
+These build canonical ``IsingModel`` arrays directly (sorted unique i<j COO), which is
+what the reference's ``from_terms`` would produce (model.py:81-104) without its
+O(terms) Python dict.  Used by bench.py and the tests.
+
+  cfg1  dense random QUBO N=100 on all i<=j pairs, Q ~ U[-1,1] (drawn like gen_random,
+        generators.py:321-323) -> qubo_to_ising (transforms.py:36-56)
+  cfg2  Sherrington-Kirkpatrick N=10^4: J_ij = +-1/sqrt(N) i.i.d., h = 0
+  cfg3  Pegasus-like N=5640 with 40,484 couplers (P16 fabric counts), J, h ~ U[-1,1].
+        The reference ships no Pegasus generator; this is a random graph
+        with P16's node and edge counts, not the Pegasus topology itself.
+  cfg4  3-regular MaxCut N=10^6 (configuration model, loops/multi-edges dropped),
+        J = +1, h = 0: minimising sum s_i s_j maximises the cut, cut = (|E| - H) / 2
+  cfg5  random QUBO, mean degree 6, diagonal and off-diagonal ~ U[-1,1] -> Ising
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .model import IsingModel, QuboModel
+from .transforms import qubo_to_ising
+
+
+def _philox(seed, index=0):
+    bits = np.random.Philox(key=np.uint64(seed))
+    if index:
+        bits = bits.jumped(index)
+    return np.random.Generator(bits)
+
+
+def cfg1_qubo(seed: int = 2501, n: int = 100) -> tuple[QuboModel, IsingModel]:
+    rng = _philox(seed)
+    iu, ju = np.triu_indices(n, 0)
+    vals = rng.uniform(-1.0, 1.0, size=len(iu))
+    q = QuboModel(n=n, rows=iu.astype(np.int64), cols=ju.astype(np.int64), values=vals + 0.0)
+    return q, qubo_to_ising(q)
+
+
+def sk(n: int = 10_000, seed: int = 2) -> IsingModel:
+    rng = np.random.default_rng(seed)
+    iu, ju = np.triu_indices(n, 1)
+    J = np.where(rng.random(len(iu)) < 0.5, -1.0, 1.0) / np.sqrt(n)
+    return IsingModel(n=n, h=np.zeros(n), rows=iu.astype(np.int64), cols=ju.astype(np.int64),
+                      values=J)
+
+
+def random_edges(n: int, m: int, seed: int):
+    rng = np.random.default_rng(seed)
+    keys = np.zeros(0, dtype=np.int64)
+    while keys.size < m:
+        a = rng.integers(0, n, 2 * (m - keys.size) + 16)
+        b = rng.integers(0, n, a.size)
+        lo, hi = np.minimum(a, b), np.maximum(a, b)
+        k = (lo * n + hi)[lo != hi]
+        keys = np.unique(np.concatenate([keys, k]))
+    keys = np.sort(rng.choice(keys, m, replace=False))
+    return keys // n, keys % n
+
+
+def pegasus_like(n: int = 5640, m: int = 40_484, seed: int = 16) -> IsingModel:
+    r, c = random_edges(n, m, seed)
+    rng = _philox(seed)
+    J = rng.uniform(-1.0, 1.0, m)
+    h = rng.uniform(-1.0, 1.0, n)
+    return IsingModel(n=n, h=h, rows=r, cols=c, values=J + 0.0)
+
+
+def maxcut3(n: int = 1_000_000, seed: int = 4) -> IsingModel:
+    rng = np.random.default_rng(seed)
+    stubs = np.repeat(np.arange(n, dtype=np.int64), 3)
+    rng.shuffle(stubs)
+    a, b = stubs[0::2], stubs[1::2]
+    lo, hi = np.minimum(a, b), np.maximum(a, b)
+    keep = lo != hi
+    key = np.unique(lo[keep] * n + hi[keep])
+    return IsingModel(n=n, h=np.zeros(n), rows=key // n, cols=key % n,
+                      values=np.ones(key.size))
+
+
+def random_qubo_deg6(n: int, seed: int = 5) -> IsingModel:
+    r, c = random_edges(n, 3 * n, seed)
+    rng = _philox(seed)
+    off = rng.uniform(-1.0, 1.0, r.size)
+    diag = rng.uniform(-1.0, 1.0, n)
+    rows = np.concatenate([r, np.arange(n)])
+    cols = np.concatenate([c, np.arange(n)])
+    vals = np.concatenate([off, diag])
+    order = np.lexsort((cols, rows))
+    q = QuboModel(n=n, rows=rows[order], cols=cols[order], values=vals[order] + 0.0)
+    return qubo_to_ising(q)
+
+
+CONFIGS = {
+    "cfg1": dict(desc="dense random QUBO N=100 -> Ising, R=64, T=1000", R=64, T=1000),
+    "cfg2": dict(desc="dense Sherrington-Kirkpatrick N=10^4 (J=+-1/sqrt N), R=1024, T=1000",
+                 R=1024, T=1000),
+    "cfg3": dict(desc="Pegasus-like N=5640 (40,484 couplers, P16 counts), R=4096, T=1000",
+                 R=4096, T=1000),
+    "cfg4": dict(desc="3-regular MaxCut N=10^6, R=256, T=1000", R=256, T=1000),
+    "cfg5": dict(desc="random QUBO N=2x10^8 mean degree 6, R=32", R=32, T=100),
+}
+
+
+def build(name: str, n: int | None = None) -> IsingModel:
+    if name == "cfg1":
+        return cfg1_qubo()[1]
+    if name == "cfg2":
+        return sk(n or 10_000)
+    if name == "cfg3":
+        return pegasus_like()
+    if name == "cfg4":
+        return maxcut3(n or 1_000_000)
+    if name == "cfg5":
+        return random_qubo_deg6(n or 200_000_000)
+    raise KeyError(name)

@@ -1,0 +1,99 @@
+"""The C-ABI boundary: libvxq.so loads, exports every symbol include/vxq.h declares,
+host-only entry points are bit-exact with the reference, and the product path fails
+loudly (no CPU fallback) without a GPU.  CPU only."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2501_19221_b200 as vxq
+from paper_2501_19221_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "vxq.h")).read()
+    return sorted(set(re.findall(r"VXQ_API\s+[\w\s\*]+?\b(vxq_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.load()
+    syms = declared_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+    assert L.vxq_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    # field order / sizes of the ctypes mirrors (x86-64 SysV)
+    assert ctypes.sizeof(_lib.PaParamsC) == 48
+    assert ctypes.sizeof(_lib.SbmParamsC) == 64
+    assert ctypes.sizeof(_lib.RunOptsC) == 32
+    assert ctypes.sizeof(_lib.OutputsC) == 80
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 10, 999, 1000, 10_000])
+@pytest.mark.parametrize("a0", [1.0, 0.3, 7.77, 1e-300])
+def test_sbm_schedule_is_numpy_linspace(T, a0):
+    assert np.array_equal(vxq.sbm_schedule(a0, T), np.linspace(0.0, a0, T))
+
+
+@pytest.mark.parametrize("T", [1, 7, 1000, 4096])
+@pytest.mark.parametrize("lam0", [7.0, 0.3635822054430425, 1e-12, 123.456])
+def test_pa_schedule_is_reference_expression(T, lam0):
+    ref = np.array([lam0 * (1.0 - t / T) for t in range(T)])
+    assert np.array_equal(vxq.pa_schedule(lam0, T), ref)
+
+
+def test_no_cpu_fallback_without_gpu():
+    if _lib.device_count() > 0:
+        pytest.skip("GPU present")
+    m = vxq.IsingModel.from_terms(2, couplings=[(0, 1, -1.0)])
+    with pytest.raises(vxq.QubokitError):
+        vxq.solve_pa(m, vxq.PaParams(steps=10, replicas=2))
+    with pytest.raises(vxq.QubokitError):
+        vxq.solve_sbm(m, vxq.SbmParams(steps=10, replicas=2))
+    with pytest.raises(vxq.QubokitError):
+        m.energies(np.ones((1, 2), dtype=np.int8))
+
+
+def test_c_layer_reports_errors_without_gpu():
+    if _lib.device_count() > 0:
+        pytest.skip("GPU present")
+    L = _lib.load()
+    h = ctypes.c_void_p()
+    rows = np.array([0], dtype=np.int64)
+    cols = np.array([1], dtype=np.int64)
+    vals = np.array([1.0])
+    hv = np.zeros(2)
+    rc = L.vxq_problem_create(2, 1, _lib.ptr(rows), _lib.ptr(cols), _lib.ptr(vals),
+                              _lib.ptr(hv), 0.0, 0, ctypes.byref(h))
+    assert rc != 0 and L.vxq_last_error()
+
+
+def test_params_validation_before_the_call():
+    with pytest.raises(vxq.ValidationError):
+        vxq.PaParams(momentum=1.0).validate()
+    with pytest.raises(vxq.ValidationError):
+        vxq.SbmParams(dt=-0.1).validate()
+    with pytest.raises(vxq.ValidationError):
+        vxq.PaParams(steps=0).validate()
+    with pytest.raises(vxq.ValidationError):
+        vxq.params_from_dict("pa", {"stepz": 3})
+    p = vxq.PaParams(steps=123, learning_rate=0.07, seed=5)
+    assert vxq.params_from_dict("pa", vxq.params_to_dict(p)) == p
+    q = vxq.SbmParams(steps=10, dt=0.2, c0=0.5)
+    assert vxq.params_from_dict("sbm", vxq.params_to_dict(q)) == q
+    # model validation (model.py:81-104)
+    with pytest.raises(vxq.ValidationError):
+        vxq.IsingModel.from_terms(3, couplings=[(1, 1, 2.0)])
+    with pytest.raises(vxq.ValidationError):
+        vxq.IsingModel.from_terms(3, couplings=[(0, 5, 2.0)])
+    with pytest.raises(vxq.ValidationError):
+        vxq.IsingModel.from_terms(0)

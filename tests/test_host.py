@@ -1,0 +1,65 @@
+"""Host logic on CPU: QUBO-in conversion, canonicalisation, spin maps, SampleSet assembly."""
+
+import numpy as np
+import pytest
+
+import paper_2501_19221_b200 as vxq
+from helpers import model_from_golden
+
+
+def test_qubo_to_ising_bitexact_with_reference(golden):
+    q = vxq.QuboModel(n=int(golden["cfg1_n"]), rows=golden["cfg1_qubo_rows"],
+                      cols=golden["cfg1_qubo_cols"], values=golden["cfg1_qubo_values"])
+    m = vxq.qubo_to_ising(q)
+    ref = model_from_golden(golden, "cfg1")
+    for f in ("rows", "cols", "values", "h"):
+        assert np.array_equal(getattr(m, f), getattr(ref, f)), f
+    assert m.offset == ref.offset
+
+
+def test_qubo_ising_energy_identity_small():
+    # all 2^8 states: QUBO energy == Ising energy (transforms.py:36-41)
+    rng = np.random.default_rng(4)
+    n = 8
+    iu, ju = np.triu_indices(n, 0)
+    q = vxq.QuboModel.from_arrays(n, iu, ju, rng.uniform(-1, 1, len(iu)), offset=0.25)
+    m = vxq.qubo_to_ising(q)
+    bits = ((np.arange(2 ** n)[:, None] >> np.arange(n)) & 1).astype(np.float64)
+    Eq = (bits[:, q.rows] * bits[:, q.cols]) @ q.values + q.offset
+    S = 2 * bits - 1
+    Ei = (S[:, m.rows] * S[:, m.cols]) @ m.values + S @ m.h + m.offset
+    assert np.allclose(Eq, Ei, atol=1e-12)
+
+
+def test_canonical_pairs_sums_duplicates_in_order():
+    m = vxq.IsingModel.from_terms(4, couplings=[(2, 0, 0.1), (0, 2, 0.2), (1, 3, -1.0),
+                                                (0, 2, 0.3)])
+    assert m.rows.tolist() == [0, 1] and m.cols.tolist() == [2, 3]
+    assert m.values[0] == (0.0 + 0.1 + 0.2) + 0.3
+    assert not m.values.flags.writeable
+
+
+def test_spin_maps():
+    s = np.array([1, -1, 1])
+    assert vxq.spins_to_bits(s).tolist() == [1, 0, 1]
+    assert vxq.bits_to_spins([1, 0, 1]).tolist() == [1, -1, 1]
+    assert vxq.sign_pm(np.array([0.0, -0.0, -1e-300, 2.0])).tolist() == [1, 1, -1, 1]
+    with pytest.raises(vxq.ValidationError):
+        vxq.as_spins([0, 1])
+
+
+def test_sampleset_assembly_is_stable_best_first():
+    from paper_2501_19221_b200.solvers import RunResult, sampleset_from
+    E = np.array([1.0, -2.0, 1.0, -2.0, 0.5])
+    order = np.argsort(E, kind="stable")
+    st = np.arange(10, dtype=np.int8).reshape(5, 2)
+    ss = sampleset_from(RunResult(st, E, order, None, None, {}), 5, 7, 0.1, replica_begin=0)
+    assert [s.replica for s in ss.samples] == [1, 3, 4, 0, 2]
+    assert ss.best.energy == -2.0 and len(ss) == 5 and ss.seed == 7
+    assert np.all(np.diff(ss.energies()) >= 0)
+
+
+def test_replica_streams_match_reference_layout():
+    g = vxq.replica_streams(123, 3)
+    bg = np.random.Philox(key=np.uint64(123)).jumped(2)
+    assert np.array_equal(g[2].uniform(-1, 1, 5), np.random.Generator(bg).uniform(-1, 1, 5))
