@@ -210,8 +210,3 @@ int vxq_energies(vxq_problem* p, const int8_t* states, int64_t R, double* energi
 }
 
 }  // extern "C"
-
-namespace vxq {
-struct DenseOperand {};
-void dense_destroy(DenseOperand* d) { delete d; }
-}  // namespace vxq

@@ -622,10 +622,24 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     const T* h = pick<T>(p->h64, p->h32);
     int RG = resident_rg(L);
     size_t smem = resident_smem_pa(L, RG, sizeof(T));
-    int path = choose_path(opts ? opts->path : 0, L, smem, p->nnz);
+    const int req = opts ? opts->path : 0;
+    int path = VXQ_PATH_DENSE;
+    if constexpr (sizeof(T) == 8) {
+        if (req == VXQ_PATH_DENSE)
+            throw Error(VXQ_ERR_UNSUPPORTED, "dense tensor-core path is fp32 only");
+    }
+    const bool dense = sizeof(T) == 4 && (req == VXQ_PATH_DENSE ||
+                                          (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+    if (!dense) path = choose_path(req, L, smem, p->nnz);
     EventTimer tm(s);
     const uint32_t* sb_final = nullptr;
-    if (path == VXQ_PATH_RESIDENT) {
+    if (dense) {
+        if constexpr (sizeof(T) == 4) {
+            dense_pa_loop(p, R, L.R_pad, L.V, L.W, sched, eta, alpha, prm->seed, rbegin,
+                          x.get(), m.get(), sbA.get(), s, &out->loop_ms, &launches);
+        }
+        sb_final = sbA.get();
+    } else if (path == VXQ_PATH_RESIDENT) {
         DevBuf<T> ds(std::max<int64_t>(T_, 1), s);
         std::vector<T> st(T_);
         for (int64_t t = 0; t < T_; ++t) st[t] = (T)sched[t];

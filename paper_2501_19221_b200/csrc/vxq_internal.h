@@ -128,6 +128,13 @@ void sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indice
                    const double* a_sched, int64_t T_, double dt, double a0, double c0,
                    double q_cap, const vxq_run_opts* opts, cudaStream_t s);
 
+// ---- dense_tc.cu (tcgen05 path)
+bool dense_eligible(const Problem* p, int64_t R);
+void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
+                   const std::vector<double>& sched, float eta, float alpha, uint64_t seed,
+                   int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, cudaStream_t s,
+                   double* loop_ms, int64_t* launches);
+
 // ---- host schedules (bit-exact with the reference's Python expressions)
 void pa_schedule(double lam0, int64_t T, double* out);   // lam0 * (1.0 - t / T)
 void sbm_schedule(double a0, int64_t T, double* out);    // np.linspace(0.0, a0, T)
