@@ -340,11 +340,19 @@ def run_ours(args):
     mean_step_kernel_ms = float(np.mean(loop_ms)) / T
     dbar = 2.0 * model.num_couplings / n
     if info.get("path") == "dense":
+        # FP8 E4M3 kind::f8f6f4 runs at 2x the dense bf16 rate on B200; the measured bf16
+        # number (MEASURED_PEAKS.json, sustained: the kernel runs inside a 1000-step loop)
+        # is doubled for the fp8 denominator and the bf16 fraction is reported beside it.
         flops = 2.0 * n * R * n
         achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": None,
-                "kernel": "dense J.S step (tcgen05) + fused integrator", "peak_source": src}
+        fp8_peak = 2.0 * bf16
+        roof = {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp8_peak, "traffic": None,
+                "kernel": "k_dense_pa_step: tcgen05.mma kind::f8f6f4 J.S + fused PA epilogue",
+                "peak_note": f"2 x measured bf16 sustained ({bf16} TF/s, {src})",
+                "frac_of_bf16_measured": achieved / bf16,
+                "flops_per_update": 2.0 * n, "units_per_launch": R * n,
+                "mean_launch_ms": mean_step_kernel_ms}
     else:
         B = bytes_per_update(args.solver, dbar, R)
         achieved = B * R * n / (mean_step_kernel_ms / 1e3) / 1e9

@@ -125,35 +125,41 @@ __global__ void k_pack_signs(const T* __restrict__ x, int64_t n, int64_t R_pad,
 }
 
 // ------------------------------------------------------------------ PA step (sparse)
-template <typename T, int V>
+// One warp owns row i and CPW consecutive replica chunks (CPW * 32 * V replicas): the CSR
+// row is read once for all of them and CPW x more loads are in flight per warp.
+template <typename T, int V, int CPW>
 __global__ void __launch_bounds__(256) k_pa_step(int64_t n, int64_t R_pad, Operator<T> op,
                                                  const T* __restrict__ h, T lam, T eta, T alpha,
                                                  T* __restrict__ x, T* __restrict__ m,
                                                  const uint32_t* __restrict__ sb_in,
                                                  uint32_t* __restrict__ sb_out) {
     using O = Ops<T>;
+    constexpr int NB = V * CPW;  // values per lane == sign words per (row, warp)
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int chunks = (int)(R_pad / (32 * V));
-    const int64_t i = warp / chunks;
-    const int c = (int)(warp % chunks);
+    const int groups = (int)(R_pad / (32 * NB));
+    const int64_t i = warp / groups;
+    const int c0 = (int)(warp % groups) * CPW;
     if (i >= n) return;
     const int64_t W = R_pad / 32;
-    const int64_t base = lane_base(i, R_pad, c, lane, V);
-    Vec<T, V> xv = *reinterpret_cast<const Vec<T, V>*>(x + base);
-    Vec<T, V> mv = *reinterpret_cast<const Vec<T, V>*>(m + base);
-
-    T f[V];
+    Vec<T, V> xv[CPW], mv[CPW];
 #pragma unroll
-    for (int b = 0; b < V; ++b) f[b] = (T)0;
-    const uint32_t* sbc = sb_in + c * V;
+    for (int g = 0; g < CPW; ++g) {
+        const int64_t base = lane_base(i, R_pad, c0 + g, lane, V);
+        xv[g] = *reinterpret_cast<const Vec<T, V>*>(x + base);
+        mv[g] = *reinterpret_cast<const Vec<T, V>*>(m + base);
+    }
+    T f[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) f[b] = (T)0;
+    const uint32_t* sbc = sb_in + c0 * V;  // NB consecutive words of row j
     const int64_t k0 = __ldg(op.indptr + i), k1 = __ldg(op.indptr + i + 1);
     int64_t k = k0;
     // batches of 4 neighbours: issue all gathers, then accumulate in order
     for (; k + 4 <= k1; k += 4) {
         int j[4];
         T a[4];
-        Vec<uint32_t, V> w[4];
+        Vec<uint32_t, V> w[4][CPW];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             j[u] = __ldg(op.indices + k + u);
@@ -161,36 +167,50 @@ __global__ void __launch_bounds__(256) k_pa_step(int64_t n, int64_t R_pad, Opera
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            w[u] = *reinterpret_cast<const Vec<uint32_t, V>*>(sbc + (int64_t)j[u] * W);
+#pragma unroll
+            for (int g = 0; g < CPW; ++g)
+                w[u][g] = *reinterpret_cast<const Vec<uint32_t, V>*>(sbc + (int64_t)j[u] * W + g * V);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int b = 0; b < V; ++b)
-                f[b] = O::add(f[b], ((w[u].v[b] >> lane) & 1u) ? a[u] : -a[u]);
+            for (int g = 0; g < CPW; ++g)
+#pragma unroll
+                for (int b = 0; b < V; ++b)
+                    f[g * V + b] = O::add(f[g * V + b],
+                                          ((w[u][g].v[b] >> lane) & 1u) ? a[u] : -a[u]);
     }
     for (; k < k1; ++k) {
-        int j = __ldg(op.indices + k);
-        T a = O::mul(op.sign, __ldg(op.data + k));
-        Vec<uint32_t, V> w = *reinterpret_cast<const Vec<uint32_t, V>*>(sbc + (int64_t)j * W);
+        const int j = __ldg(op.indices + k);
+        const T a = O::mul(op.sign, __ldg(op.data + k));
 #pragma unroll
-        for (int b = 0; b < V; ++b) f[b] = O::add(f[b], ((w.v[b] >> lane) & 1u) ? a : -a);
+        for (int g = 0; g < CPW; ++g) {
+            Vec<uint32_t, V> w =
+                *reinterpret_cast<const Vec<uint32_t, V>*>(sbc + (int64_t)j * W + g * V);
+#pragma unroll
+            for (int b = 0; b < V; ++b)
+                f[g * V + b] = O::add(f[g * V + b], ((w.v[b] >> lane) & 1u) ? a : -a);
+        }
     }
 
     const T hi = __ldg(h + i);
 #pragma unroll
-    for (int b = 0; b < V; ++b) {
-        T xo = xv.v[b];
-        T grad = O::add(O::add(O::mul(lam, xo), f[b]), hi);
-        T mn = O::sub(O::mul(alpha, mv.v[b]), O::mul(eta, grad));
-        T xn = O::add(xo, mn);
-        xn = xn < (T)-1 ? (T)-1 : (xn > (T)1 ? (T)1 : xn);
-        xv.v[b] = xn;
-        mv.v[b] = mn;
-        uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
-        if (lane == b) sb_out[i * W + c * V + b] = word;
+    for (int g = 0; g < CPW; ++g) {
+#pragma unroll
+        for (int b = 0; b < V; ++b) {
+            T xo = xv[g].v[b];
+            T grad = O::add(O::add(O::mul(lam, xo), f[g * V + b]), hi);
+            T mn = O::sub(O::mul(alpha, mv[g].v[b]), O::mul(eta, grad));
+            T xn = O::add(xo, mn);
+            xn = xn < (T)-1 ? (T)-1 : (xn > (T)1 ? (T)1 : xn);
+            xv[g].v[b] = xn;
+            mv[g].v[b] = mn;
+            uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
+            if (lane == g * V + b) sb_out[i * W + c0 * V + g * V + b] = word;
+        }
+        const int64_t base = lane_base(i, R_pad, c0 + g, lane, V);
+        *reinterpret_cast<Vec<T, V>*>(x + base) = xv[g];
+        *reinterpret_cast<Vec<T, V>*>(m + base) = mv[g];
     }
-    *reinterpret_cast<Vec<T, V>*>(x + base) = xv;
-    *reinterpret_cast<Vec<T, V>*>(m + base) = mv;
 }
 
 // ------------------------------------------------------------------ SBM step (sparse)
@@ -459,16 +479,22 @@ int block_threads(int64_t items) {
 template <typename T>
 void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T eta, T alpha,
                     T* x, T* m, const uint32_t* sbi, uint32_t* sbo, cudaStream_t s) {
-    int64_t warps = L.n * (L.R_pad / (32 * L.V));
-    unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
-    switch (L.V) {
-        case 1: k_pa_step<T, 1><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, h, lam, eta, alpha, x, m, sbi, sbo); break;
-        case 2: k_pa_step<T, 2><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, h, lam, eta, alpha, x, m, sbi, sbo); break;
-        default:
-            if constexpr (sizeof(T) == 4)
-                k_pa_step<T, 4><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, h, lam, eta, alpha, x, m, sbi, sbo);
-            break;
+    const int64_t chunks = L.R_pad / (32 * L.V);
+    const int cpw = (chunks % 2 == 0) ? 2 : 1;  // two chunks per warp when they pair up
+    const int64_t warps = L.n * (chunks / cpw);
+    const unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
+#define VXQ_PA_STEP(VV, CC) \
+    k_pa_step<T, VV, CC><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, h, lam, eta, alpha, x, m, sbi, sbo)
+    if (L.V == 1) {
+        if (cpw == 2) VXQ_PA_STEP(1, 2); else VXQ_PA_STEP(1, 1);
+    } else if (L.V == 2) {
+        if (cpw == 2) VXQ_PA_STEP(2, 2); else VXQ_PA_STEP(2, 1);
+    } else {
+        if constexpr (sizeof(T) == 4) {
+            if (cpw == 2) VXQ_PA_STEP(4, 2); else VXQ_PA_STEP(4, 1);
+        }
     }
+#undef VXQ_PA_STEP
 }
 
 template <typename T>
@@ -524,7 +550,8 @@ struct EventTimer {
 // Common tail: sign bits -> exact energies -> states / order / analog exports.
 template <typename T>
 void finish_outputs(Problem* p, const Layout& L, const uint32_t* sb, const T* xa, const T* ma,
-                    const vxq_run_opts* opts, vxq_outputs* out, cudaStream_t s) {
+                    const vxq_run_opts* opts, vxq_outputs* out, cudaStream_t s,
+                    const long long* q2 = nullptr) {
     const bool on_dev = opts && opts->outputs_on_device;
     const int64_t n = L.n, R = L.R;
     DevBuf<double> e_tmp;
@@ -533,7 +560,7 @@ void finish_outputs(Problem* p, const Layout& L, const uint32_t* sb, const T* xa
         e_tmp = DevBuf<double>(R, s);
         e_dev = e_tmp.get();
     }
-    energies_from_bits(p, sb, L.W, R, e_dev, s);
+    energies_from_bits(p, sb, L.W, R, e_dev, s, q2);
     DevBuf<int8_t> st_tmp;
     int8_t* st_dev = out->states;
     if (!on_dev) {
@@ -633,10 +660,12 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     if (!dense) path = choose_path(req, L, smem, p->nnz);
     EventTimer tm(s);
     const uint32_t* sb_final = nullptr;
+    DevBuf<long long> q2;
     if (dense) {
+        q2 = DevBuf<long long>(R, s);
         if constexpr (sizeof(T) == 4) {
             dense_pa_loop(p, R, L.R_pad, L.V, L.W, sched, eta, alpha, prm->seed, rbegin,
-                          x.get(), m.get(), sbA.get(), s, &out->loop_ms, &launches);
+                          x.get(), m.get(), sbA.get(), q2.get(), s, &out->loop_ms, &launches);
         }
         sb_final = sbA.get();
     } else if (path == VXQ_PATH_RESIDENT) {
@@ -674,7 +703,7 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         out->loop_ms = tm.ms();
     }
     out->path_used = path;
-    finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s);
+    finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s, q2.get());
     out->launches = launches + 4;
 }
 

@@ -22,51 +22,80 @@ namespace {
 
 constexpr int EB = 256;  // threads per block (8 warps)
 
-template <int L>
+// Partial sums: block (word w, split) -> partial[split][r][L+1] (limbs, then a coupling
+// count).  COUNT: all |J_ij| are equal (uniform magnitude c): couplings add sign(J_ij)*s_i*s_j
+// to an integer count folded in as count * c at the end; otherwise each coupling adds
+// +-limbs.  m_used = 0 skips the couplings entirely (count supplied by the caller).
+template <int L, bool COUNT>
 __global__ void __launch_bounds__(EB) k_energy_partial(
-    int64_t m, int64_t n, const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
+    int64_t m_used, int64_t n, const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
     const uint32_t* __restrict__ coef_fx, const uint32_t* __restrict__ h_fx,
     const uint32_t* __restrict__ sb, int64_t W, int64_t R, long long* __restrict__ partial) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t w = blockIdx.x;
     const int64_t split = blockIdx.y, nsplit = gridDim.y;
     long long acc[L];
+    long long cnt = 0;
 #pragma unroll
     for (int q = 0; q < L; ++q) acc[q] = 0;
-    const int64_t total = m + n;
-    const int64_t stride = nsplit * (EB / 32);
-    for (int64_t k = split * (EB / 32) + warp; k < total; k += stride) {
-        uint32_t x;
-        const uint32_t* c;
-        if (k < m) {
-            uint32_t wi = __ldg(sb + (int64_t)__ldg(ci + k) * W + w);
-            uint32_t wj = __ldg(sb + (int64_t)__ldg(cj + k) * W + w);
-            x = ~(wi ^ wj);  // bit 1 <=> s_i s_j = +1
-            c = coef_fx + k * L;
-        } else {
-            int64_t i = k - m;
-            x = __ldg(sb + i * W + w);  // bit 1 <=> s_i = +1
-            c = h_fx + i * L;
+    constexpr int U = 4;  // couplings per warp iteration (loads batched for MLP)
+    const int64_t stride = nsplit * (EB / 32) * U;
+    for (int64_t k0 = (split * (EB / 32) + warp) * U; k0 < m_used; k0 += stride) {
+        int32_t ii[U], jj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = k0 + u < m_used ? k0 + u : m_used - 1;
+            ii[u] = __ldg(ci + k);
+            jj[u] = __ldg(cj + k);
         }
-        const bool pos = (x >> lane) & 1u;
+        uint32_t wi[U], wj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            wi[u] = __ldg(sb + (int64_t)ii[u] * W + w);
+            wj[u] = __ldg(sb + (int64_t)jj[u] * W + w);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (k0 + u >= m_used) break;
+            const bool pos = ((~(wi[u] ^ wj[u])) >> lane) & 1u;  // s_i s_j = +1
+            const uint32_t* c = coef_fx + (k0 + u) * L;
+            if constexpr (COUNT) {
+                const bool neg = (int32_t)__ldg(c + L - 1) < 0;
+                cnt += (pos != neg) ? 1 : -1;
+            } else {
+#pragma unroll
+                for (int q = 0; q < L; ++q) {
+                    const uint32_t limb = __ldg(c + q);
+                    const long long v = (q == L - 1) ? (long long)(int32_t)limb : (long long)limb;
+                    acc[q] += pos ? v : -v;
+                }
+            }
+        }
+    }
+    // fields: sum_i h_i s_i
+    const int64_t fstride = nsplit * (EB / 32);
+    for (int64_t i = split * (EB / 32) + warp; i < n; i += fstride) {
+        const bool pos = (__ldg(sb + i * W + w) >> lane) & 1u;
+        const uint32_t* c = h_fx + i * L;
 #pragma unroll
         for (int q = 0; q < L; ++q) {
-            uint32_t limb = __ldg(c + q);
-            long long v = (q == L - 1) ? (long long)(int32_t)limb : (long long)limb;
+            const uint32_t limb = __ldg(c + q);
+            const long long v = (q == L - 1) ? (long long)(int32_t)limb : (long long)limb;
             acc[q] += pos ? v : -v;
         }
     }
-    __shared__ long long sh[EB / 32][32][L];
+    __shared__ long long sh[EB / 32][32][L + 1];
 #pragma unroll
     for (int q = 0; q < L; ++q) sh[warp][lane][q] = acc[q];
+    sh[warp][lane][L] = cnt;
     __syncthreads();
     if (warp == 0) {
-        int64_t r = w * 32 + lane;
+        const int64_t r = w * 32 + lane;
 #pragma unroll
-        for (int q = 0; q < L; ++q) {
+        for (int q = 0; q <= L; ++q) {
             long long t = 0;
             for (int ww = 0; ww < EB / 32; ++ww) t += sh[ww][lane][q];
-            if (r < R) partial[(split * R + r) * L + q] = t;
+            if (r < R) partial[(split * R + r) * (L + 1) + q] = t;
         }
     }
 }
@@ -85,18 +114,23 @@ __device__ uint64_t get_bits(const uint32_t* mag, int nl, int pos, int cnt) {
     return r;
 }
 
+struct FxConst {
+    uint32_t off[kMaxLimbs];  // offset
+    uint32_t mag[kMaxLimbs];  // +|J| (uniform-magnitude problems)
+};
+
 __global__ void k_energy_final(int64_t R, int L, int nsplit, const long long* partial,
-                               const uint32_t* offset_fx_unused, uint32_t o0, uint32_t o1,
-                               uint32_t o2, uint32_t o3, uint32_t o4, uint32_t o5, uint32_t o6,
-                               uint32_t o7, int e_low, double* out) {
+                               const long long* q2, FxConst fx, int e_low, double* out) {
     int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= R) return;
-    const uint32_t ofx[kMaxLimbs] = {o0, o1, o2, o3, o4, o5, o6, o7};
+    long long cnt = q2 ? q2[r] / 2 : 0;
+    for (int s = 0; s < nsplit; ++s) cnt += partial[((int64_t)s * R + r) * (L + 1) + L];
     long long acc[kMaxLimbs];
     for (int q = 0; q < L; ++q) {
-        long long v = (q == L - 1) ? (long long)(int32_t)ofx[q] : (long long)ofx[q];
-        for (int s = 0; s < nsplit; ++s) v += partial[((int64_t)s * R + r) * L + q];
-        acc[q] = v;
+        long long v = (q == L - 1) ? (long long)(int32_t)fx.off[q] : (long long)fx.off[q];
+        for (int s = 0; s < nsplit; ++s) v += partial[((int64_t)s * R + r) * (L + 1) + q];
+        const long long mg = (q == L - 1) ? (long long)(int32_t)fx.mag[q] : (long long)fx.mag[q];
+        acc[q] = v + cnt * mg;  // |cnt| < 2^31, |mg| < 2^32
     }
     // normalise into L+2 two's-complement 32-bit limbs
     uint32_t d[kMaxLimbs + 2];
@@ -172,41 +206,50 @@ __global__ void k_iota64(int64_t R, int64_t* v) {
 }
 
 template <int L>
-void launch_partial(Problem* p, const uint32_t* sb, int64_t W, int64_t R, int nsplit,
-                    long long* partial, cudaStream_t s) {
+void launch_partial(Problem* p, int64_t m_used, bool count, const uint32_t* sb, int64_t W,
+                    int64_t R, int nsplit, long long* partial, cudaStream_t s) {
     dim3 grid((unsigned)W, (unsigned)nsplit);
-    k_energy_partial<L><<<grid, EB, 0, s>>>(p->m, p->n, p->coo_i, p->coo_j, p->coef_fx,
-                                            p->h_fx, sb, W, R, partial);
+    if (count)
+        k_energy_partial<L, true><<<grid, EB, 0, s>>>(m_used, p->n, p->coo_i, p->coo_j,
+                                                      p->coef_fx, p->h_fx, sb, W, R, partial);
+    else
+        k_energy_partial<L, false><<<grid, EB, 0, s>>>(m_used, p->n, p->coo_i, p->coo_j,
+                                                       p->coef_fx, p->h_fx, sb, W, R, partial);
     VXQ_CHECK_LAUNCH();
 }
 
 }  // namespace
 
 void energies_from_bits(Problem* p, const uint32_t* sb, int64_t W, int64_t R,
-                        double* energies_dev, cudaStream_t s) {
+                        double* energies_dev, cudaStream_t s, const long long* q2) {
     if (!p->energy_ok)
         throw Error(VXQ_ERR_UNSUPPORTED,
                     "coefficient dynamic range exceeds the exact accumulator (256 bits)");
     const int L = p->limbs;
-    const int64_t terms = p->m + p->n;
-    // enough blocks to fill 148 SMs several times, each split >= 2048 terms
+    const int64_t m_used = q2 ? 0 : p->m;
+    const bool count = p->uniform_magnitude && !q2;
+    const int64_t terms = m_used + p->n;
+    // enough blocks to fill 148 SMs several times, each split >= 4096 terms
     int64_t want = std::max<int64_t>(1, (148 * 8) / std::max<int64_t>(W, 1));
-    int64_t maxs = std::max<int64_t>(1, terms / 2048);
+    int64_t maxs = std::max<int64_t>(1, terms / 4096);
     int nsplit = (int)std::min<int64_t>(std::min<int64_t>(want, maxs), 65535);
-    DevBuf<long long> partial((size_t)nsplit * R * L, s);
+    DevBuf<long long> partial((size_t)nsplit * R * (L + 1), s);
     switch (L) {
-        case 2: launch_partial<2>(p, sb, W, R, nsplit, partial.get(), s); break;
-        case 3: launch_partial<3>(p, sb, W, R, nsplit, partial.get(), s); break;
-        case 4: launch_partial<4>(p, sb, W, R, nsplit, partial.get(), s); break;
-        case 5: launch_partial<5>(p, sb, W, R, nsplit, partial.get(), s); break;
-        case 6: launch_partial<6>(p, sb, W, R, nsplit, partial.get(), s); break;
-        case 7: launch_partial<7>(p, sb, W, R, nsplit, partial.get(), s); break;
-        default: launch_partial<8>(p, sb, W, R, nsplit, partial.get(), s); break;
+        case 2: launch_partial<2>(p, m_used, count, sb, W, R, nsplit, partial.get(), s); break;
+        case 3: launch_partial<3>(p, m_used, count, sb, W, R, nsplit, partial.get(), s); break;
+        case 4: launch_partial<4>(p, m_used, count, sb, W, R, nsplit, partial.get(), s); break;
+        case 5: launch_partial<5>(p, m_used, count, sb, W, R, nsplit, partial.get(), s); break;
+        case 6: launch_partial<6>(p, m_used, count, sb, W, R, nsplit, partial.get(), s); break;
+        case 7: launch_partial<7>(p, m_used, count, sb, W, R, nsplit, partial.get(), s); break;
+        default: launch_partial<8>(p, m_used, count, sb, W, R, nsplit, partial.get(), s); break;
     }
-    const uint32_t* o = p->offset_fx;
-    k_energy_final<<<(unsigned)ceil_div(R, 128), 128, 0, s>>>(
-        R, L, nsplit, partial.get(), nullptr, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7],
-        p->e_low, energies_dev);
+    FxConst fx;
+    for (int q = 0; q < kMaxLimbs; ++q) {
+        fx.off[q] = p->offset_fx[q];
+        fx.mag[q] = p->mag_fx[q];
+    }
+    k_energy_final<<<(unsigned)ceil_div(R, 128), 128, 0, s>>>(R, L, nsplit, partial.get(), q2,
+                                                              fx, p->e_low, energies_dev);
     VXQ_CHECK_LAUNCH();
 }
 

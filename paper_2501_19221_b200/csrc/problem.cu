@@ -45,9 +45,12 @@ __global__ void k_validate_coo(int64_t n, int64_t m, const int64_t* rows, const 
 __global__ void k_count_deg(int64_t m, const int64_t* rows, const int64_t* cols, int32_t* deg_up,
                             int32_t* deg_lo, int32_t* ci, int32_t* cj) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= m) return;
-    int32_t i = (int32_t)rows[k], j = (int32_t)cols[k];
-    atomicAdd(deg_up + i, 1);
+    const bool ok = k < m;
+    int32_t i = ok ? (int32_t)rows[k] : -1, j = ok ? (int32_t)cols[k] : -1;
+    // rows are sorted: lanes sharing a row aggregate into one atomic
+    const unsigned peers = __match_any_sync(0xffffffffu, i);
+    if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(deg_up + i, __popc(peers));
+    if (!ok) return;
     atomicAdd(deg_lo + j, 1);
     ci[k] = i;
     cj[k] = j;
@@ -105,11 +108,23 @@ __global__ void k_fields(int64_t n, const double* h, float* h32, double* g64, fl
 
 __global__ void k_abs_minmax(int64_t m, const double* v, unsigned long long* mn,
                              unsigned long long* mx) {
-    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= m) return;
-    unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v[k]));
-    atomicMin(mn, b);
-    atomicMax(mx, b);
+    unsigned long long lo = ~0ULL, hi = 0ULL;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)blockDim.x * gridDim.x) {
+        unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v[k]));
+        lo = b < lo ? b : lo;
+        hi = b > hi ? b : hi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+        unsigned long long c = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = c > hi ? c : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mn, lo);
+        atomicMax(mx, hi);
+    }
 }
 
 // ---- exact fixed-point encoding of coefficients ----
@@ -348,7 +363,7 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
             DevBuf<unsigned long long> mm(2, s);
             unsigned long long init[2] = {~0ULL, 0ULL};
             VXQ_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
-            k_abs_minmax<<<nblk(m), TB, 0, s>>>(m, dval.get(), mm.get(), mm.get() + 1);
+            k_abs_minmax<<<(unsigned)std::min<int64_t>(nblk(m), 148 * 16), TB, 0, s>>>(m, dval.get(), mm.get(), mm.get() + 1);
             VXQ_CHECK_LAUNCH();
             unsigned long long res[2];
             VXQ_CUDA(cudaMemcpyAsync(res, mm.get(), sizeof(res), cudaMemcpyDeviceToHost, s));
@@ -397,6 +412,14 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
                 VXQ_CHECK_LAUNCH();
                 VXQ_CUDA(cudaMemcpyAsync(P->offset_fx, ofx.get(), L * sizeof(uint32_t),
                                          cudaMemcpyDeviceToHost, s));
+                if (P->uniform_magnitude) {
+                    DevBuf<uint32_t> mfx(L, s);
+                    k_encode_scalar<<<1, 1, 0, s>>>(P->magnitude, P->e_low, L, mfx.get());
+                    VXQ_CHECK_LAUNCH();
+                    VXQ_CUDA(cudaMemcpyAsync(P->mag_fx, mfx.get(), L * sizeof(uint32_t),
+                                             cudaMemcpyDeviceToHost, s));
+                    VXQ_CUDA(cudaStreamSynchronize(s));
+                }
             }
         }
         VXQ_CUDA(cudaStreamSynchronize(s));

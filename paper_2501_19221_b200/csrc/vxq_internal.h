@@ -42,6 +42,7 @@ struct Problem {
     uint32_t* coef_fx = nullptr;   // [m][limbs]
     uint32_t* h_fx = nullptr;      // [n][limbs]
     uint32_t offset_fx[kMaxLimbs] = {0};
+    uint32_t mag_fx[kMaxLimbs] = {0};  // +|J_ij| when uniform_magnitude
     bool energy_ok = true;         // false if the dynamic range exceeds kMaxLimbs*32 bits
 
     int64_t max_row_nnz = 0;
@@ -56,11 +57,29 @@ struct Problem {
     ~Problem();
 };
 
+// Keep the device's stream-ordered pool from trimming at every synchronize, so repeated
+// solves reuse workspace instead of going back to the driver (once per device).
+inline void retain_mempool() {
+    static std::mutex mu;
+    static bool done[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> g(mu);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 // run-scoped stream holder
 struct StreamScope {
     cudaStream_t s = nullptr;
     bool owned = false;
     explicit StreamScope(void* user) {
+        retain_mempool();
         if (user) {
             s = (cudaStream_t)user;
         } else {
@@ -110,8 +129,10 @@ double lanczos_lambda_max(int64_t n, const int64_t* indptr, const int32_t* indic
 
 // ---- energy.cu
 // energies of bit-packed spins sb[n][W] (bit (r%32) of word r/32) for replicas r < R
+// q2 (optional, uniform-magnitude problems): per replica 2*sum_{i<j} K_ij s_i s_j with
+// J = c K, already computed (dense tensor-core energy step); only h/offset are summed here.
 void energies_from_bits(Problem* p, const uint32_t* sb, int64_t W, int64_t R,
-                        double* energies_dev, cudaStream_t s);
+                        double* energies_dev, cudaStream_t s, const long long* q2 = nullptr);
 void pack_states_to_bits(const int8_t* states_dev, int64_t n, int64_t R, int64_t W,
                          uint32_t* sb, cudaStream_t s);
 void bits_to_states(const uint32_t* sb, int64_t n, int64_t R, int64_t W, int8_t* states_dev,
@@ -132,8 +153,8 @@ void sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indice
 bool dense_eligible(const Problem* p, int64_t R);
 void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                    const std::vector<double>& sched, float eta, float alpha, uint64_t seed,
-                   int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, cudaStream_t s,
-                   double* loop_ms, int64_t* launches);
+                   int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, long long* q2,
+                   cudaStream_t s, double* loop_ms, int64_t* launches);
 
 // ---- host schedules (bit-exact with the reference's Python expressions)
 void pa_schedule(double lam0, int64_t T, double* out);   // lam0 * (1.0 - t / T)
