@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             ptx::mbar_wait(tfull + acc, acc_ph);
             ptx::tc_fence_after();
             if (a.mode == 0) {
+                const uint64_t stream = ptx::policy_evict_first();
                 uint8_t* __restrict__ sg = (t & 1) ? a.s_buf[0] : a.s_buf[1];  // S_{t+1}
                 const float lam = __ldg(a.lam + t);
                 const float hi = row_ok ? __ldg(a.h + i) : 0.f;
@@ -318,8 +319,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {  // L2 (cg): written by another SM
                         const bool ok = row_ok && (r0 + jj) < a.R;
-                        xo[jj] = ok ? __ldcg(xg + base + (int64_t)jj * a.ld) : 0.f;
-                        mo[jj] = ok ? __ldcg(mg + base + (int64_t)jj * a.ld) : 0.f;
+                        xo[jj] = ok ? ptx::ld_stream(xg + base + (int64_t)jj * a.ld, stream) : 0.f;
+                        mo[jj] = ok ? ptx::ld_stream(mg + base + (int64_t)jj * a.ld, stream) : 0.f;
                     }
                     ptx::tmem_ld_wait();
 #pragma unroll
@@ -332,8 +333,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         xn = xn < -1.f ? -1.f : (xn > 1.f ? 1.f : xn);
                         if (ok) {
                             const int64_t off = base + (int64_t)jj * a.ld;
-                            __stcg(xg + off, xn);
-                            __stcg(mg + off, mn);
+                            ptx::st_stream(xg + off, xn, stream);
+                            ptx::st_stream(mg + off, mn, stream);
                             sg[off] = xn >= 0.f ? FP8_P1 : FP8_M1;
                         }
                     }
