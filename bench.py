@@ -70,6 +70,17 @@ def peaks():
     return FALLBACK_HBM_GBS, 1400.0, "fallback"
 
 
+def measured_traffic(kernel: str):
+    """DRAM bytes per dynamics step of `kernel` from the newest committed ncu capture."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")),
+                       reverse=True):
+        d = json.load(open(path))
+        if kernel in d:
+            return d[kernel]["dram_bytes_per_step"], os.path.relpath(path, ROOT)
+    return None, None
+
+
 def bytes_per_update(solver: str, dbar: float, R: int) -> float:
     """algorithmic bytes per replica-variable update (fp32 state, int32+fp32 CSR)."""
     amort = (8.0 * dbar + 4.0) / R
@@ -346,9 +357,11 @@ def run_ours(args):
         flops = 2.0 * n * R * n
         achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
         fp8_peak = 2.0 * bf16
+        tr, tsrc = measured_traffic("k_dense_pa_run")
         roof = {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp8_peak, "traffic": None,
-                "kernel": "k_dense_pa_step: tcgen05.mma kind::f8f6f4 J.S + fused PA epilogue",
+                "frac": achieved / fp8_peak, "traffic": tr, "traffic_unit": "bytes/step",
+                "traffic_source": tsrc,
+                "kernel": "k_dense_pa_run: tcgen05.mma kind::f8f6f4 J.S + fused PA epilogue (persistent)",
                 "peak_note": f"2 x measured bf16 sustained ({bf16} TF/s, {src})",
                 "frac_of_bf16_measured": achieved / bf16,
                 "flops_per_update": 2.0 * n, "units_per_launch": R * n,
@@ -356,8 +369,10 @@ def run_ours(args):
     else:
         B = bytes_per_update(args.solver, dbar, R)
         achieved = B * R * n / (mean_step_kernel_ms / 1e3) / 1e9
+        tr, tsrc = measured_traffic(f"k_{args.solver}_step")
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
+                "frac": achieved / hbm, "traffic": tr, "traffic_unit": "bytes/step",
+                "traffic_source": tsrc,
                 "kernel": f"k_{args.solver}_step ({info.get('path')})",
                 "bytes_per_update": B, "units_per_launch": R * n,
                 "mean_launch_ms": mean_step_kernel_ms,
