@@ -1,22 +1,29 @@
-// dense_tc.cu -- dense J.S coupling field on the 5th-gen tensor cores, PA integrator fused.
+// dense_tc.cu -- dense coupling field on the 5th-gen tensor cores with the integrator fused.
 //
-// Replaces `sign_pm(X).astype(f64) @ A` + the PA update (parallel_annealing.py:42-45) for
-// dense couplings with a uniform magnitude |J_ij| = c (e.g. Sherrington-Kirkpatrick,
-// BASELINE config 2): J = c * K with K in {-1, 0, +1} and spins in {-1, +1} are exact in
-// FP8 E4M3, and the f32 TMEM accumulator holds the integer K.s exactly (|K.s| < 2^24), so
-// the field f = c * (K.s) carries a single rounding.
+// For dense couplings with a uniform magnitude |J_ij| = c (e.g. Sherrington-Kirkpatrick,
+// BASELINE config 2): J = c * K with K in {-1, 0, +1}.
+//   PA  (parallel_annealing.py:42-45): F = K.s with s in {-1,+1}; K and s are exact in FP8
+//       E4M3, the f32 TMEM accumulator holds the integer K.s exactly (|K.s| < 2^24), and
+//       f = c * (K.s) carries a single rounding.                     (Kind::kFp8, 1 plane)
+//   SBM (bifurcation.py:40-46): F = K.q with continuous fp32 q, split exactly into three
+//       bf16 terms q = q1 + q2 + q3 (8 + 8 + 8 significant bits); K.q1 + K.q2 + K.q3
+//       accumulate into one f32 TMEM accumulator (kind::f16).     (Kind::kBf16x3, 3 planes)
 //
-// One launch per dynamics step (the step-to-step dependency is grid-wide):
-//   F^T[i, r] = sum_j K[i, j] S[r, j]      M = n rows (i), N = replicas (r), K = n
-//   A = K  [n_pad][n_pad] fp8, K-major      (TMA, SWIZZLE_128B, 128 x 128 B boxes)
-//   B = S  [R][n_pad]    fp8, K-major      (TMA, SWIZZLE_128B, 256 x 128 B boxes)
-//   D in TMEM: 128 lanes (rows i) x 256 f32 columns (replicas r), double-buffered
-// Persistent warp-specialised CTA (1 per SM, 320 threads):
-//   warp 0  TMA producer        4-stage smem ring (48 KB / stage)
-//   warp 1  MMA issuer          one elected thread: 4 x tcgen05.mma (K = 32) per stage
-//   warps 2-9 epilogue          tcgen05.ld -> PA update of (x, m) in HBM -> next S (fp8)
-// The epilogue of tile t overlaps the mainloop of tile t+1 (2 TMEM accumulators).
+//   F^T[i, r] = sum_j K[i, j] B[r, j]     M = n rows (i), N = replicas (r), K = n
+//   A = K  [ld][ld] K-major                 (TMA, SWIZZLE_128B, 128 rows x 128 B boxes)
+//   B = S or q-planes [planes][R][ld]       (TMA, SWIZZLE_128B, bn rows x 128 B x planes)
+//   D in TMEM: 128 lanes (rows i) x bn f32 columns (replicas r), 2 accumulators
+// Persistent warp-specialised CTA (1 per SM, 320 threads) running ALL T steps:
+//   warp 0  TMA producer        STAGES-deep smem ring
+//   warp 1  MMA issuer          one elected thread issues tcgen05.mma for the CTA
+//   warps 2-9 epilogue          tcgen05.ld -> integrator update of the state in HBM ->
+//                               next-step B operand (fp8 signs / bf16 q-splits)
+// Tiles are enumerated (step t, replica block nb, row block mb) and dealt round-robin; a
+// tile of step t only waits for the step-(t-1) tiles of its replica block (release/acquire
+// counter + proxy fence before the TMA), so steps overlap with no per-step launch, prologue
+// or wave quantisation.
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -27,24 +34,48 @@
 
 namespace vxq {
 
-constexpr int DBM = 128;       // rows (i) per tile
-constexpr int DBN = 256;       // max replicas (r) per tile; the run picks bn <= DBN
-constexpr int DBK = 128;       // K bytes (fp8 elements) per stage
-constexpr int DSTAGES = 4;
-constexpr int DA_BYTES = DBM * DBK;
-constexpr int DB_BYTES = DBN * DBK;
-constexpr int DSTAGE_BYTES = DA_BYTES + DB_BYTES;
-constexpr int DSMEM = DSTAGES * DSTAGE_BYTES + 1024 + 256;
+constexpr int DBM = 128;   // rows (i) per tile
+constexpr int DROW = 128;  // bytes per K-major smem row (one SWIZZLE_128B atom row)
+constexpr int DA_BYTES = DBM * DROW;
 constexpr int DTHREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
+constexpr int DSMEM = 192 * 1024 + 1024 + 256;
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
+enum class Kind : int { kFp8 = 0, kBf16x3 = 1 };
+
+template <Kind K>
+struct KindTraits;
+template <>
+struct KindTraits<Kind::kFp8> {
+    static constexpr int kPlanes = 1, kStages = 4, kBnMax = 256, kElemBytes = 1;
+    static constexpr int kKPerMma = 32;  // fp8: K = 32 per tcgen05.mma (32 B)
+    // D=F32, A=B=E4M3, K-major
+    static constexpr uint32_t kIdescBase = (1u << 4);
+};
+template <>
+struct KindTraits<Kind::kBf16x3> {
+    static constexpr int kPlanes = 3, kStages = 3, kBnMax = 128, kElemBytes = 2;
+    static constexpr int kKPerMma = 16;  // bf16: K = 16 per tcgen05.mma (32 B)
+    // D=F32, A=B=BF16, K-major
+    static constexpr uint32_t kIdescBase = (1u << 4) | (1u << 7) | (1u << 10);
+};
+
+template <Kind K>
+constexpr int stage_bytes() {
+    return DA_BYTES + KindTraits<K>::kPlanes * KindTraits<K>::kBnMax * DROW;
+}
+static_assert(4 * stage_bytes<Kind::kFp8>() <= 192 * 1024, "fp8 ring");
+static_assert(3 * stage_bytes<Kind::kBf16x3>() <= 192 * 1024, "bf16 ring");
+
 struct DenseOperand {
-    int64_t n = 0, ld = 0;  // ld = n_pad (multiple of 128)
-    uint8_t* K = nullptr;   // [ld][ld] fp8 E4M3 in {-1, 0, +1}
-    float scale = 0.f;      // c (fp32)
-    CUtensorMap tmA;
+    int64_t n = 0, ld = 0;      // ld = n_pad (multiple of 128)
+    float scale = 0.f;          // c (fp32)
+    uint8_t* K8 = nullptr;      // [ld][ld] fp8 E4M3 in {-1, 0, +1}
+    __nv_bfloat16* K16 = nullptr;  // [ld][ld] bf16 in {-1, 0, +1} (SBM, built lazily)
+    CUtensorMap tmA8, tmA16;
     ~DenseOperand() {
-        if (K) cudaFree(K);
+        if (K8) cudaFree(K8);
+        if (K16) cudaFree(K16);
     }
 };
 
@@ -72,17 +103,19 @@ EncodeFn get_encode() {
     return fn;
 }
 
-// 2-D uint8 tensor [outer][inner] with row pitch `pitch` bytes, SW128 boxes
-CUtensorMap make_map_u8(const void* base, uint64_t inner, uint64_t outer, uint64_t pitch,
-                        uint32_t box_inner, uint32_t box_outer) {
+// up to 3-D tensor [planes][outer][inner] (elements of `esize` bytes), SW128 boxes
+CUtensorMap make_map(const void* base, CUtensorMapDataType dt, int esize, uint64_t inner,
+                     uint64_t outer, uint64_t planes, uint32_t box_inner, uint32_t box_outer,
+                     uint32_t box_planes) {
     CUtensorMap m;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {pitch};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base),
-                              dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    const cuuint32_t rank = planes > 1 ? 3 : 2;
+    cuuint64_t dims[3] = {inner, outer, planes};
+    cuuint64_t strides[2] = {inner * esize, inner * outer * esize};
+    cuuint32_t box[3] = {box_inner, box_outer, box_planes};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = get_encode()(&m, dt, rank, const_cast<void*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(VXQ_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     return m;
@@ -90,18 +123,32 @@ CUtensorMap make_map_u8(const void* base, uint64_t inner, uint64_t outer, uint64
 
 __global__ void k_build_sign_matrix(int64_t n, int64_t ld, const int64_t* __restrict__ indptr,
                                     const int32_t* __restrict__ indices,
-                                    const double* __restrict__ data, uint8_t* __restrict__ K) {
+                                    const double* __restrict__ data, uint8_t* __restrict__ K8,
+                                    __nv_bfloat16* __restrict__ K16) {
     int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (row >= n) return;
-    for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32)
-        K[row * ld + indices[k]] = data[k] > 0 ? FP8_P1 : FP8_M1;
+    for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32) {
+        const bool pos = data[k] > 0;
+        if (K8) K8[row * ld + indices[k]] = pos ? FP8_P1 : FP8_M1;
+        if (K16) K16[row * ld + indices[k]] = __float2bfloat16_rn(pos ? 1.f : -1.f);
+    }
 }
 
 __device__ __forceinline__ int64_t pos_interleaved(int64_t r, int V) {
     int64_t ch = 32 * V;
     int64_t c = r / ch, rem = r % ch;
     return c * ch + (rem % 32) * V + rem / 32;
+}
+
+// exact 3-way bf16 split of an fp32 value: v == q1 + q2 + q3
+__device__ __forceinline__ void split3(float v, __nv_bfloat16& q1, __nv_bfloat16& q2,
+                                       __nv_bfloat16& q3) {
+    q1 = __float2bfloat16_rn(v);
+    const float r1 = __fsub_rn(v, __bfloat162float(q1));
+    q2 = __float2bfloat16_rn(r1);
+    const float r2 = __fsub_rn(r1, __bfloat162float(q2));
+    q3 = __float2bfloat16_rn(r2);
 }
 
 // x0 ~ uniform(-1, 1) from replica stream r (same draws as k_init_pa), row-major [R][ld]
@@ -121,6 +168,34 @@ __global__ void k_init_pa_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, in
             x[r * ld + i] = v;
             m[r * ld + i] = 0.f;
             s[r * ld + i] = v >= 0.f ? FP8_P1 : FP8_M1;
+        }
+    }
+}
+
+// q0, p0 (stream r: n q-draws then n p-draws, as k_init_sbm) + the bf16 q-splits
+__global__ void k_init_sbm_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, int64_t rbegin,
+                              double amp, float* __restrict__ q, float* __restrict__ p,
+                              __nv_bfloat16* __restrict__ planes) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t nq = (2 * n + 3) / 4;
+    if (idx >= nq * R) return;
+    int64_t r = idx / nq, qd = idx % nq;
+    U64x4 o = philox4x64_10((uint64_t)qd + 1, 0, (uint64_t)(rbegin + r), 0, seed, 0);
+    const double lo = -amp, range = __dadd_rn(amp, amp);
+    const int64_t plane = R * ld;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        int64_t k = 4 * qd + w;
+        float v = (float)uniform_from_raw(o.v[w], lo, range);
+        if (k < n) {
+            q[r * ld + k] = v;
+            __nv_bfloat16 a, b, c;
+            split3(v, a, b, c);
+            planes[r * ld + k] = a;
+            planes[plane + r * ld + k] = b;
+            planes[2 * plane + r * ld + k] = c;
+        } else if (k < 2 * n) {
+            p[r * ld + (k - n)] = v;
         }
     }
 }
@@ -145,16 +220,27 @@ __global__ void k_pack_bits_rm(const float* __restrict__ x, int64_t n, int64_t R
     if (lane == 0) sb[i * W + w] = word;
 }
 
+__global__ void k_signs_fp8_rm(const float* __restrict__ x, int64_t n, int64_t R, int64_t ld,
+                               uint8_t* __restrict__ s) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n * R) return;
+    int64_t r = idx / n, i = idx % n;
+    s[r * ld + i] = x[r * ld + i] >= 0.f ? FP8_P1 : FP8_M1;
+}
+
 struct DenseRunArgs {
     int n, R, ld, kblocks, m_tiles, n_tiles, bn;
     int T;                   // dynamics steps covered by this launch
-    float scale, eta, alpha;
-    const float* lam;        // [T] lambda_t (fp32)
-    const float* h;
-    float* x;
-    float* m;
-    uint8_t* s_buf[2];       // S_t lives in s_buf[t & 1]; step t writes s_buf[(t+1) & 1]
-    int mode;                // 0: PA steps, 1: energy pass over S_0 (q2), 2: no-op epilogue
+    float scale;             // c
+    float eta, alpha;        // PA
+    float dt, a0, c0, dta0, q_cap;  // SBM
+    const float* sched;      // [T] lambda_t (PA) / a_t (SBM), fp32
+    const float* h;          // PA: h;  SBM: g = -h
+    float* x;                // PA: x;  SBM: q
+    float* m;                // PA: m;  SBM: p
+    uint8_t* b_buf[2];       // B operand of step t lives in b_buf[t & 1]
+    int64_t plane_elems;     // elements per q-plane (R * ld) for kBf16x3
+    int mode;                // 0: dynamics steps, 1: energy pass over b_buf[0] (q2), 2: no-op
     long long* q2;           // [R] 2 * sum_{i<j} K_ij s_i s_j  (mode 1)
     unsigned* done;          // [T][n_tiles] finished row-tiles per (step, replica block)
 };
@@ -165,27 +251,26 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     return v;
 }
 
-// Persistent dataflow kernel over all T steps.  Tiles are enumerated (step, replica block
-// nb, row block mb) and dealt round-robin to the CTAs (1 per SM).  A tile of step t reads
-// S_t[nb block] and x/m of (nb, mb), all produced by step t-1 tiles of the same replica
-// block, so it only waits for done[t-1][nb] == m_tiles: the tail of step t-1 overlaps the
-// head of step t and there is no per-step launch, prologue or wave quantisation.
+template <Kind KD>
 __global__ void __launch_bounds__(DTHREADS, 1)
-    k_dense_pa_run(const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB0,
-                   const __grid_constant__ CUtensorMap tmB1, DenseRunArgs a) {
+    k_dense_run(const __grid_constant__ CUtensorMap tmA,
+                const __grid_constant__ CUtensorMap tmB0,
+                const __grid_constant__ CUtensorMap tmB1, DenseRunArgs a) {
+    using TR = KindTraits<KD>;
+    constexpr int STAGES = TR::kStages;
+    constexpr int SBYTES = stage_bytes<KD>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + DSTAGES * DSTAGE_BYTES);
-    uint64_t* empty = full + DSTAGES;
-    uint64_t* tfull = empty + DSTAGES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 192 * 1024);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < DSTAGES; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(full + s, 1);
             ptx::mbar_init(empty + s, 1);
         }
@@ -205,12 +290,12 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
     const int tps = a.m_tiles * a.n_tiles;  // tiles per step
     const int num_tiles = tps * a.T;
+    const uint32_t b_plane_bytes = (uint32_t)a.bn * DROW;
 
     if (warp == 0) {
         // ---------------- TMA producer
         if (ptx::elect_one()) {
-            // J (100 MB at n = 10^4) and S stay L2-resident across steps; x/m stream past
-            const uint64_t keep = ptx::policy_evict_last();
+            const uint64_t keep = ptx::policy_evict_last();  // K and B stay in L2
             int stage = 0;
             uint32_t ph = 0;
             for (int g = blockIdx.x; g < num_tiles; g += gridDim.x) {
@@ -219,11 +304,12 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const CUtensorMap* tmB = (t & 1) ? &tmB1 : &tmB0;
                 for (int kb = 0; kb < a.kblocks; ++kb) {
                     ptx::mbar_wait(empty + stage, ph ^ 1);
-                    uint8_t* sa = smem + stage * DSTAGE_BYTES;
-                    ptx::mbar_arrive_expect_tx(full + stage, DA_BYTES + a.bn * DBK);
-                    ptx::tma_load_2d_hint(sa, &tmA, full + stage, kb * DBK, mb * DBM, keep);
+                    uint8_t* sa = smem + stage * SBYTES;
+                    ptx::mbar_arrive_expect_tx(full + stage, DA_BYTES + TR::kPlanes * b_plane_bytes);
+                    const int kcol = kb * (DROW / TR::kElemBytes);
+                    ptx::tma_load_2d_hint(sa, &tmA, full + stage, kcol, mb * DBM, keep);
                     if (kb == 0 && t > 0) {
-                        // S_t[nb] complete? (release/acquire on the step t-1 counter, then a
+                        // B_t[nb] complete? (release/acquire on the step t-1 counter, then a
                         // proxy fence so the async-proxy TMA sees the generic-proxy stores)
                         const unsigned* cnt = a.done + (size_t)(t - 1) * a.n_tiles + nb;
                         if (ld_acquire_gpu(cnt) < (unsigned)a.m_tiles) {
@@ -237,9 +323,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         }
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                     }
-                    ptx::tma_load_2d_hint(sa + DA_BYTES, tmB, full + stage, kb * DBK,
-                                          nb * a.bn, keep);
-                    if (++stage == DSTAGES) {
+                    if constexpr (TR::kPlanes == 1)
+                        ptx::tma_load_2d_hint(sa + DA_BYTES, tmB, full + stage, kcol,
+                                              nb * a.bn, keep);
+                    else
+                        ptx::tma_load_3d_hint(sa + DA_BYTES, tmB, full + stage, kcol,
+                                              nb * a.bn, 0, keep);
+                    if (++stage == STAGES) {
                         stage = 0;
                         ph ^= 1;
                     }
@@ -248,9 +338,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (single thread issues for the CTA)
-        // idesc: D=F32, A=B=E4M3, K-major both, N=bn, M=128
         const uint32_t idesc =
-            (1u << 4) | ((uint32_t)(a.bn >> 3) << 17) | ((uint32_t)(DBM >> 4) << 24);
+            TR::kIdescBase | ((uint32_t)(a.bn >> 3) << 17) | ((uint32_t)(DBM >> 4) << 24);
         int stage = 0;
         uint32_t ph = 0;
         int lt = 0;
@@ -259,21 +348,30 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             const uint32_t acc_ph = (lt >> 1) & 1;
             ptx::mbar_wait(tempty + acc, acc_ph ^ 1);
             ptx::tc_fence_after();
-            const uint32_t d = tmem_base + acc * DBN;
+            const uint32_t d = tmem_base + acc * 256;
             for (int kb = 0; kb < a.kblocks; ++kb) {
                 ptx::mbar_wait(full + stage, ph);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    const uint32_t sa = ptx::smem_u32(smem + stage * DSTAGE_BYTES);
+                    const uint32_t sa = ptx::smem_u32(smem + stage * SBYTES);
                     const uint64_t da = ptx::sw128_kmajor_desc(sa);
-                    const uint64_t db = ptx::sw128_kmajor_desc(sa + DA_BYTES);
 #pragma unroll
-                    for (int k = 0; k < DBK / 32; ++k)  // K = 32 fp8 per MMA = 32 B = 2 x 16 B
-                        ptx::mma_f8f6f4(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                    for (int pl = 0; pl < TR::kPlanes; ++pl) {
+                        const uint64_t db =
+                            ptx::sw128_kmajor_desc(sa + DA_BYTES + pl * b_plane_bytes);
+#pragma unroll
+                        for (int k = 0; k < DROW / 32; ++k) {  // 32 B of K per MMA
+                            const uint32_t accum = (kb | pl | k) != 0;
+                            if constexpr (KD == Kind::kFp8)
+                                ptx::mma_f8f6f4(d, da + 2 * k, db + 2 * k, idesc, accum);
+                            else
+                                ptx::mma_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
+                        }
+                    }
                     ptx::mma_commit(empty + stage);
                 }
                 __syncwarp();
-                if (++stage == DSTAGES) {
+                if (++stage == STAGES) {
                     stage = 0;
                     ph ^= 1;
                 }
@@ -282,7 +380,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             __syncwarp();
         }
     } else {
-        // ---------------- epilogue (8 warps): TMEM -> PA update -> next spins
+        // ---------------- epilogue (8 warps): TMEM -> integrator -> next B operand
         // warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a lane quarter
         // take alternate 16-column chunks of the tile.
         const int q = warp & 3;
@@ -301,13 +399,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             const uint32_t acc_ph = (lt >> 1) & 1;
             const int i = mb * DBM + row;
             const bool row_ok = i < a.n;
-            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * DBN;
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
             ptx::mbar_wait(tfull + acc, acc_ph);
             ptx::tc_fence_after();
             if (a.mode == 0) {
                 const uint64_t stream = ptx::policy_evict_first();
-                uint8_t* __restrict__ sg = (t & 1) ? a.s_buf[0] : a.s_buf[1];  // S_{t+1}
-                const float lam = __ldg(a.lam + t);
+                uint8_t* nxt = (t & 1) ? a.b_buf[0] : a.b_buf[1];  // B operand of step t+1
+                const float st = __ldg(a.sched + t);
                 const float hi = row_ok ? __ldg(a.h + i) : 0.f;
 #pragma unroll 1
                 for (int c = half; c < nch; c += 2) {
@@ -317,7 +415,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     const int64_t base = (int64_t)r0 * a.ld + i;
                     float xo[16], mo[16];
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {  // L2 (cg): written by another SM
+                    for (int jj = 0; jj < 16; ++jj) {
                         const bool ok = row_ok && (r0 + jj) < a.R;
                         xo[jj] = ok ? ptx::ld_stream(xg + base + (int64_t)jj * a.ld, stream) : 0.f;
                         mo[jj] = ok ? ptx::ld_stream(mg + base + (int64_t)jj * a.ld, stream) : 0.f;
@@ -326,21 +424,46 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
                         const bool ok = row_ok && (r0 + jj) < a.R;
+                        const int64_t off = base + (int64_t)jj * a.ld;
                         const float f = O::mul(a.scale, __uint_as_float(v[jj]));
-                        const float grad = O::add(O::add(O::mul(lam, xo[jj]), f), hi);
-                        const float mn = O::sub(O::mul(a.alpha, mo[jj]), O::mul(a.eta, grad));
-                        float xn = O::add(xo[jj], mn);
-                        xn = xn < -1.f ? -1.f : (xn > 1.f ? 1.f : xn);
-                        if (ok) {
-                            const int64_t off = base + (int64_t)jj * a.ld;
-                            ptx::st_stream(xg + off, xn, stream);
-                            ptx::st_stream(mg + off, mn, stream);
-                            sg[off] = xn >= 0.f ? FP8_P1 : FP8_M1;
+                        if constexpr (KD == Kind::kFp8) {
+                            // PA: grad = (lam x + f) + h; m = alpha m - eta grad; x = clip
+                            const float grad = O::add(O::add(O::mul(st, xo[jj]), f), hi);
+                            const float mn = O::sub(O::mul(a.alpha, mo[jj]), O::mul(a.eta, grad));
+                            float xn = O::add(xo[jj], mn);
+                            xn = xn < -1.f ? -1.f : (xn > 1.f ? 1.f : xn);
+                            if (ok) {
+                                ptx::st_stream(xg + off, xn, stream);
+                                ptx::st_stream(mg + off, mn, stream);
+                                nxt[off] = xn >= 0.f ? FP8_P1 : FP8_M1;
+                            }
+                        } else {
+                            // SBM with B = -A = -c K, g = -h (field = -f)
+                            const float qi = xo[jj];
+                            const float inner = -O::sub(O::add(O::mul(qi, qi), a.a0), st);
+                            const float force =
+                                O::add(O::mul(inner, qi), O::mul(a.c0, O::add(-f, hi)));
+                            float pn = O::add(mo[jj], O::mul(a.dt, force));
+                            float qn = O::add(qi, O::mul(a.dta0, pn));
+                            if (fabsf(qn) > a.q_cap) {
+                                qn = qn < -a.q_cap ? -a.q_cap : a.q_cap;
+                                pn = 0.f;
+                            }
+                            if (ok) {
+                                ptx::st_stream(xg + off, qn, stream);
+                                ptx::st_stream(mg + off, pn, stream);
+                                __nv_bfloat16 q1, q2, q3;
+                                split3(qn, q1, q2, q3);
+                                __nv_bfloat16* pl = reinterpret_cast<__nv_bfloat16*>(nxt);
+                                pl[off] = q1;
+                                pl[a.plane_elems + off] = q2;
+                                pl[2 * a.plane_elems + off] = q3;
+                            }
                         }
                     }
                 }
             } else if (a.mode == 1) {
-                // energy pass: 2 q_r = sum_i s_i (K s)_i, exact integers
+                // energy pass (fp8 signs): 2 q_r = sum_i s_i (K s)_i, exact integers
 #pragma unroll 1
                 for (int c = half; c < nch; c += 2) {
                     uint32_t v[16];
@@ -380,6 +503,52 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 constexpr int TB = 256;
 inline unsigned nblk(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, TB)); }
 
+int num_sms() {
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return nsm;
+}
+
+// replica tile width bn: minimise tiles x per-k-block time, where a k-block costs
+// max(MMA = planes x 4 x 128*bn/256 = planes*2*bn, smem read (16 KB A + planes*128*bn B) /
+// 128 B/cyc) cycles.  The persistent kernel spreads all T steps' tiles over the SMs, so
+// per-step rounds do not matter.
+int choose_bn(int64_t n, int64_t R, int planes, int bn_max) {
+    const int64_t m_tiles = ceil_div(n, DBM);
+    int bn = bn_max;
+    int64_t best = INT64_MAX;
+    for (int cand = bn_max; cand >= 64; cand -= 16) {
+        const int64_t tiles = m_tiles * ceil_div(R, cand);
+        const int64_t cost =
+            tiles * std::max<int64_t>((int64_t)planes * 2 * cand, 128 + (int64_t)planes * cand);
+        if (cost < best) {
+            best = cost;
+            bn = cand;
+        }
+    }
+    if (const char* e = getenv("VXQ_DENSE_BN")) bn = std::max(16, std::min(bn_max, atoi(e) / 16 * 16));
+    return bn;
+}
+
+template <Kind KD>
+void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorMap& tmB1,
+                DenseRunArgs a, int64_t steps_for_grid, cudaStream_t s, bool cooperative) {
+    VXQ_CUDA(cudaFuncSetAttribute(k_dense_run<KD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  DSMEM));
+    const int64_t tiles = (int64_t)a.m_tiles * a.n_tiles * std::max<int64_t>(steps_for_grid, 1);
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, num_sms());
+    if (cooperative) {
+        // all CTAs must be co-resident (they wait on each other's tiles): one per SM
+        void* args[] = {(void*)&tmA, (void*)&tmB0, (void*)&tmB1, (void*)&a};
+        VXQ_CUDA(cudaLaunchCooperativeKernel((const void*)k_dense_run<KD>, dim3(grid),
+                                             dim3(DTHREADS), args, DSMEM, s));
+    } else {
+        k_dense_run<KD><<<grid, DTHREADS, DSMEM, s>>>(tmA, tmB0, tmB1, a);
+    }
+    VXQ_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 bool dense_eligible(const Problem* p, int64_t R) {
@@ -388,38 +557,104 @@ bool dense_eligible(const Problem* p, int64_t R) {
     return density >= 0.25;
 }
 
-DenseOperand* dense_operand(Problem* p, cudaStream_t s) {
+// Lazily build the sign matrix K (fp8 for PA/energies, bf16 for SBM) and its TMA maps.
+DenseOperand* dense_operand(Problem* p, cudaStream_t s, bool need_bf16) {
     std::lock_guard<std::mutex> g(p->mu);
-    if (p->dense) return p->dense;
     if (!p->uniform_magnitude)
         throw Error(VXQ_ERR_UNSUPPORTED, "dense tensor-core path needs uniform |J_ij|");
-    DenseOperand* d = new DenseOperand();
-    try {
+    DenseOperand* d = p->dense;
+    const bool fresh = d == nullptr;
+    if (fresh) {
+        d = new DenseOperand();
         d->n = p->n;
-        d->ld = ceil_div(p->n, DBK) * DBK;
+        d->ld = ceil_div(p->n, 128) * 128;
         d->scale = (float)p->magnitude;
-        VXQ_CUDA(cudaMalloc(&d->K, d->ld * d->ld));
-        VXQ_CUDA(cudaMemsetAsync(d->K, 0, d->ld * d->ld, s));
-        k_build_sign_matrix<<<(unsigned)ceil_div(p->n * 32, TB), TB, 0, s>>>(
-            p->n, d->ld, p->indptr, p->indices, p->data64, d->K);
-        VXQ_CHECK_LAUNCH();
-        d->tmA = make_map_u8(d->K, d->ld, d->ld, d->ld, DBK, DBM);
-        VXQ_CUDA(cudaStreamSynchronize(s));
+    }
+    try {
+        const int64_t ld = d->ld;
+        uint8_t* k8 = nullptr;
+        __nv_bfloat16* k16 = nullptr;
+        if (!d->K8) {
+            VXQ_CUDA(cudaMalloc(&d->K8, ld * ld));
+            VXQ_CUDA(cudaMemsetAsync(d->K8, 0, ld * ld, s));
+            k8 = d->K8;
+            d->tmA8 = make_map(d->K8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, ld, 1, DROW, DBM, 1);
+        }
+        if (need_bf16 && !d->K16) {
+            VXQ_CUDA(cudaMalloc(&d->K16, ld * ld * 2));
+            VXQ_CUDA(cudaMemsetAsync(d->K16, 0, ld * ld * 2, s));
+            k16 = d->K16;
+            d->tmA16 = make_map(d->K16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, ld, 1, DROW / 2,
+                                DBM, 1);
+        }
+        if (k8 || k16) {
+            k_build_sign_matrix<<<(unsigned)ceil_div(p->n * 32, TB), TB, 0, s>>>(
+                p->n, ld, p->indptr, p->indices, p->data64, k8, k16);
+            VXQ_CHECK_LAUNCH();
+            VXQ_CUDA(cudaStreamSynchronize(s));
+        }
     } catch (...) {
-        delete d;
+        if (fresh) delete d;
         throw;
     }
     p->dense = d;
     return d;
 }
 
+// fp8 energy pass over the signs of `x` ([R][ld]) -> q2 = 2 sum_{i<j} K_ij s_i s_j
+static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, long long* q2,
+                        cudaStream_t s, int64_t* launches) {
+    const int64_t ld = d->ld;
+    DevBuf<uint8_t> sg(R * ld, s);
+    VXQ_CUDA(cudaMemsetAsync(sg.get(), 0, R * ld, s));
+    k_signs_fp8_rm<<<nblk(n * R), TB, 0, s>>>(x, n, R, ld, sg.get());
+    VXQ_CUDA(cudaMemsetAsync(q2, 0, R * sizeof(long long), s));
+    const int bn = choose_bn(n, R, 1, KindTraits<Kind::kFp8>::kBnMax);
+    CUtensorMap tb = make_map(sg.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW, bn, 1);
+    DenseRunArgs e{};
+    e.n = (int)n;
+    e.R = (int)R;
+    e.ld = (int)ld;
+    e.kblocks = (int)(ld / DROW);
+    e.m_tiles = (int)ceil_div(n, DBM);
+    e.n_tiles = (int)ceil_div(R, bn);
+    e.bn = bn;
+    e.T = 1;
+    e.x = const_cast<float*>(x);
+    e.mode = 1;
+    e.q2 = q2;
+    launch_run<Kind::kFp8>(d->tmA8, tb, tb, e, 1, s, false);
+    *launches += 2;
+    VXQ_CUDA(cudaStreamSynchronize(s));
+}
+
+static double run_loop(const DenseRunArgs& a, const CUtensorMap& tmA, const CUtensorMap& tb0,
+                       const CUtensorMap& tb1, bool bf16, cudaStream_t s) {
+    cudaEvent_t e0, e1;
+    VXQ_CUDA(cudaEventCreate(&e0));
+    VXQ_CUDA(cudaEventCreate(&e1));
+    VXQ_CUDA(cudaEventRecord(e0, s));
+    if (a.T > 0) {
+        if (bf16) launch_run<Kind::kBf16x3>(tmA, tb0, tb1, a, a.T, s, true);
+        else launch_run<Kind::kFp8>(tmA, tb0, tb1, a, a.T, s, true);
+    }
+    VXQ_CUDA(cudaEventRecord(e1, s));
+    float ms = 0;
+    VXQ_CUDA(cudaEventSynchronize(e1));
+    VXQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms;
+}
+
 // Run the T-step PA loop on the tensor cores.  Outputs the final (x, m) in the interleaved
-// layout of dynamics.cu ([n][R_pad], V lanes) and the final sign bits sb[n][W].
+// layout of dynamics.cu ([n][R_pad], V lanes), the final sign bits sb[n][W] and, if q2 is
+// given, the exact coupling energy counts of the final spins.
 void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                    const std::vector<double>& sched, float eta, float alpha, uint64_t seed,
                    int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, long long* q2,
                    cudaStream_t s, double* loop_ms, int64_t* launches) {
-    DenseOperand* d = dense_operand(p, s);
+    DenseOperand* d = dense_operand(p, s, false);
     const int64_t n = p->n, ld = d->ld, T = (int64_t)sched.size();
     DevBuf<float> x(R * ld, s), m(R * ld, s);
     DevBuf<uint8_t> s0(R * ld, s), s1(R * ld, s);
@@ -428,41 +663,18 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     k_init_pa_rm<<<nblk(((n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, x.get(), m.get(),
                                                        s0.get());
     VXQ_CHECK_LAUNCH();
-    int nsm = 148;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    // replica tile width bn: minimise tiles x per-k-block time, where a k-block costs
-    // max(MMA 4 x 128*bn/256 = 2 bn, smem read (16 KB A + 128 bn B) / 128 B/cyc) cycles;
-    // bn >= 128 keeps the MMA (not shared-memory bandwidth) the limit.  The persistent
-    // kernel spreads all T steps' tiles over the SMs, so per-step rounds do not matter.
-    const int64_t m_tiles = ceil_div(n, DBM);
-    int bn = DBN;
-    int64_t best = INT64_MAX;
-    for (int cand = DBN; cand >= 128; cand -= 16) {
-        const int64_t tiles = m_tiles * ceil_div(R, cand);
-        const int64_t cost = tiles * std::max<int64_t>(2 * cand, 128 + cand);
-        if (cost < best) {
-            best = cost;
-            bn = cand;
-        }
-    }
-    if (const char* e = getenv("VXQ_DENSE_BN")) bn = std::max(16, std::min(DBN, atoi(e) / 16 * 16));
-    CUtensorMap tmB0 = make_map_u8(s0.get(), ld, R, ld, DBK, bn);
-    CUtensorMap tmB1 = make_map_u8(s1.get(), ld, R, ld, DBK, bn);
-    VXQ_CUDA(cudaFuncSetAttribute(k_dense_pa_run, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  DSMEM));
-    std::vector<float> lam32(T);
-    for (int64_t t = 0; t < T; ++t) lam32[t] = (float)sched[t];
-    DevBuf<float> lam(std::max<int64_t>(T, 1), s);
-    VXQ_CUDA(cudaMemcpyAsync(lam.get(), lam32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
-    DenseRunArgs a;
+    const int bn = choose_bn(n, R, 1, KindTraits<Kind::kFp8>::kBnMax);
+    CUtensorMap tmB0 = make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW, bn, 1);
+    CUtensorMap tmB1 = make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW, bn, 1);
+    std::vector<float> s32(T);
+    for (int64_t t = 0; t < T; ++t) s32[t] = (float)sched[t];
+    DevBuf<float> sc(std::max<int64_t>(T, 1), s);
+    VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
+    DenseRunArgs a{};
     a.n = (int)n;
     a.R = (int)R;
     a.ld = (int)ld;
-    a.kblocks = (int)(ld / DBK);
+    a.kblocks = (int)(ld / DROW);
     a.m_tiles = (int)ceil_div(n, DBM);
     a.n_tiles = (int)ceil_div(R, bn);
     a.bn = bn;
@@ -470,58 +682,88 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     a.scale = d->scale;
     a.eta = eta;
     a.alpha = alpha;
-    a.lam = lam.get();
+    a.sched = sc.get();
     a.h = p->h32;
     a.x = x.get();
     a.m = m.get();
-    a.s_buf[0] = s0.get();
-    a.s_buf[1] = s1.get();
-    a.mode = 0;
-    a.q2 = nullptr;
+    a.b_buf[0] = s0.get();
+    a.b_buf[1] = s1.get();
     const char* dbg = getenv("VXQ_DENSE_DEBUG_NOEPI");  // profiling knob: no-op epilogue
-    if (dbg && dbg[0] == '1') a.mode = 2;
+    a.mode = (dbg && dbg[0] == '1') ? 2 : 0;
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
-    const int64_t tiles_total = (int64_t)a.m_tiles * a.n_tiles * std::max<int64_t>(T, 1);
-    const unsigned grid = (unsigned)std::min<int64_t>(tiles_total, nsm);
-    cudaEvent_t e0, e1;
-    VXQ_CUDA(cudaEventCreate(&e0));
-    VXQ_CUDA(cudaEventCreate(&e1));
-    VXQ_CUDA(cudaEventRecord(e0, s));
-    if (T > 0) {
-        // all CTAs must be co-resident (they wait on each other's tiles): one per SM
-        void* args[] = {(void*)&d->tmA, (void*)&tmB0, (void*)&tmB1, (void*)&a};
-        VXQ_CUDA(cudaLaunchCooperativeKernel((const void*)k_dense_pa_run, dim3(grid),
-                                             dim3(DTHREADS), args, DSMEM, s));
-    }
-    VXQ_CHECK_LAUNCH();
-    VXQ_CUDA(cudaEventRecord(e1, s));
+    *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, s);
     *launches += 2;
-    if (q2) {
-        // one more tensor-core pass over s_T: 2 q_r = s_T . (K s_T), exact (energies)
-        VXQ_CUDA(cudaMemsetAsync(q2, 0, R * sizeof(long long), s));
-        DenseRunArgs e = a;
-        e.T = 1;
-        e.mode = 1;
-        e.q2 = q2;
-        const CUtensorMap& tb = (T & 1) ? tmB1 : tmB0;  // S_T
-        const unsigned eg = (unsigned)std::min<int64_t>((int64_t)a.m_tiles * a.n_tiles, nsm);
-        k_dense_pa_run<<<eg, DTHREADS, DSMEM, s>>>(d->tmA, tb, tb, e);
-        VXQ_CHECK_LAUNCH();
-        *launches += 1;
-    }
+    if (q2) energy_pass(d, x.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(x.get(), n, R, ld, R_pad, V, x_il);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(m.get(), n, R, ld, R_pad, V, m_il);
     k_pack_bits_rm<<<(unsigned)ceil_div(n * W * 32, TB), TB, 0, s>>>(x.get(), n, R, ld, W, sb);
     VXQ_CHECK_LAUNCH();
     *launches += 3;
-    float ms = 0;
-    VXQ_CUDA(cudaEventSynchronize(e1));
-    VXQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    *loop_ms = ms;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    VXQ_CUDA(cudaStreamSynchronize(s));
+}
+
+// Run the T-step SBM loop (B = -A, g = -h) on the tensor cores with bf16x3 q-splits.
+void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
+                    const std::vector<double>& a_sched, double dt, double a0, double c0,
+                    double q_cap, double amp, uint64_t seed, int64_t rbegin, float* q_il,
+                    float* p_il, uint32_t* sb, long long* q2, cudaStream_t s, double* loop_ms,
+                    int64_t* launches) {
+    DenseOperand* d = dense_operand(p, s, true);
+    const int64_t n = p->n, ld = d->ld, T = (int64_t)a_sched.size();
+    const int64_t plane = R * ld;
+    DevBuf<float> q(R * ld, s), pm(R * ld, s);
+    DevBuf<__nv_bfloat16> b0(3 * plane, s), b1(3 * plane, s);
+    VXQ_CUDA(cudaMemsetAsync(b0.get(), 0, 3 * plane * 2, s));
+    VXQ_CUDA(cudaMemsetAsync(b1.get(), 0, 3 * plane * 2, s));
+    k_init_sbm_rm<<<nblk(((2 * n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, amp,
+                                                            q.get(), pm.get(), b0.get());
+    VXQ_CHECK_LAUNCH();
+    const int bn = choose_bn(n, R, 3, KindTraits<Kind::kBf16x3>::kBnMax);
+    CUtensorMap tmB0 = make_map(b0.get(), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, R, 3,
+                                DROW / 2, bn, 3);
+    CUtensorMap tmB1 = make_map(b1.get(), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, R, 3,
+                                DROW / 2, bn, 3);
+    std::vector<float> s32(T);
+    for (int64_t t = 0; t < T; ++t) s32[t] = (float)a_sched[t];
+    DevBuf<float> sc(std::max<int64_t>(T, 1), s);
+    VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
+    DenseRunArgs a{};
+    a.n = (int)n;
+    a.R = (int)R;
+    a.ld = (int)ld;
+    a.kblocks = (int)(ld / (DROW / 2));
+    a.m_tiles = (int)ceil_div(n, DBM);
+    a.n_tiles = (int)ceil_div(R, bn);
+    a.bn = bn;
+    a.T = (int)T;
+    a.scale = d->scale;
+    a.dt = (float)dt;
+    a.a0 = (float)a0;
+    a.c0 = (float)c0;
+    a.dta0 = (float)(dt * a0);
+    a.q_cap = (float)q_cap;
+    a.sched = sc.get();
+    a.h = p->g32;  // g = -h
+    a.x = q.get();
+    a.m = pm.get();
+    a.b_buf[0] = reinterpret_cast<uint8_t*>(b0.get());
+    a.b_buf[1] = reinterpret_cast<uint8_t*>(b1.get());
+    a.plane_elems = plane;
+    a.mode = 0;
+    DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
+    VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
+    a.done = done.get();
+    *loop_ms = run_loop(a, d->tmA16, tmB0, tmB1, true, s);
+    *launches += 2;
+    if (q2) energy_pass(d, q.get(), n, R, q2, s, launches);
+    k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(q.get(), n, R, ld, R_pad, V, q_il);
+    k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(pm.get(), n, R, ld, R_pad, V, p_il);
+    k_pack_bits_rm<<<(unsigned)ceil_div(n * W * 32, TB), TB, 0, s>>>(q.get(), n, R, ld, W, sb);
+    VXQ_CHECK_LAUNCH();
+    *launches += 3;
+    VXQ_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace vxq

@@ -774,11 +774,30 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
         n, L.R_pad, L.V, prm->seed, rbegin, prm->init_noise, q.get(), pm.get());
     VXQ_CHECK_LAUNCH();
     ++launches;
+    const int req = opts ? opts->path : 0;
+    if constexpr (sizeof(T) == 8) {
+        if (req == VXQ_PATH_DENSE)
+            throw Error(VXQ_ERR_UNSUPPORTED, "dense tensor-core path is fp32 only");
+    }
+    const bool dense = sizeof(T) == 4 && (req == VXQ_PATH_DENSE ||
+                                          (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+    if (dense) {
+        DevBuf<long long> qq(R, s);
+        if constexpr (sizeof(T) == 4) {
+            dense_sbm_loop(p, R, L.R_pad, L.V, L.W, sched, prm->dt, prm->a0, c0, prm->q_cap,
+                           prm->init_noise, prm->seed, rbegin, q.get(), pm.get(), sb.get(),
+                           qq.get(), s, &out->loop_ms, &launches);
+        }
+        out->path_used = VXQ_PATH_DENSE;
+        finish_outputs<T>(p, L, sb.get(), q.get(), pm.get(), opts, out, s, qq.get());
+        out->launches = launches + 4;
+        return;
+    }
     Operator<T> op = problem_operator<T>(p, (T)-1);  // B = -A
     const T* g = pick<T>(p->g64, p->g32);            // g = -h
     T* qf = nullptr;
-    sbm_run_core<T>(p, L, op, g, sched, prm->dt, prm->a0, c0, prm->q_cap, opts ? opts->path : 0,
-                    p->nnz, q.get(), q2.get(), pm.get(), out, launches, s, &qf);
+    sbm_run_core<T>(p, L, op, g, sched, prm->dt, prm->a0, c0, prm->q_cap, req, p->nnz,
+                    q.get(), q2.get(), pm.get(), out, launches, s, &qf);
     launch_pack<T>(L, qf, sb.get(), s);
     ++launches;
     finish_outputs<T>(p, L, sb.get(), qf, pm.get(), opts, out, s);

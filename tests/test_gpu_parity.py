@@ -288,6 +288,26 @@ def test_dense_tensor_core_path_bitexact_with_emulation(n, R):
     assert np.array_equal(r.energies, O.energies_exact(m, r.states))
 
 
+@pytest.mark.parametrize("n,R", [(1000, 256), (700, 200)])
+def test_dense_sbm_tensor_core_short_horizon(n, R):
+    """SBM on the tensor cores (bf16x3 exact q-splits, f32 accumulation) tracks the fp64
+    restatement of the reference loop within the fp32 tolerance for t <= 30."""
+    m = sk_model(n, 6)
+    c0 = 0.02
+    r = vxq.run_sbm(m, vxq.SbmParams(steps=30, dt=0.05, replicas=R, seed=2, c0=c0),
+                    want_state=True)
+    assert r.info["path"] == "dense"
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    Q, P = O.sbm_init(2, 8, m.n, 1.0)
+    Q, P = O.sbm_run(ip, ix, -dv, -m.h, O.sbm_schedule(1.0, 30), 0.05, 1.0, c0, 1.0, Q, P)
+    assert np.abs(r.x[:8] - Q).max() <= 1e-4
+    assert np.abs(r.m[:8] - P).max() <= 1e-4
+    assert np.array_equal(r.energies, O.energies_exact(m, r.states))
+    s = vxq.run_sbm(m, vxq.SbmParams(steps=30, dt=0.05, replicas=R, seed=2, c0=c0),
+                    path="sparse", want_state=True)
+    assert np.abs(r.x - s.x).max() <= 1e-4
+
+
 def test_dense_vs_sparse_same_dynamics_quality():
     m = sk_model(1024, 5)
     d = vxq.run_pa(m, vxq.PaParams(steps=300, replicas=256, seed=1), path="dense")
