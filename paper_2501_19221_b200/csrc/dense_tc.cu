@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -243,7 +244,31 @@ struct DenseRunArgs {
     int mode;                // 0: dynamics steps, 1: energy pass over b_buf[0] (q2), 2: no-op
     long long* q2;           // [R] 2 * sum_{i<j} K_ij s_i s_j  (mode 1)
     unsigned* done;          // [T][n_tiles] finished row-tiles per (step, replica block)
+    int group;               // replica blocks interleaved per row block (A-panel reuse)
+    unsigned long long* stats;  // optional [8] wait-cycle counters (VXQ_DENSE_STATS=1)
 };
+
+// stats slots: 0 producer<-empty, 1 producer<-dependency, 2 mma<-full, 3 mma<-tempty,
+//              4 epilogue<-tfull, 5 epilogue busy, 6 tiles, 7 kernel cycles (max CTA)
+__device__ __forceinline__ long long clk() {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    return c;
+}
+
+// Tile g -> (step t, replica block nb, row block mb).  Within a step, replica blocks are
+// processed in groups of `group`: the group's tiles for one row block are adjacent, so they
+// run concurrently and share the A panel (J rows) through L2, while earlier groups still
+// complete early enough for the next step to start on them.
+__device__ __forceinline__ void decode_tile(const DenseRunArgs& a, int g, int tps, int mrows,
+                                            int& t, int& nb, int& mb) {
+    t = g / tps;
+    const int rem = g % tps;
+    const int per_group = mrows * a.group;
+    const int grp = rem / per_group, w = rem % per_group;
+    mb = w / a.group;
+    nb = grp * a.group + w % a.group;
+}
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     unsigned v;
@@ -251,7 +276,10 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     return v;
 }
 
-template <Kind KD>
+// CL = CTAs per cluster along the row dimension: the CL CTAs of a cluster process row
+// blocks mb = CL*p + rank of the same (step, replica block) and each TMA-multicasts 1/CL of
+// the shared B tile into all of them, cutting L2->SM traffic for B by CL.
+template <Kind KD, int CL>
 __global__ void __launch_bounds__(DTHREADS, 1)
     k_dense_run(const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB0,
@@ -269,10 +297,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long t_start = clk();
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(full + s, 1);
-            ptx::mbar_init(empty + s, 1);
+            ptx::mbar_init(empty + s, CL);  // released by the MMA of every CTA in the cluster
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(tfull + s, 1);
@@ -285,30 +314,48 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     }
     if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL > 1) ptx::cluster_sync();  // peers' barriers initialised before use
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int tps = a.m_tiles * a.n_tiles;  // tiles per step
+    const int crank = CL > 1 ? (int)ptx::cluster_ctarank() : 0;
+    const int wid0 = blockIdx.x / CL, wstride = gridDim.x / CL;  // cluster work index
+    const int mrows = (a.m_tiles + CL - 1) / CL;                 // row-block groups per step
+    const int tps = mrows * a.n_tiles;                           // work items per step
     const int num_tiles = tps * a.T;
     const uint32_t b_plane_bytes = (uint32_t)a.bn * DROW;
+    constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
     if (warp == 0) {
         // ---------------- TMA producer
         if (ptx::elect_one()) {
             const uint64_t keep = ptx::policy_evict_last();  // K and B stay in L2
+            long long st_empty = 0, st_dep = 0;
             int stage = 0;
             uint32_t ph = 0;
-            for (int g = blockIdx.x; g < num_tiles; g += gridDim.x) {
-                const int t = g / tps, rem = g % tps;
-                const int nb = rem / a.m_tiles, mb = rem % a.m_tiles;
+            for (int g = wid0; g < num_tiles; g += wstride) {
+                int t, nb, mb;
+                decode_tile(a, g, tps, mrows, t, nb, mb);
+                mb = mb * CL + crank;
                 const CUtensorMap* tmB = (t & 1) ? &tmB1 : &tmB0;
+                // A (the coupling panel) never depends on the dynamics: keep kPrefetch
+                // k-blocks of it on their way into L2 ahead of the smem loads
+                constexpr int kPrefetch = 8;
+                for (int kb = 0; kb < kPrefetch && kb < a.kblocks; ++kb)
+                    ptx::tma_prefetch_2d(&tmA, kb * (DROW / TR::kElemBytes), mb * DBM);
                 for (int kb = 0; kb < a.kblocks; ++kb) {
+                    if (kb + kPrefetch < a.kblocks)
+                        ptx::tma_prefetch_2d(&tmA, (kb + kPrefetch) * (DROW / TR::kElemBytes),
+                                             mb * DBM);
+                    long long c0 = a.stats ? clk() : 0;
                     ptx::mbar_wait(empty + stage, ph ^ 1);
+                    if (a.stats) st_empty += clk() - c0;
                     uint8_t* sa = smem + stage * SBYTES;
                     ptx::mbar_arrive_expect_tx(full + stage, DA_BYTES + TR::kPlanes * b_plane_bytes);
                     const int kcol = kb * (DROW / TR::kElemBytes);
                     ptx::tma_load_2d_hint(sa, &tmA, full + stage, kcol, mb * DBM, keep);
                     if (kb == 0 && t > 0) {
+                        const long long c1 = a.stats ? clk() : 0;
                         // B_t[nb] complete? (release/acquire on the step t-1 counter, then a
                         // proxy fence so the async-proxy TMA sees the generic-proxy stores)
                         const unsigned* cnt = a.done + (size_t)(t - 1) * a.n_tiles + nb;
@@ -322,18 +369,30 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             }
                         }
                         asm volatile("fence.proxy.async.global;" ::: "memory");
+                        if (a.stats) st_dep += clk() - c1;
                     }
-                    if constexpr (TR::kPlanes == 1)
+                    if constexpr (CL > 1) {
+                        static_assert(TR::kPlanes == 1, "B multicast: single-plane B only");
+                        const int hrows = a.bn / CL;
+                        ptx::tma_load_2d_mc(sa + DA_BYTES + crank * hrows * DROW, tmB,
+                                            full + stage, kcol, nb * a.bn + crank * hrows, kMask,
+                                            keep);
+                    } else if constexpr (TR::kPlanes == 1) {
                         ptx::tma_load_2d_hint(sa + DA_BYTES, tmB, full + stage, kcol,
                                               nb * a.bn, keep);
-                    else
+                    } else {
                         ptx::tma_load_3d_hint(sa + DA_BYTES, tmB, full + stage, kcol,
                                               nb * a.bn, 0, keep);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         ph ^= 1;
                     }
                 }
+            }
+            if (a.stats) {
+                atomicAdd(a.stats + 0, (unsigned long long)st_empty);
+                atomicAdd(a.stats + 1, (unsigned long long)st_dep);
             }
         }
     } else if (warp == 1) {
@@ -343,14 +402,19 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         int stage = 0;
         uint32_t ph = 0;
         int lt = 0;
-        for (int g = blockIdx.x; g < num_tiles; g += gridDim.x, ++lt) {
+        long long mm_full = 0, mm_tempty = 0;
+        for (int g = wid0; g < num_tiles; g += wstride, ++lt) {
             const int acc = lt & 1;
             const uint32_t acc_ph = (lt >> 1) & 1;
+            long long c0 = a.stats ? clk() : 0;
             ptx::mbar_wait(tempty + acc, acc_ph ^ 1);
+            if (a.stats) mm_tempty += clk() - c0;
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + acc * 256;
             for (int kb = 0; kb < a.kblocks; ++kb) {
+                c0 = a.stats ? clk() : 0;
                 ptx::mbar_wait(full + stage, ph);
+                if (a.stats) mm_full += clk() - c0;
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
                     const uint32_t sa = ptx::smem_u32(smem + stage * SBYTES);
@@ -368,7 +432,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                                 ptx::mma_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
                         }
                     }
-                    ptx::mma_commit(empty + stage);
+                    if constexpr (CL > 1) ptx::mma_commit_mc(empty + stage, kMask);
+                    else ptx::mma_commit(empty + stage);
                 }
                 __syncwarp();
                 if (++stage == STAGES) {
@@ -378,6 +443,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             }
             if (ptx::elect_one()) ptx::mma_commit(tfull + acc);
             __syncwarp();
+        }
+        if (a.stats && lane == 0) {
+            atomicAdd(a.stats + 2, (unsigned long long)mm_full);
+            atomicAdd(a.stats + 3, (unsigned long long)mm_tempty);
+            atomicAdd(a.stats + 6, (unsigned long long)lt);
         }
     } else {
         // ---------------- epilogue (8 warps): TMEM -> integrator -> next B operand
@@ -392,15 +462,21 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         float* __restrict__ xg = a.x;
         float* __restrict__ mg = a.m;
         int lt = 0;
-        for (int g = blockIdx.x; g < num_tiles; g += gridDim.x, ++lt) {
-            const int t = g / tps, rem = g % tps;
-            const int nb = rem / a.m_tiles, mb = rem % a.m_tiles;
+        long long ep_wait = 0, ep_busy = 0;
+        for (int g = wid0; g < num_tiles; g += wstride, ++lt) {
+            int t, nb, mb;
+            decode_tile(a, g, tps, mrows, t, nb, mb);
+            mb = mb * CL + crank;
+            const bool tile_ok = mb < a.m_tiles;  // last cluster row group may be partial
             const int acc = lt & 1;
             const uint32_t acc_ph = (lt >> 1) & 1;
             const int i = mb * DBM + row;
             const bool row_ok = i < a.n;
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+            long long c0 = (a.stats && ep_tid == 0) ? clk() : 0;
             ptx::mbar_wait(tfull + acc, acc_ph);
+            long long c1 = (a.stats && ep_tid == 0) ? clk() : 0;
+            if (a.stats && ep_tid == 0) ep_wait += c1 - c0;
             ptx::tc_fence_after();
             if (a.mode == 0) {
                 const uint64_t stream = ptx::policy_evict_first();
@@ -484,9 +560,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     }
                 }
             }
+            if (a.stats && ep_tid == 0) ep_busy += clk() - c1;
             ptx::tc_fence_before();
             ptx::mbar_arrive(tempty + acc);
-            if (a.mode == 0 && t + 1 < a.T) {
+            if (a.mode != 1 && tile_ok && t + 1 < a.T) {
                 // publish: all 256 epilogue threads' stores, then one release increment
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 if (ep_tid == 0) {
@@ -495,8 +572,14 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 }
             }
         }
+        if (a.stats && ep_tid == 0) {
+            atomicAdd(a.stats + 4, (unsigned long long)ep_wait);
+            atomicAdd(a.stats + 5, (unsigned long long)ep_busy);
+        }
     }
     __syncthreads();
+    if (a.stats && threadIdx.x == 0) atomicMax(a.stats + 7, (unsigned long long)(clk() - t_start));
+    if constexpr (CL > 1) ptx::cluster_sync();  // no CTA exits while peers still signal it
     if (warp == 1) ptx::tmem_dealloc<512>(tmem_base);
 }
 
@@ -531,21 +614,44 @@ int choose_bn(int64_t n, int64_t R, int planes, int bn_max) {
     return bn;
 }
 
-template <Kind KD>
+int pick_group(int n_tiles) {
+    int gsz = 1;
+    if (const char* e = getenv("VXQ_DENSE_GROUP")) gsz = std::max(1, atoi(e));
+    while (gsz > 1 && n_tiles % gsz) --gsz;
+    return gsz;
+}
+
+template <Kind KD, int CL>
 void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorMap& tmB1,
                 DenseRunArgs a, int64_t steps_for_grid, cudaStream_t s, bool cooperative) {
-    VXQ_CUDA(cudaFuncSetAttribute(k_dense_run<KD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  DSMEM));
-    const int64_t tiles = (int64_t)a.m_tiles * a.n_tiles * std::max<int64_t>(steps_for_grid, 1);
-    const unsigned grid = (unsigned)std::min<int64_t>(tiles, num_sms());
+    auto kern = k_dense_run<KD, CL>;
+    VXQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM));
+    const int64_t items = (int64_t)((a.m_tiles + CL - 1) / CL) * a.n_tiles *
+                          std::max<int64_t>(steps_for_grid, 1);
+    const int64_t clusters = std::min<int64_t>(items, num_sms() / CL);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(clusters * CL));
+    cfg.blockDim = dim3(DTHREADS);
+    cfg.dynamicSmemBytes = DSMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[2];
+    int na = 0;
+    if (CL > 1) {
+        attrs[na].id = cudaLaunchAttributeClusterDimension;
+        attrs[na].val.clusterDim.x = CL;
+        attrs[na].val.clusterDim.y = 1;
+        attrs[na].val.clusterDim.z = 1;
+        ++na;
+    }
     if (cooperative) {
         // all CTAs must be co-resident (they wait on each other's tiles): one per SM
-        void* args[] = {(void*)&tmA, (void*)&tmB0, (void*)&tmB1, (void*)&a};
-        VXQ_CUDA(cudaLaunchCooperativeKernel((const void*)k_dense_run<KD>, dim3(grid),
-                                             dim3(DTHREADS), args, DSMEM, s));
-    } else {
-        k_dense_run<KD><<<grid, DTHREADS, DSMEM, s>>>(tmA, tmB0, tmB1, a);
+        attrs[na].id = cudaLaunchAttributeCooperative;
+        attrs[na].val.cooperative = 1;
+        ++na;
     }
+    cfg.attrs = attrs;
+    cfg.numAttrs = na;
+    VXQ_CUDA(cudaLaunchKernelEx(&cfg, kern, tmA, tmB0, tmB1, a));
     VXQ_CHECK_LAUNCH();
 }
 
@@ -623,20 +729,29 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
     e.x = const_cast<float*>(x);
     e.mode = 1;
     e.q2 = q2;
-    launch_run<Kind::kFp8>(d->tmA8, tb, tb, e, 1, s, false);
+    e.group = 1;
+    launch_run<Kind::kFp8, 1>(d->tmA8, tb, tb, e, 1, s, false);
     *launches += 2;
     VXQ_CUDA(cudaStreamSynchronize(s));
 }
 
-static double run_loop(const DenseRunArgs& a, const CUtensorMap& tmA, const CUtensorMap& tb0,
-                       const CUtensorMap& tb1, bool bf16, cudaStream_t s) {
+static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap& tb0,
+                       const CUtensorMap& tb1, bool bf16, int cl, cudaStream_t s) {
+    const char* want = getenv("VXQ_DENSE_STATS");
+    DevBuf<unsigned long long> stats;
+    if (want && want[0] == '1') {
+        stats = DevBuf<unsigned long long>(8, s);
+        VXQ_CUDA(cudaMemsetAsync(stats.get(), 0, 8 * sizeof(unsigned long long), s));
+        a.stats = stats.get();
+    }
     cudaEvent_t e0, e1;
     VXQ_CUDA(cudaEventCreate(&e0));
     VXQ_CUDA(cudaEventCreate(&e1));
     VXQ_CUDA(cudaEventRecord(e0, s));
     if (a.T > 0) {
-        if (bf16) launch_run<Kind::kBf16x3>(tmA, tb0, tb1, a, a.T, s, true);
-        else launch_run<Kind::kFp8>(tmA, tb0, tb1, a, a.T, s, true);
+        if (bf16) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (cl == 2) launch_run<Kind::kFp8, 2>(tmA, tb0, tb1, a, a.T, s, true);
+        else launch_run<Kind::kFp8, 1>(tmA, tb0, tb1, a, a.T, s, true);
     }
     VXQ_CUDA(cudaEventRecord(e1, s));
     float ms = 0;
@@ -644,6 +759,17 @@ static double run_loop(const DenseRunArgs& a, const CUtensorMap& tmA, const CUte
     VXQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (a.stats) {
+        unsigned long long h[8];
+        VXQ_CUDA(cudaMemcpy(h, a.stats, sizeof(h), cudaMemcpyDeviceToHost));
+        const double ctas = (double)std::min<int64_t>((int64_t)a.m_tiles * a.n_tiles * a.T,
+                                                      num_sms());
+        fprintf(stderr,
+                "[vxq dense stats] kernel %.0f cyc | per CTA: prod<-empty %.0f, prod<-dep %.0f, "
+                "mma<-full %.0f, mma<-tempty %.0f, epi<-tfull %.0f, epi busy %.0f | tiles %llu\n",
+                (double)h[7], h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas,
+                h[5] / ctas, h[6]);
+    }
     return ms;
 }
 
@@ -664,8 +790,13 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                                                        s0.get());
     VXQ_CHECK_LAUNCH();
     const int bn = choose_bn(n, R, 1, KindTraits<Kind::kFp8>::kBnMax);
-    CUtensorMap tmB0 = make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW, bn, 1);
-    CUtensorMap tmB1 = make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW, bn, 1);
+    int cl = 2;  // B multicast across a 2-CTA cluster
+    if (const char* e = getenv("VXQ_DENSE_CLUSTER")) cl = atoi(e) == 2 ? 2 : 1;
+    if (ceil_div(n, DBM) < 2) cl = 1;
+    CUtensorMap tmB0 = make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW,
+                                bn / cl, 1);
+    CUtensorMap tmB1 = make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW,
+                                bn / cl, 1);
     std::vector<float> s32(T);
     for (int64_t t = 0; t < T; ++t) s32[t] = (float)sched[t];
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
@@ -688,12 +819,13 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     a.m = m.get();
     a.b_buf[0] = s0.get();
     a.b_buf[1] = s1.get();
+    a.group = pick_group(a.n_tiles);
     const char* dbg = getenv("VXQ_DENSE_DEBUG_NOEPI");  // profiling knob: no-op epilogue
     a.mode = (dbg && dbg[0] == '1') ? 2 : 0;
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
-    *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, s);
+    *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, cl, s);
     *launches += 2;
     if (q2) energy_pass(d, x.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(x.get(), n, R, ld, R_pad, V, x_il);
@@ -751,11 +883,12 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     a.b_buf[0] = reinterpret_cast<uint8_t*>(b0.get());
     a.b_buf[1] = reinterpret_cast<uint8_t*>(b1.get());
     a.plane_elems = plane;
+    a.group = pick_group(a.n_tiles);
     a.mode = 0;
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
-    *loop_ms = run_loop(a, d->tmA16, tmB0, tmB1, true, s);
+    *loop_ms = run_loop(a, d->tmA16, tmB0, tmB1, true, 1, s);
     *launches += 2;
     if (q2) energy_pass(d, q.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(q.get(), n, R, ld, R_pad, V, q_il);
