@@ -136,6 +136,26 @@ VXQ_API int vxq_sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t
                       double* P, const double* a_sched, int64_t T, double dt, double a0,
                       double c0, double q_cap, const vxq_run_opts* opts);
 
+/* ---- Row-partitioned solves (multi-GPU): one session per rank ----
+ * The rank updates rows [row_begin, row_end) of every replica each step; every row's state
+ * is read from an exchange buffer (caller-owned device memory, rows_alloc x row_bytes,
+ * globally row-indexed: PA = sign bits, SBM = q) that the caller all-gathers between steps
+ * (e.g. NCCL all_gather over NVLink).  Buffer k & 1 holds state k: create() writes the
+ * local rows of state 0; step(t) reads buffer t & 1 and writes the local rows of buffer
+ * (t+1) & 1 on opts->stream.  finish() needs the final buffer complete on every row and
+ * returns states/energies of all replicas (x/m outputs must be NULL).
+ * solver: 0 = PA (pa params), 1 = SBM (sbm params).                                  */
+typedef struct vxq_session vxq_session;
+VXQ_API int vxq_exchange_row_bytes(int32_t solver, int64_t replicas, int32_t precision,
+                                   int64_t* out);
+VXQ_API int vxq_session_create(vxq_problem* p, int32_t solver, const vxq_pa_params* pa,
+                               const vxq_sbm_params* sbm, int64_t row_begin, int64_t row_end,
+                               int64_t rows_alloc, void* xbuf0, void* xbuf1,
+                               const vxq_run_opts* opts, vxq_session** out);
+VXQ_API int vxq_session_step(vxq_session* s, int64_t t);
+VXQ_API int vxq_session_finish(vxq_session* s, vxq_outputs* out);
+VXQ_API int vxq_session_destroy(vxq_session* s);
+
 /* Exact energies of R spin states [R][n] int8 (host, or device if
  * opts->outputs_on_device) -> energies[R] (same residency). */
 VXQ_API int vxq_energies(vxq_problem* p, const int8_t* states, int64_t R, double* energies,

@@ -31,7 +31,8 @@ EXPORTS = (
     "vxq_problem_create", "vxq_problem_destroy", "vxq_problem_info", "vxq_problem_lambda0",
     "vxq_problem_c0", "vxq_pa_solve", "vxq_sbm_solve", "vxq_sbm_integrate", "vxq_energies",
     "vxq_pa_schedule", "vxq_sbm_schedule", "vxq_last_error", "vxq_abi_version",
-    "vxq_device_count",
+    "vxq_device_count", "vxq_exchange_row_bytes", "vxq_session_create", "vxq_session_step",
+    "vxq_session_finish", "vxq_session_destroy",
 )
 
 
@@ -90,6 +91,13 @@ def load():
         L.vxq_energies.argtypes = [P, P, i64, P, ctypes.POINTER(RunOptsC)]
         L.vxq_pa_schedule.argtypes = [f64, i64, P]
         L.vxq_sbm_schedule.argtypes = [f64, i64, P]
+        L.vxq_exchange_row_bytes.argtypes = [i32, i64, i32, ctypes.POINTER(i64)]
+        L.vxq_session_create.argtypes = [P, i32, ctypes.POINTER(PaParamsC),
+                                         ctypes.POINTER(SbmParamsC), i64, i64, i64, P, P,
+                                         ctypes.POINTER(RunOptsC), ctypes.POINTER(P)]
+        L.vxq_session_step.argtypes = [P, i64]
+        L.vxq_session_finish.argtypes = [P, ctypes.POINTER(OutputsC)]
+        L.vxq_session_destroy.argtypes = [P]
         L.vxq_last_error.restype = ctypes.c_char_p
         L.vxq_abi_version.restype = ctypes.c_int
         L.vxq_device_count.restype = ctypes.c_int

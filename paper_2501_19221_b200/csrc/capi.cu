@@ -46,6 +46,15 @@ struct vxq_problem {
     vxq::Problem* p;
 };
 
+namespace {
+struct SessionBox {
+    vxq::Session* S;
+    int device;
+    vxq_run_opts opts;
+};
+void retain_mempool_public() { vxq::retain_mempool(); }
+}  // namespace
+
 extern "C" {
 
 int vxq_abi_version(void) { return VXQ_ABI_VERSION; }
@@ -206,6 +215,66 @@ int vxq_energies(vxq_problem* p, const int8_t* states, int64_t R, double* energi
         if (!on_dev)
             VXQ_CUDA(cudaMemcpyAsync(energies, ed, R * sizeof(double), cudaMemcpyDeviceToHost, s));
         VXQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int vxq_exchange_row_bytes(int32_t solver, int64_t replicas, int32_t precision, int64_t* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(out && replicas > 0 && (solver == 0 || solver == 1), "invalid arguments");
+        *out = vxq::exchange_row_bytes(solver, replicas, precision);
+    });
+}
+
+int vxq_session_create(vxq_problem* p, int32_t solver, const vxq_pa_params* pa,
+                       const vxq_sbm_params* sbm, int64_t row_begin, int64_t row_end,
+                       int64_t rows_alloc, void* xbuf0, void* xbuf1, const vxq_run_opts* opts,
+                       vxq_session** out) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && out && (solver == 0 ? pa != nullptr : sbm != nullptr), "null argument");
+        *out = nullptr;
+        VXQ_CUDA(cudaSetDevice(p->p->device));
+        retain_mempool_public();
+        cudaStream_t st = opts && opts->stream ? (cudaStream_t)opts->stream : nullptr;
+        bool own = false;
+        if (!st) {
+            VXQ_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            own = true;
+        }
+        vxq::Session* S = vxq::session_create(p->p, solver, pa, sbm, row_begin, row_end,
+                                              rows_alloc, xbuf0, xbuf1, opts, st);
+        vxq::session_set_own_stream(S, own);
+        *out = reinterpret_cast<vxq_session*>(new SessionBox{S, p->p->device,
+                                                             opts ? *opts : vxq_run_opts{}});
+    });
+}
+
+int vxq_session_step(vxq_session* s, int64_t t) {
+    return guarded([&] {
+        VXQ_REQUIRE(s, "null session");
+        SessionBox* b = reinterpret_cast<SessionBox*>(s);
+        VXQ_CUDA(cudaSetDevice(b->device));
+        vxq::session_step(b->S, t);
+    });
+}
+
+int vxq_session_finish(vxq_session* s, vxq_outputs* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(s, "null session");
+        check_outputs(out);
+        VXQ_REQUIRE(!out->x && !out->m, "session outputs: x/m must be NULL");
+        SessionBox* b = reinterpret_cast<SessionBox*>(s);
+        VXQ_CUDA(cudaSetDevice(b->device));
+        vxq::session_finish(b->S, out, &b->opts);
+    });
+}
+
+int vxq_session_destroy(vxq_session* s) {
+    return guarded([&] {
+        if (!s) return;
+        SessionBox* b = reinterpret_cast<SessionBox*>(s);
+        cudaSetDevice(b->device);
+        vxq::session_destroy(b->S);
+        delete b;
     });
 }
 

@@ -21,6 +21,7 @@
 //   one 16-byte vector access and the V sign words of the chunk come out of V ballots.
 //   sign bits sb[i][W], W = R_pad / 32: bit (r % 32) of word r / 32 (natural order).
 #include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "vxq_internal.h"
@@ -46,42 +47,55 @@ __device__ __forceinline__ int64_t pos_of(int64_t r, int V) {
 }
 
 // ------------------------------------------------------------------ init (Philox)
+// rows [row0, row0 + nrows) of x/m (local indexing); draw k of stream r is row k
 template <typename T>
-__global__ void k_init_pa(int64_t n, int64_t R_pad, int V, uint64_t seed, int64_t rbegin,
-                          T* __restrict__ x, T* __restrict__ m) {
+__global__ void k_init_pa(int64_t row0, int64_t nrows, int64_t R_pad, int V, uint64_t seed,
+                          int64_t rbegin, T* __restrict__ x, T* __restrict__ m) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int64_t nq = (n + 3) / 4;
-    if (idx >= nq * R_pad) return;
-    int64_t q = idx / R_pad, r = idx % R_pad;
+    const int64_t q0 = row0 / 4, q1 = (row0 + nrows + 3) / 4;
+    if (idx >= (q1 - q0) * R_pad) return;
+    int64_t q = q0 + idx / R_pad, r = idx % R_pad;
     U64x4 o = philox4x64_10((uint64_t)q + 1, 0, (uint64_t)(rbegin + r), 0, seed, 0);
     int64_t p = pos_of(r, V);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
         int64_t i = 4 * q + w;
-        if (i < n) {
+        if (i >= row0 && i < row0 + nrows) {
             double v = uniform_from_raw(o.v[w], -1.0, 2.0);  // uniform(-1, 1)
-            x[i * R_pad + p] = (T)v;
-            m[i * R_pad + p] = (T)0;
+            x[(i - row0) * R_pad + p] = (T)v;
+            m[(i - row0) * R_pad + p] = (T)0;
         }
     }
 }
 
+// q of rows [row0, row0+nrows) into the full (global-row) buffer q, p into the local pm;
+// stream r draws n q-values then n p-values (bifurcation.py:60-61)
 template <typename T>
-__global__ void k_init_sbm(int64_t n, int64_t R_pad, int V, uint64_t seed, int64_t rbegin,
-                           double amp, T* __restrict__ q, T* __restrict__ pm) {
+__global__ void k_init_sbm(int64_t n, int64_t row0, int64_t nrows, int64_t R_pad, int V,
+                           uint64_t seed, int64_t rbegin, double amp, T* __restrict__ q,
+                           T* __restrict__ pm) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nq = (2 * n + 3) / 4;
     if (idx >= nq * R_pad) return;
     int64_t qd = idx / R_pad, r = idx % R_pad;
+    // skip quads with no local row among their draws
+    const int64_t k0 = 4 * qd, k1 = k0 + 3;
+    const bool q_hit = k0 < row0 + nrows && k1 >= row0;
+    const bool p_hit = k0 < n + row0 + nrows && k1 >= n + row0;
+    if (!q_hit && !p_hit) return;
     U64x4 o = philox4x64_10((uint64_t)qd + 1, 0, (uint64_t)(rbegin + r), 0, seed, 0);
     int64_t p = pos_of(r, V);
     const double lo = -amp, range = __dadd_rn(amp, amp);  // hi - lo
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-        int64_t k = 4 * qd + w;
+        int64_t k = k0 + w;
         double v = uniform_from_raw(o.v[w], lo, range);
-        if (k < n) q[k * R_pad + p] = (T)v;
-        else if (k < 2 * n) pm[(k - n) * R_pad + p] = (T)v;
+        if (k < n) {
+            if (k >= row0 && k < row0 + nrows) q[k * R_pad + p] = (T)v;
+        } else if (k < 2 * n) {
+            const int64_t i = k - n;
+            if (i >= row0 && i < row0 + nrows) pm[(i - row0) * R_pad + p] = (T)v;
+        }
     }
 }
 
@@ -107,30 +121,33 @@ __global__ void k_export(const T* __restrict__ src, int64_t n, int64_t R, int64_
 
 // sign bits of the final analog state
 template <typename T, int V>
-__global__ void k_pack_signs(const T* __restrict__ x, int64_t n, int64_t R_pad,
+__global__ void k_pack_signs(const T* __restrict__ x, int64_t row0, int64_t nrows, int64_t R_pad,
                              uint32_t* __restrict__ sb) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int chunks = (int)(R_pad / (32 * V));
-    const int64_t i = warp / chunks;
+    const int64_t il = warp / chunks;
     const int c = (int)(warp % chunks);
-    if (i >= n) return;
-    Vec<T, V> xv = *reinterpret_cast<const Vec<T, V>*>(x + lane_base(i, R_pad, c, lane, V));
+    if (il >= nrows) return;
+    Vec<T, V> xv = *reinterpret_cast<const Vec<T, V>*>(x + lane_base(il, R_pad, c, lane, V));
     const int64_t W = R_pad / 32;
 #pragma unroll
     for (int b = 0; b < V; ++b) {
         uint32_t word = __ballot_sync(0xffffffffu, xv.v[b] >= (T)0);
-        if (lane == b) sb[i * W + c * V + b] = word;
+        if (lane == b) sb[(row0 + il) * W + c * V + b] = word;
     }
 }
 
 // ------------------------------------------------------------------ PA step (sparse)
 // One warp owns row i and CPW consecutive replica chunks (CPW * 32 * V replicas): the CSR
 // row is read once for all of them and CPW x more loads are in flight per warp.
+// Rows [row0, row0 + nrows): x/m are indexed locally (row - row0), the CSR, h and the
+// sign-bit buffers by global row (a row-partitioned rank reads every row's spins).
 template <typename T, int V, int CPW>
-__global__ void __launch_bounds__(256) k_pa_step(int64_t n, int64_t R_pad, Operator<T> op,
-                                                 const T* __restrict__ h, T lam, T eta, T alpha,
-                                                 T* __restrict__ x, T* __restrict__ m,
+__global__ void __launch_bounds__(256) k_pa_step(int64_t row0, int64_t nrows, int64_t R_pad,
+                                                 Operator<T> op, const T* __restrict__ h,
+                                                 T lam, T eta, T alpha, T* __restrict__ x,
+                                                 T* __restrict__ m,
                                                  const uint32_t* __restrict__ sb_in,
                                                  uint32_t* __restrict__ sb_out) {
     using O = Ops<T>;
@@ -138,14 +155,15 @@ __global__ void __launch_bounds__(256) k_pa_step(int64_t n, int64_t R_pad, Opera
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int groups = (int)(R_pad / (32 * NB));
-    const int64_t i = warp / groups;
+    const int64_t il = warp / groups;
     const int c0 = (int)(warp % groups) * CPW;
-    if (i >= n) return;
+    if (il >= nrows) return;
+    const int64_t i = row0 + il;
     const int64_t W = R_pad / 32;
     Vec<T, V> xv[CPW], mv[CPW];
 #pragma unroll
     for (int g = 0; g < CPW; ++g) {
-        const int64_t base = lane_base(i, R_pad, c0 + g, lane, V);
+        const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
         xv[g] = *reinterpret_cast<const Vec<T, V>*>(x + base);
         mv[g] = *reinterpret_cast<const Vec<T, V>*>(m + base);
     }
@@ -207,7 +225,7 @@ __global__ void __launch_bounds__(256) k_pa_step(int64_t n, int64_t R_pad, Opera
             uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
             if (lane == g * V + b) sb_out[i * W + c0 * V + g * V + b] = word;
         }
-        const int64_t base = lane_base(i, R_pad, c0 + g, lane, V);
+        const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
         *reinterpret_cast<Vec<T, V>*>(x + base) = xv[g];
         *reinterpret_cast<Vec<T, V>*>(m + base) = mv[g];
     }
@@ -219,20 +237,23 @@ struct SbmScalars {
     T a_t, dt, a0, c0, dta0, q_cap;
 };
 
+// Rows [row0, row0 + nrows): q_in/q_out are full (global-row) buffers, p is local.
 template <typename T, int V>
-__global__ void __launch_bounds__(256) k_sbm_step(int64_t n, int64_t R_pad, Operator<T> op,
-                                                  const T* __restrict__ g, SbmScalars<T> sc,
-                                                  const T* __restrict__ q_in,
+__global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, int64_t R_pad,
+                                                  Operator<T> op, const T* __restrict__ g,
+                                                  SbmScalars<T> sc, const T* __restrict__ q_in,
                                                   T* __restrict__ q_out, T* __restrict__ p) {
     using O = Ops<T>;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int chunks = (int)(R_pad / (32 * V));
-    const int64_t i = warp / chunks;
+    const int64_t il = warp / chunks;
     const int c = (int)(warp % chunks);
-    if (i >= n) return;
+    if (il >= nrows) return;
+    const int64_t i = row0 + il;
     const int64_t off = (int64_t)c * 32 * V + (int64_t)lane * V;
     const int64_t base = i * R_pad + off;
+    const int64_t pbase = il * R_pad + off;
     T f[V];
 #pragma unroll
     for (int b = 0; b < V; ++b) f[b] = (T)0;
@@ -263,7 +284,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t n, int64_t R_pad, Oper
         for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a, qv.v[b]));
     }
     Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(q_in + base);
-    Vec<T, V> pv = *reinterpret_cast<const Vec<T, V>*>(p + base);
+    Vec<T, V> pv = *reinterpret_cast<const Vec<T, V>*>(p + pbase);
     const T gi = __ldg(g + i);
 #pragma unroll
     for (int b = 0; b < V; ++b) {
@@ -280,7 +301,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t n, int64_t R_pad, Oper
         pv.v[b] = pn;
     }
     *reinterpret_cast<Vec<T, V>*>(q_out + base) = qv;
-    *reinterpret_cast<Vec<T, V>*>(p + base) = pv;
+    *reinterpret_cast<Vec<T, V>*>(p + pbase) = pv;
 }
 
 // ------------------------------------------------------------------ resident (small n)
@@ -428,6 +449,7 @@ inline unsigned nblk(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div
 struct Layout {
     int64_t n, R, R_pad, W;
     int V;
+    int64_t row0 = 0, nrows = 0;  // rows this launch updates (row partition), default all
 };
 
 Layout make_layout(int64_t n, int64_t R, bool fp64) {
@@ -439,6 +461,8 @@ Layout make_layout(int64_t n, int64_t R, bool fp64) {
     int64_t ch = 32 * L.V;
     L.R_pad = ceil_div(R, ch) * ch;
     L.W = L.R_pad / 32;
+    L.row0 = 0;
+    L.nrows = n;
     return L;
 }
 
@@ -481,10 +505,11 @@ void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T
                     T* x, T* m, const uint32_t* sbi, uint32_t* sbo, cudaStream_t s) {
     const int64_t chunks = L.R_pad / (32 * L.V);
     const int cpw = (chunks % 2 == 0) ? 2 : 1;  // two chunks per warp when they pair up
-    const int64_t warps = L.n * (chunks / cpw);
+    const int64_t warps = L.nrows * (chunks / cpw);
     const unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
-#define VXQ_PA_STEP(VV, CC) \
-    k_pa_step<T, VV, CC><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, h, lam, eta, alpha, x, m, sbi, sbo)
+#define VXQ_PA_STEP(VV, CC)                                                                \
+    k_pa_step<T, VV, CC><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, h, lam, eta, \
+                                                alpha, x, m, sbi, sbo)
     if (L.V == 1) {
         if (cpw == 2) VXQ_PA_STEP(1, 2); else VXQ_PA_STEP(1, 1);
     } else if (L.V == 2) {
@@ -500,27 +525,27 @@ void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T
 template <typename T>
 void launch_sbm_step(const Layout& L, const Operator<T>& op, const T* g, SbmScalars<T> sc,
                      const T* qi, T* qo, T* p, cudaStream_t s) {
-    int64_t warps = L.n * (L.R_pad / (32 * L.V));
+    int64_t warps = L.nrows * (L.R_pad / (32 * L.V));
     unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
     switch (L.V) {
-        case 1: k_sbm_step<T, 1><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, g, sc, qi, qo, p); break;
-        case 2: k_sbm_step<T, 2><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, g, sc, qi, qo, p); break;
+        case 1: k_sbm_step<T, 1><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, qo, p); break;
+        case 2: k_sbm_step<T, 2><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, qo, p); break;
         default:
             if constexpr (sizeof(T) == 4)
-                k_sbm_step<T, 4><<<blocks, 256, 0, s>>>(L.n, L.R_pad, op, g, sc, qi, qo, p);
+                k_sbm_step<T, 4><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, qo, p);
             break;
     }
 }
 
 template <typename T>
 void launch_pack(const Layout& L, const T* x, uint32_t* sb, cudaStream_t s) {
-    int64_t warps = L.n * (L.R_pad / (32 * L.V));
+    int64_t warps = L.nrows * (L.R_pad / (32 * L.V));
     unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
     switch (L.V) {
-        case 1: k_pack_signs<T, 1><<<blocks, 256, 0, s>>>(x, L.n, L.R_pad, sb); break;
-        case 2: k_pack_signs<T, 2><<<blocks, 256, 0, s>>>(x, L.n, L.R_pad, sb); break;
+        case 1: k_pack_signs<T, 1><<<blocks, 256, 0, s>>>(x, L.row0, L.nrows, L.R_pad, sb); break;
+        case 2: k_pack_signs<T, 2><<<blocks, 256, 0, s>>>(x, L.row0, L.nrows, L.R_pad, sb); break;
         default:
-            if constexpr (sizeof(T) == 4) k_pack_signs<T, 4><<<blocks, 256, 0, s>>>(x, L.n, L.R_pad, sb);
+            if constexpr (sizeof(T) == 4) k_pack_signs<T, 4><<<blocks, 256, 0, s>>>(x, L.row0, L.nrows, L.R_pad, sb);
             break;
     }
     VXQ_CHECK_LAUNCH();
@@ -641,8 +666,8 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     DevBuf<T> x(n * L.R_pad, s), m(n * L.R_pad, s);
     DevBuf<uint32_t> sbA(n * L.W, s), sbB(n * L.W, s);
     int64_t launches = 0;
-    k_init_pa<T><<<nblk(((n + 3) / 4) * L.R_pad), TB, 0, s>>>(n, L.R_pad, L.V, prm->seed, rbegin,
-                                                            x.get(), m.get());
+    k_init_pa<T><<<nblk(((n + 3) / 4 + 1) * L.R_pad), TB, 0, s>>>(0, n, L.R_pad, L.V, prm->seed,
+                                                                rbegin, x.get(), m.get());
     VXQ_CHECK_LAUNCH();
     ++launches;
     Operator<T> op = problem_operator<T>(p, (T)1);
@@ -771,7 +796,7 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
     DevBuf<uint32_t> sb(n * L.W, s);
     int64_t launches = 0;
     k_init_sbm<T><<<nblk(((2 * n + 3) / 4) * L.R_pad), TB, 0, s>>>(
-        n, L.R_pad, L.V, prm->seed, rbegin, prm->init_noise, q.get(), pm.get());
+        n, 0, n, L.R_pad, L.V, prm->seed, rbegin, prm->init_noise, q.get(), pm.get());
     VXQ_CHECK_LAUNCH();
     ++launches;
     const int req = opts ? opts->path : 0;
@@ -882,5 +907,172 @@ void sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indice
         integrate_t<float>(n, bt_indptr, bt_indices, bt_data, g, R, Q, P, a_sched, T_, dt, a0,
                            c0, q_cap, opts, s);
 }
+
+}  // namespace vxq
+
+// ====================================================================== row-partitioned sessions
+// One rank of a row-partitioned solve: this process updates rows
+// [row0, row0 + nrows) of every replica each step and reads every row's state from an
+// exchange buffer that the caller all-gathers between steps (NCCL over NVLink):
+//   PA : sign bits  [rows_alloc][W] uint32      (1 bit per replica-variable)
+//   SBM: q          [rows_alloc][R_pad] fp32/64 (interleaved replica layout)
+// Buffer k & 1 holds state k; init writes state 0 (local rows), step t reads buffer t & 1
+// and writes the local rows of buffer (t + 1) & 1.
+namespace vxq {
+
+struct Session {
+    Problem* p = nullptr;
+    int solver = 0;  // 0 PA, 1 SBM
+    int prec = VXQ_FP32;
+    Layout L;
+    int64_t rows_alloc = 0, rbegin = 0;
+    uint64_t seed = 0;
+    void* xb[2] = {nullptr, nullptr};
+    void* x = nullptr;  // PA x / SBM p (local rows)
+    void* m = nullptr;  // PA m (local rows)
+    std::vector<double> sched;
+    double eta = 0, alpha = 0, lam0 = 0;                          // PA
+    double dt = 0, a0 = 0, c0 = 0, q_cap = 0, amp = 0;            // SBM
+    cudaStream_t s = nullptr;
+    bool own_stream = false;
+    ~Session() {
+        if (x) cudaFree(x);
+        if (m) cudaFree(m);
+        if (own_stream && s) cudaStreamDestroy(s);
+    }
+};
+
+int64_t exchange_row_bytes(int solver, int64_t R, int prec) {
+    Layout L = make_layout(1, R, prec == VXQ_FP64);
+    if (solver == 0) return L.W * 4;
+    return L.R_pad * (prec == VXQ_FP64 ? 8 : 4);
+}
+
+namespace {
+template <typename T>
+void session_init_t(Session* S) {
+    const Layout& L = S->L;
+    const int64_t n = S->p->n;
+    VXQ_CUDA(cudaMalloc(&S->x, std::max<int64_t>(L.nrows, 1) * L.R_pad * sizeof(T)));
+    if (S->solver == 0) {
+        VXQ_CUDA(cudaMalloc(&S->m, std::max<int64_t>(L.nrows, 1) * L.R_pad * sizeof(T)));
+        k_init_pa<T><<<nblk(((L.nrows + 3) / 4 + 1) * L.R_pad), TB, 0, S->s>>>(
+            L.row0, L.nrows, L.R_pad, L.V, S->seed, S->rbegin, (T*)S->x, (T*)S->m);
+        VXQ_CHECK_LAUNCH();
+        launch_pack<T>(L, (const T*)S->x, (uint32_t*)S->xb[0], S->s);
+    } else {
+        k_init_sbm<T><<<nblk(((2 * n + 3) / 4) * L.R_pad), TB, 0, S->s>>>(
+            n, L.row0, L.nrows, L.R_pad, L.V, S->seed, S->rbegin, S->amp, (T*)S->xb[0],
+            (T*)S->x);
+        VXQ_CHECK_LAUNCH();
+    }
+}
+
+template <typename T>
+void session_step_t(Session* S, int64_t t) {
+    const Layout& L = S->L;
+    if (S->solver == 0) {
+        Operator<T> op = problem_operator<T>(S->p, (T)1);
+        launch_pa_step<T>(L, op, pick<T>(S->p->h64, S->p->h32), (T)S->sched[t], (T)S->eta,
+                          (T)S->alpha, (T*)S->x, (T*)S->m, (const uint32_t*)S->xb[t & 1],
+                          (uint32_t*)S->xb[(t + 1) & 1], S->s);
+    } else {
+        SbmScalars<T> sc;
+        sc.a_t = (T)S->sched[t];
+        sc.dt = (T)S->dt;
+        sc.a0 = (T)S->a0;
+        sc.c0 = (T)S->c0;
+        sc.dta0 = (T)(S->dt * S->a0);
+        sc.q_cap = (T)S->q_cap;
+        Operator<T> op = problem_operator<T>(S->p, (T)-1);
+        launch_sbm_step<T>(L, op, pick<T>(S->p->g64, S->p->g32), sc, (const T*)S->xb[t & 1],
+                           (T*)S->xb[(t + 1) & 1], (T*)S->x, S->s);
+    }
+    VXQ_CHECK_LAUNCH();
+}
+
+template <typename T>
+void session_finish_t(Session* S, int64_t T_, vxq_outputs* out, const vxq_run_opts* opts) {
+    // full final state: PA sign bits / SBM q in buffer T & 1 (all rows, after the gather)
+    Layout F = S->L;
+    F.row0 = 0;
+    F.nrows = S->p->n;
+    const uint32_t* sb = nullptr;
+    DevBuf<uint32_t> tmp;
+    if (S->solver == 0) {
+        sb = (const uint32_t*)S->xb[T_ & 1];
+    } else {
+        tmp = DevBuf<uint32_t>(S->p->n * F.W, S->s);
+        launch_pack<T>(F, (const T*)S->xb[T_ & 1], tmp.get(), S->s);
+        sb = tmp.get();
+    }
+    vxq_outputs o = *out;
+    o.x = nullptr;
+    o.m = nullptr;
+    finish_outputs<T>(S->p, F, sb, (const T*)nullptr, (const T*)nullptr, opts, &o, S->s);
+    out->loop_ms = 0;
+    out->path_used = VXQ_PATH_SPARSE;
+}
+}  // namespace
+
+Session* session_create(Problem* p, int solver, const vxq_pa_params* pa,
+                        const vxq_sbm_params* sbm, int64_t row_begin, int64_t row_end,
+                        int64_t rows_alloc, void* xbuf0, void* xbuf1, const vxq_run_opts* opts,
+                        cudaStream_t s) {
+    VXQ_REQUIRE(solver == 0 || solver == 1, "solver must be 0 (PA) or 1 (SBM)");
+    VXQ_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= p->n, "bad row range");
+    VXQ_REQUIRE(rows_alloc >= p->n, "rows_alloc must be >= n");
+    VXQ_REQUIRE(xbuf0 && xbuf1, "exchange buffers required");
+    auto S = std::make_unique<Session>();
+    S->p = p;
+    S->solver = solver;
+    S->prec = opts ? opts->precision : VXQ_FP32;
+    const int64_t R = solver == 0 ? pa->replicas : sbm->replicas;
+    const int64_t T_ = solver == 0 ? pa->steps : sbm->steps;
+    S->L = make_layout(p->n, R, S->prec == VXQ_FP64);
+    S->L.row0 = row_begin;
+    S->L.nrows = row_end - row_begin;
+    S->rows_alloc = rows_alloc;
+    S->rbegin = opts ? opts->replica_begin : 0;
+    S->xb[0] = xbuf0;
+    S->xb[1] = xbuf1;
+    S->s = s;
+    S->sched.resize(T_);
+    if (solver == 0) {
+        S->seed = pa->seed;
+        S->eta = pa->learning_rate;
+        S->alpha = pa->momentum;
+        S->lam0 = std::isnan(pa->lambda0) ? problem_lambda0(p, s) : pa->lambda0;
+        pa_schedule(S->lam0, T_, S->sched.data());
+    } else {
+        S->seed = sbm->seed;
+        S->dt = sbm->dt;
+        S->a0 = sbm->a0;
+        S->c0 = std::isnan(sbm->c0) ? problem_c0(p, s) : sbm->c0;
+        S->q_cap = sbm->q_cap;
+        S->amp = sbm->init_noise;
+        sbm_schedule(S->a0, T_, S->sched.data());
+    }
+    if (S->prec == VXQ_FP64) session_init_t<double>(S.get());
+    else session_init_t<float>(S.get());
+    return S.release();
+}
+
+void session_step(Session* S, int64_t t) {
+    VXQ_REQUIRE(t >= 0 && t < (int64_t)S->sched.size(), "step index out of range");
+    if (S->prec == VXQ_FP64) session_step_t<double>(S, t);
+    else session_step_t<float>(S, t);
+}
+
+void session_finish(Session* S, vxq_outputs* out, const vxq_run_opts* opts) {
+    const int64_t T_ = (int64_t)S->sched.size();
+    if (S->prec == VXQ_FP64) session_finish_t<double>(S, T_, out, opts);
+    else session_finish_t<float>(S, T_, out, opts);
+    out->lambda0_used = S->lam0;
+    out->c0_used = S->c0;
+}
+
+void session_destroy(Session* S) { delete S; }
+void session_set_own_stream(Session* S, bool own) { S->own_stream = own; }
 
 }  // namespace vxq

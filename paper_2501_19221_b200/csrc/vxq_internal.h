@@ -149,6 +149,18 @@ void sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indice
                    const double* a_sched, int64_t T_, double dt, double a0, double c0,
                    double q_cap, const vxq_run_opts* opts, cudaStream_t s);
 
+// row-partitioned sessions (dynamics.cu)
+struct Session;
+int64_t exchange_row_bytes(int solver, int64_t R, int prec);
+Session* session_create(Problem* p, int solver, const vxq_pa_params* pa,
+                        const vxq_sbm_params* sbm, int64_t row_begin, int64_t row_end,
+                        int64_t rows_alloc, void* xbuf0, void* xbuf1, const vxq_run_opts* opts,
+                        cudaStream_t s);
+void session_step(Session* S, int64_t t);
+void session_finish(Session* S, vxq_outputs* out, const vxq_run_opts* opts);
+void session_destroy(Session* S);
+void session_set_own_stream(Session* S, bool own);
+
 // ---- dense_tc.cu (tcgen05 path)
 bool dense_eligible(const Problem* p, int64_t R);
 void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,

@@ -1,0 +1,154 @@
+"""Row-partitioned multi-GPU solves (BASELINE config 5).
+
+Instances too large for replica sharding (up to 2e8 variables) are split by rows: rank g
+owns rows [g*B, min(n, (g+1)*B)) with B = ceil(n / world) and updates them for every
+replica each step; the step needs every row's state, so after each step the ranks
+all-gather the exchange buffer (NCCL over NVLink):
+
+    PA : the bit-packed spins, n * R / 8 bytes per step (1 bit per replica-variable)
+    SBM: the fp32 positions q,  4 * n * R bytes per step (32x larger: SBM is exchange-bound)
+
+Buffer k & 1 holds state k.  `drive()` is the per-step loop; it takes any session with
+`step(t)` and an in-place gather, so the multi-rank logic is exercised on CPU with gloo
+(tests/test_distributed.py) while the product path runs `vxq_session_*` kernels on the
+GPU with NCCL.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _lib
+from .device import get_problem
+from .errors import ValidationError
+from .solvers import Sample, SampleSet, _opts, _seed
+
+
+def row_split(n: int, world: int) -> tuple[list[tuple[int, int]], int]:
+    """Equal contiguous row blocks (the exchange all-gather needs equal chunk sizes)."""
+    B = -(-int(n) // int(world))
+    return [(min(n, g * B), min(n, (g + 1) * B)) for g in range(world)], B
+
+
+def gather_inplace(buf, rank: int, world: int, chunk_bytes: int, group=None):
+    """All-gather chunk `rank` of `buf` (uint8 tensor, world * chunk_bytes) in place."""
+    import torch.distributed as dist
+    if world == 1:
+        return
+    dist.all_gather_into_tensor(buf, buf[rank * chunk_bytes:(rank + 1) * chunk_bytes],
+                                group=group)
+
+
+def drive(session, bufs, T: int, gather) -> None:
+    """The row-partitioned loop: state 0 exchange, then step t / exchange t+1."""
+    gather(bufs[0])
+    for t in range(T):
+        session.step(t)
+        gather(bufs[(t + 1) & 1])
+
+
+class GpuSession:
+    """One rank's vxq_session (GPU kernels over rows [row_begin, row_end))."""
+
+    def __init__(self, model, solver: str, params, row_begin, row_end, rows_alloc, bufs,
+                 precision="fp32", device=0, stream=None, replica_begin=0):
+        L = _lib.load()
+        dp = get_problem(model, device)
+        self._dp = dp
+        opts = _opts(precision, "sparse", replica_begin, stream=stream)
+        self._opts = opts
+        pa = sbm = None
+        if solver == "pa":
+            pa = _lib.PaParamsC(int(params.steps), float(params.learning_rate),
+                                float(params.momentum), _lib.nan_if_none(params.lambda0),
+                                int(params.replicas), _seed(params.seed))
+        else:
+            sbm = _lib.SbmParamsC(int(params.steps), float(params.dt), float(params.a0),
+                                  _lib.nan_if_none(params.c0), float(params.q_cap),
+                                  float(params.init_noise), int(params.replicas),
+                                  _seed(params.seed))
+        h = ctypes.c_void_p()
+        _lib.check(L.vxq_session_create(dp.handle, 0 if solver == "pa" else 1,
+                                        ctypes.byref(pa) if pa else None,
+                                        ctypes.byref(sbm) if sbm else None, int(row_begin),
+                                        int(row_end), int(rows_alloc),
+                                        ctypes.c_void_p(bufs[0].data_ptr()),
+                                        ctypes.c_void_p(bufs[1].data_ptr()), ctypes.byref(opts),
+                                        ctypes.byref(h)))
+        self.handle = h
+        self.R = int(params.replicas)
+        self.n = int(model.n)
+
+    def step(self, t: int):
+        _lib.check(_lib.load().vxq_session_step(self.handle, int(t)))
+
+    def finish(self):
+        st = np.empty((self.R, self.n), dtype=np.int8)
+        en = np.empty(self.R)
+        order = np.empty(self.R, dtype=np.int64)
+        out = _lib.OutputsC()
+        out.states, out.energies, out.order = _lib.ptr(st), _lib.ptr(en), _lib.ptr(order)
+        _lib.check(_lib.load().vxq_session_finish(self.handle, ctypes.byref(out)))
+        return st, en, order, {"lambda0": out.lambda0_used, "c0": out.c0_used}
+
+    def close(self):
+        if self.handle:
+            _lib.load().vxq_session_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+
+def exchange_row_bytes(solver: str, replicas: int, precision: str = "fp32") -> int:
+    v = ctypes.c_int64()
+    _lib.check(_lib.load().vxq_exchange_row_bytes(0 if solver == "pa" else 1, int(replicas),
+                                                  1 if precision == "fp64" else 0,
+                                                  ctypes.byref(v)))
+    return int(v.value)
+
+
+def solve_rowpart(solver: str, model, params, group=None, precision: str = "fp32",
+                  timing: dict | None = None) -> SampleSet:
+    """Row-partitioned PA/SBM over the ranks of `group` (one GPU per rank, NCCL exchange).
+
+    Every rank returns the same best-first SampleSet.  With a single rank this is the
+    ordinary sparse path (bit-identical)."""
+    import torch
+    import torch.distributed as dist
+
+    if solver not in ("pa", "sbm"):
+        raise ValidationError("solver must be 'pa' or 'sbm'")
+    params.validate()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    dev = torch.cuda.current_device()
+    n = int(model.n)
+    spans, B = row_split(n, world)
+    rb = exchange_row_bytes(solver, params.replicas, precision)
+    rows_alloc = B * world
+    bufs = [torch.zeros(rows_alloc * rb, dtype=torch.uint8, device=f"cuda:{dev}")
+            for _ in range(2)]
+    stream = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    sess = GpuSession(model, solver, params, spans[rank][0], spans[rank][1], rows_alloc, bufs,
+                      precision, dev, stream.cuda_stream)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    drive(sess, bufs, int(params.steps),
+          lambda b: gather_inplace(b, rank, world, B * rb, group))
+    ev1.record(stream)
+    st, en, order, info = sess.finish()
+    sess.close()
+    if timing is not None:
+        torch.cuda.synchronize()
+        timing["loop_ms"] = ev0.elapsed_time(ev1)
+        timing["exchange_bytes_per_step"] = rows_alloc * rb
+    samples = [Sample(st[r].copy(), float(en[r]), int(r)) for r in order]
+    return SampleSet(samples=samples, replica_count=int(params.replicas), seed=params.seed,
+                     wall_time=time.perf_counter() - t0,
+                     info={**info, "world": world, "rank": rank, "rows": spans[rank],
+                           "path": "rowpart"})

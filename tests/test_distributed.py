@@ -86,3 +86,86 @@ def test_replica_sharded_merge_equals_single_process(total):
         assert np.array_equal(np.array(energies), en[order])
         assert np.array_equal(np.array(states, dtype=np.int8), st[order])
     assert out[0][3] == shard_range(total, world, 0) and out[1][3] == shard_range(total, world, 1)
+
+
+# ---------------------------------------------------------------- row partition (config 5)
+class _OracleRowSession:
+    """numpy stand-in for one rank's vxq_session (PA, fp64): same exchange-buffer protocol
+    (sign bits, [rows_alloc][W] uint32, bit r%32 of word r/32) as the GPU kernels."""
+
+    def __init__(self, model, R, T, seed, rb, re, bufs):
+        self.ip, self.ix, self.dv = O.symmetric_csr(model.n, model.rows, model.cols,
+                                                     model.values)
+        self.h = np.asarray(model.h)
+        self.lam = O.pa_schedule(O.resolve_lambda0(model), T)
+        self.rb, self.re, self.R = rb, re, R
+        self.W = (R + 31) // 32
+        X = np.stack([O.uniform(seed, r, 0, model.n, -1.0, 1.0) for r in range(R)])
+        self.x = X[:, rb:re].copy()
+        self.m = np.zeros_like(self.x)
+        self.bufs = bufs
+        self._write(0, self.x)
+
+    def _words(self, k):
+        return self.bufs[k & 1].numpy().view(np.uint32).reshape(-1, self.W)
+
+    def _write(self, k, x):
+        bits = (x >= 0)  # (R, local rows)
+        words = np.zeros((self.re - self.rb, self.W), dtype=np.uint32)
+        for r in range(self.R):
+            words[:, r // 32] |= (bits[r].astype(np.uint32) << np.uint32(r % 32))
+        self._words(k)[self.rb:self.re] = words
+
+    def _spins(self, k):
+        words = self._words(k)
+        r = np.arange(self.R)
+        bits = (words[:, r // 32] >> (r % 32).astype(np.uint32)) & 1  # (rows_alloc, R)
+        return np.where(bits == 1, 1.0, -1.0).T
+
+    def step(self, t):
+        S = self._spins(t)
+        for li, i in enumerate(range(self.rb, self.re)):
+            f = np.zeros(self.R)
+            for k in range(self.ip[i], self.ip[i + 1]):
+                f = f + self.dv[k] * S[:, self.ix[k]]
+            grad = (self.lam[t] * self.x[:, li] + f) + self.h[i]
+            self.m[:, li] = 0.9 * self.m[:, li] - 0.05 * grad
+            self.x[:, li] = np.clip(self.x[:, li] + self.m[:, li], -1.0, 1.0)
+        self._write(t + 1, self.x)
+
+
+def _rowpart_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_19221_b200.rowpart import drive, gather_inplace, row_split
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = _model()
+        R, T = 40, 25
+        spans, B = row_split(m.n, world)
+        W = (R + 31) // 32
+        row_bytes = 4 * W
+        bufs = [torch.zeros(B * world * row_bytes, dtype=torch.uint8) for _ in range(2)]
+        sess = _OracleRowSession(m, R, T, 3, spans[rank][0], spans[rank][1], bufs)
+        drive(sess, bufs, T, lambda b: gather_inplace(b, rank, world, B * row_bytes))
+        out[rank] = sess._spins(T)[:, : m.n].astype(np.int8).tolist()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_partitioned_exchange_equals_single_process():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_rowpart_worker, args=(world, _free_port(), out), nprocs=world,
+                       join=True, start_method="spawn")
+    m = _model()
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    X = O.pa_init(3, 40, m.n)
+    X, _ = O.pa_run(ip, ix, dv, m.h, O.pa_schedule(O.resolve_lambda0(m), 25), 0.05, 0.9, X,
+                    np.zeros_like(X))
+    want = O.sign_pm(X)
+    for rank in range(world):
+        assert np.array_equal(np.array(out[rank], dtype=np.int8), want)
