@@ -118,6 +118,16 @@ VXQ_API int vxq_problem_create(int64_t n, int64_t num_couplings, const int64_t* 
                        const int64_t* cols, const double* values, const double* h,
                        double offset, int device, vxq_problem** out);
 VXQ_API int vxq_problem_destroy(vxq_problem* p);
+/* Generate an instance directly on the device (no host arrays).
+ * family 0 = "qubo_deg6": random QUBO with mean degree ~6 (three seeded circulant offsets
+ * per variable, duplicates merged), Q ~ U[-1,1), converted like qubo_to_ising
+ * (transforms.py:36-56) -- BASELINE config 5 at n = 2e8.  Definition: csrc/generate.cu. */
+VXQ_API int vxq_problem_generate(int32_t family, int64_t n, uint64_t seed, int device,
+                                 vxq_problem** out);
+/* Copy the canonical model back (host or device pointers, any may be NULL): couplings
+ * rows/cols/values [num_couplings] (i<j, sorted), h [n], offset. */
+VXQ_API int vxq_problem_export(const vxq_problem* p, int64_t* rows, int64_t* cols,
+                               double* values, double* h, double* offset);
 /* info: [n, num_couplings, nnz_sym, dense_eligible, uniform_magnitude] */
 VXQ_API int vxq_problem_info(const vxq_problem* p, int64_t* info5);
 

@@ -32,7 +32,7 @@ EXPORTS = (
     "vxq_problem_c0", "vxq_pa_solve", "vxq_sbm_solve", "vxq_sbm_integrate", "vxq_energies",
     "vxq_pa_schedule", "vxq_sbm_schedule", "vxq_last_error", "vxq_abi_version",
     "vxq_device_count", "vxq_exchange_row_bytes", "vxq_session_create", "vxq_session_step",
-    "vxq_session_finish", "vxq_session_destroy",
+    "vxq_session_finish", "vxq_session_destroy", "vxq_problem_generate", "vxq_problem_export",
 )
 
 
@@ -79,6 +79,8 @@ def load():
         L.vxq_problem_create.argtypes = [i64, i64, P, P, P, P, f64, ctypes.c_int,
                                          ctypes.POINTER(P)]
         L.vxq_problem_destroy.argtypes = [P]
+        L.vxq_problem_generate.argtypes = [i32, i64, u64, ctypes.c_int, ctypes.POINTER(P)]
+        L.vxq_problem_export.argtypes = [P, P, P, P, P, ctypes.POINTER(f64)]
         L.vxq_problem_info.argtypes = [P, P]
         L.vxq_problem_lambda0.argtypes = [P, ctypes.POINTER(f64)]
         L.vxq_problem_c0.argtypes = [P, ctypes.POINTER(f64)]

@@ -97,6 +97,28 @@ int vxq_problem_create(int64_t n, int64_t num_couplings, const int64_t* rows,
     });
 }
 
+int vxq_problem_generate(int32_t family, int64_t n, uint64_t seed, int device,
+                         vxq_problem** out) {
+    return guarded([&] {
+        VXQ_REQUIRE(out != nullptr, "out must not be null");
+        *out = nullptr;
+        int ndev = 0;
+        VXQ_CUDA(cudaGetDeviceCount(&ndev));
+        VXQ_REQUIRE(device >= 0 && device < ndev, "invalid CUDA device ordinal");
+        DeviceGuard dg(device);
+        *out = new vxq_problem{vxq::problem_generate(family, n, seed, device)};
+    });
+}
+
+int vxq_problem_export(const vxq_problem* p, int64_t* rows, int64_t* cols, double* values,
+                       double* h, double* offset) {
+    return guarded([&] {
+        VXQ_REQUIRE(p, "null problem");
+        DeviceGuard dg(p->p->device);
+        vxq::problem_export(p->p, rows, cols, values, h, offset);
+    });
+}
+
 int vxq_problem_destroy(vxq_problem* p) {
     return guarded([&] {
         if (!p) return;

@@ -16,8 +16,8 @@ Problem::~Problem() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
-    void* ptrs[] = {indptr, indices, data64, data32, lower_count, h64, h32, g64,
-                    g32,    coo_i,   coo_j,  coef_fx, h_fx};
+    void* ptrs[] = {indptr, indices, data64, data32, lower_count, h64,  h32,
+                    g64,    g32,     coo_i,  coo_j,  coo_v,       coef_fx, h_fx};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     extern void dense_destroy(DenseOperand*);
@@ -225,6 +225,61 @@ void widen_i32_i64(int64_t n, const int32_t* a, int64_t* b, cudaStream_t s) {
 
 }  // namespace
 
+void encode_energy(Problem* P, cudaStream_t s) {
+    if (P->coef_fx) cudaFree(P->coef_fx);
+    if (P->h_fx) cudaFree(P->h_fx);
+    P->coef_fx = P->h_fx = nullptr;
+    P->energy_ok = true;
+    const int64_t n = P->n, m = P->m;
+    {
+            DevBuf<int> rng(2, s);
+            int init[2] = {1 << 20, -(1 << 20)};
+            VXQ_CUDA(cudaMemcpyAsync(rng.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
+            if (m > 0) k_exp_range<<<nblk(m), TB, 0, s>>>(m, P->coo_v, rng.get(), rng.get() + 1);
+            k_exp_range<<<nblk(n), TB, 0, s>>>(n, P->h64, rng.get(), rng.get() + 1);
+            DevBuf<double> doff(1, s);
+            VXQ_CUDA(cudaMemcpyAsync(doff.get(), &P->offset, sizeof(double),
+                                     cudaMemcpyHostToDevice, s));
+            k_exp_range<<<1, 1, 0, s>>>(1, doff.get(), rng.get(), rng.get() + 1);
+            VXQ_CHECK_LAUNCH();
+            int res[2];
+            VXQ_CUDA(cudaMemcpyAsync(res, rng.get(), sizeof(res), cudaMemcpyDeviceToHost, s));
+            VXQ_CUDA(cudaStreamSynchronize(s));
+            if (res[0] > res[1]) {  // all coefficients zero
+                res[0] = 0;
+                res[1] = 0;
+            }
+            P->e_low = res[0];
+            int span = res[1] - res[0] + 1;  // bits of the largest |coefficient|
+            int L = (span + 1 + 31) / 32 + (span % 32 > 29 ? 1 : 0);
+            L = std::max(L, 2);
+            if (L > kMaxLimbs) {
+                P->energy_ok = false;
+                L = kMaxLimbs;
+            }
+            P->limbs = L;
+            VXQ_CUDA(cudaMalloc(&P->coef_fx, std::max<int64_t>(m, 1) * L * sizeof(uint32_t)));
+            VXQ_CUDA(cudaMalloc(&P->h_fx, n * L * sizeof(uint32_t)));
+            if (P->energy_ok) {
+                if (m > 0) k_encode<<<nblk(m), TB, 0, s>>>(m, P->coo_v, P->e_low, L, P->coef_fx);
+                k_encode<<<nblk(n), TB, 0, s>>>(n, P->h64, P->e_low, L, P->h_fx);
+                DevBuf<uint32_t> ofx(L, s);
+                k_encode_scalar<<<1, 1, 0, s>>>(P->offset, P->e_low, L, ofx.get());
+                VXQ_CHECK_LAUNCH();
+                VXQ_CUDA(cudaMemcpyAsync(P->offset_fx, ofx.get(), L * sizeof(uint32_t),
+                                         cudaMemcpyDeviceToHost, s));
+                if (P->uniform_magnitude) {
+                    DevBuf<uint32_t> mfx(L, s);
+                    k_encode_scalar<<<1, 1, 0, s>>>(P->magnitude, P->e_low, L, mfx.get());
+                    VXQ_CHECK_LAUNCH();
+                    VXQ_CUDA(cudaMemcpyAsync(P->mag_fx, mfx.get(), L * sizeof(uint32_t),
+                                             cudaMemcpyDeviceToHost, s));
+                    VXQ_CUDA(cudaStreamSynchronize(s));
+                }
+            }
+        }
+}
+
 Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t* cols,
                         const double* values, const double* h, double offset, int device) {
     VXQ_REQUIRE(n >= 1, "model needs at least one variable");
@@ -266,7 +321,7 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
 
         // fields
         if (h) {
-            VXQ_CUDA(cudaMemcpyAsync(P->h64, h, n * sizeof(double), cudaMemcpyHostToDevice, s));
+            VXQ_CUDA(cudaMemcpyAsync(P->h64, h, n * sizeof(double), cudaMemcpyDefault, s));
         } else {
             VXQ_CUDA(cudaMemsetAsync(P->h64, 0, n * sizeof(double), s));
         }
@@ -278,17 +333,18 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
             lo64(n + 1, s);
         VXQ_CUDA(cudaMemsetAsync(deg_up.get(), 0, n * sizeof(int32_t), s));
         VXQ_CUDA(cudaMemsetAsync(deg_lo.get(), 0, n * sizeof(int32_t), s));
-        DevBuf<double> dval(std::max<int64_t>(m, 1), s);
+        VXQ_CUDA(cudaMalloc(&P->coo_v, std::max<int64_t>(m, 1) * sizeof(double)));
+        struct DV {
+            double* p;
+            double* get() const { return p; }
+        } dval{P->coo_v};
         DevBuf<int32_t> err(1, s);
         VXQ_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(int), s));
         if (m > 0) {
             DevBuf<int64_t> drows(m, s), dcols(m, s);
-            VXQ_CUDA(cudaMemcpyAsync(drows.get(), rows, m * sizeof(int64_t),
-                                     cudaMemcpyHostToDevice, s));
-            VXQ_CUDA(cudaMemcpyAsync(dcols.get(), cols, m * sizeof(int64_t),
-                                     cudaMemcpyHostToDevice, s));
-            VXQ_CUDA(cudaMemcpyAsync(dval.get(), values, m * sizeof(double),
-                                     cudaMemcpyHostToDevice, s));
+            VXQ_CUDA(cudaMemcpyAsync(drows.get(), rows, m * sizeof(int64_t), cudaMemcpyDefault, s));
+            VXQ_CUDA(cudaMemcpyAsync(dcols.get(), cols, m * sizeof(int64_t), cudaMemcpyDefault, s));
+            VXQ_CUDA(cudaMemcpyAsync(dval.get(), values, m * sizeof(double), cudaMemcpyDefault, s));
             k_validate_coo<<<nblk(m), TB, 0, s>>>(n, m, drows.get(), dcols.get(), dval.get(),
                                                   err.get());
             VXQ_CHECK_LAUNCH();
@@ -374,60 +430,26 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
             P->uniform_magnitude = (a == b) && a > 0;
             P->magnitude = b;
         }
-        // exact-energy encoding
-        {
-            DevBuf<int> rng(2, s);
-            int init[2] = {1 << 20, -(1 << 20)};
-            VXQ_CUDA(cudaMemcpyAsync(rng.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
-            if (m > 0) k_exp_range<<<nblk(m), TB, 0, s>>>(m, dval.get(), rng.get(), rng.get() + 1);
-            k_exp_range<<<nblk(n), TB, 0, s>>>(n, P->h64, rng.get(), rng.get() + 1);
-            DevBuf<double> doff(1, s);
-            VXQ_CUDA(cudaMemcpyAsync(doff.get(), &P->offset, sizeof(double),
-                                     cudaMemcpyHostToDevice, s));
-            k_exp_range<<<1, 1, 0, s>>>(1, doff.get(), rng.get(), rng.get() + 1);
-            VXQ_CHECK_LAUNCH();
-            int res[2];
-            VXQ_CUDA(cudaMemcpyAsync(res, rng.get(), sizeof(res), cudaMemcpyDeviceToHost, s));
-            VXQ_CUDA(cudaStreamSynchronize(s));
-            if (res[0] > res[1]) {  // all coefficients zero
-                res[0] = 0;
-                res[1] = 0;
-            }
-            P->e_low = res[0];
-            int span = res[1] - res[0] + 1;  // bits of the largest |coefficient|
-            int L = (span + 1 + 31) / 32 + (span % 32 > 29 ? 1 : 0);
-            L = std::max(L, 2);
-            if (L > kMaxLimbs) {
-                P->energy_ok = false;
-                L = kMaxLimbs;
-            }
-            P->limbs = L;
-            VXQ_CUDA(cudaMalloc(&P->coef_fx, std::max<int64_t>(m, 1) * L * sizeof(uint32_t)));
-            VXQ_CUDA(cudaMalloc(&P->h_fx, n * L * sizeof(uint32_t)));
-            if (P->energy_ok) {
-                if (m > 0) k_encode<<<nblk(m), TB, 0, s>>>(m, dval.get(), P->e_low, L, P->coef_fx);
-                k_encode<<<nblk(n), TB, 0, s>>>(n, P->h64, P->e_low, L, P->h_fx);
-                DevBuf<uint32_t> ofx(L, s);
-                k_encode_scalar<<<1, 1, 0, s>>>(P->offset, P->e_low, L, ofx.get());
-                VXQ_CHECK_LAUNCH();
-                VXQ_CUDA(cudaMemcpyAsync(P->offset_fx, ofx.get(), L * sizeof(uint32_t),
-                                         cudaMemcpyDeviceToHost, s));
-                if (P->uniform_magnitude) {
-                    DevBuf<uint32_t> mfx(L, s);
-                    k_encode_scalar<<<1, 1, 0, s>>>(P->magnitude, P->e_low, L, mfx.get());
-                    VXQ_CHECK_LAUNCH();
-                    VXQ_CUDA(cudaMemcpyAsync(P->mag_fx, mfx.get(), L * sizeof(uint32_t),
-                                             cudaMemcpyDeviceToHost, s));
-                    VXQ_CUDA(cudaStreamSynchronize(s));
-                }
-            }
-        }
+        encode_energy(P, s);
         VXQ_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         delete P;
         throw;
     }
     return P;
+}
+
+void problem_set_fields(Problem* P, const double* h, double offset, cudaStream_t s) {
+    VXQ_REQUIRE(std::isfinite(offset), "offset must be finite");
+    VXQ_CUDA(cudaMemcpyAsync(P->h64, h, P->n * sizeof(double), cudaMemcpyDefault, s));
+    k_fields<<<nblk(P->n), TB, 0, s>>>(P->n, P->h64, P->h32, P->g64, P->g32);
+    VXQ_CHECK_LAUNCH();
+    P->offset = offset;
+    encode_energy(P, s);
+    VXQ_CUDA(cudaStreamSynchronize(s));
+    std::lock_guard<std::mutex> g(P->mu);
+    P->lambda0 = NAN;
+    P->c0 = NAN;
 }
 
 double problem_lambda0(Problem* p, cudaStream_t s) {

@@ -35,6 +35,7 @@ struct Problem {
     float* g32 = nullptr;          // [n]
     int32_t* coo_i = nullptr;      // [m] couplings i<j (energy evaluation)
     int32_t* coo_j = nullptr;      // [m]
+    double* coo_v = nullptr;       // [m] coupling values (COO order)
 
     // exact energy: every coefficient as an L-limb two's-complement integer * 2^e_low
     int limbs = 0;
@@ -122,6 +123,13 @@ struct DevBuf {
 Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t* cols,
                         const double* values, const double* h, double offset, int device);
 double problem_lambda0(Problem* p, cudaStream_t s);
+void encode_energy(Problem* P, cudaStream_t s);
+// replace h / offset (host or device pointer) and re-derive everything that depends on them
+void problem_set_fields(Problem* P, const double* h, double offset, cudaStream_t s);
+// generate.cu: device-side instance families (0 = qubo_deg6, BASELINE config 5)
+Problem* problem_generate(int family, int64_t n, uint64_t seed, int device);
+void problem_export(Problem* P, int64_t* rows, int64_t* cols, double* values, double* h,
+                    double* offset);
 double problem_c0(Problem* p, cudaStream_t s);
 // Lanczos lambda_max of the operator w_ij = sign * data[k] (row i lists field weights)
 double lanczos_lambda_max(int64_t n, const int64_t* indptr, const int32_t* indices,

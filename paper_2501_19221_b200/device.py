@@ -63,7 +63,46 @@ class DeviceProblem:
         self._finalizer()
 
 
+class GeneratedModel:
+    """An instance synthesised on the GPU (vxq_problem_generate): no host arrays unless
+    exported.  Accepted by every solver like an IsingModel; `export()` returns the
+    canonical IsingModel (host copy) for small instances / cross-checks."""
+
+    FAMILIES = {"qubo_deg6": 0}
+
+    def __init__(self, family: str, n: int, seed: int, device: int = 0):
+        if family not in self.FAMILIES:
+            raise ValidationError(f"unknown family {family!r}")
+        L = _lib.load()
+        _lib.require_gpu()
+        handle = ctypes.c_void_p()
+        _lib.check(L.vxq_problem_generate(self.FAMILIES[family], int(n), int(seed),
+                                          int(device), ctypes.byref(handle)))
+        dp = DeviceProblem.__new__(DeviceProblem)
+        dp.handle, dp.n, dp.device = handle, int(n), device
+        dp._finalizer = weakref.finalize(dp, L.vxq_problem_destroy, handle)
+        self._dp = dp
+        self.family, self.n, self.seed, self.device = family, int(n), int(seed), device
+        self.num_couplings = dp.info()["num_couplings"]
+
+    def export(self):
+        from .model import IsingModel
+        m = self.num_couplings
+        rows = np.empty(m, dtype=np.int64)
+        cols = np.empty(m, dtype=np.int64)
+        vals = np.empty(m)
+        h = np.empty(self.n)
+        off = ctypes.c_double()
+        _lib.check(_lib.load().vxq_problem_export(self._dp.handle, _lib.ptr(rows), _lib.ptr(cols),
+                                                  _lib.ptr(vals), _lib.ptr(h), ctypes.byref(off)))
+        return IsingModel(n=self.n, h=h, rows=rows, cols=cols, values=vals, offset=off.value)
+
+
 def get_problem(model, device: int = 0, cache: bool = True) -> DeviceProblem:
+    if isinstance(model, GeneratedModel):
+        if model.device != device:
+            raise ValidationError("generated model lives on another device")
+        return model._dp
     if not cache:
         return DeviceProblem(model, device)
     key = (id(model), device)

@@ -92,6 +92,66 @@ def random_qubo_deg6(n: int, seed: int = 5) -> IsingModel:
     return qubo_to_ising(q)
 
 
+# ------------------------------------------------------------- config-5 family (device)
+_M32 = np.uint64(0xFFFFFFFF)
+
+
+def _mulhilo(a, b):
+    a_lo, a_hi = a & _M32, a >> np.uint64(32)
+    b_lo, b_hi = b & _M32, b >> np.uint64(32)
+    p0, p1, p2, p3 = a_lo * b_lo, a_lo * b_hi, a_hi * b_lo, a_hi * b_hi
+    mid = (p0 >> np.uint64(32)) + (p1 & _M32) + (p2 & _M32)
+    hi = p3 + (p1 >> np.uint64(32)) + (p2 >> np.uint64(32)) + (mid >> np.uint64(32))
+    return hi, a * b
+
+
+def philox_raw(seed: int, stream: int, k) -> np.ndarray:
+    """Vectorised Philox4x64-10 draw k of stream `stream` (ctr = (k/4+1, 0, stream, 0),
+    key = (seed, 0)) -- the numpy replica-stream layout, any stream index."""
+    k = np.asarray(k, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        c0 = k // np.uint64(4) + np.uint64(1)
+        c1 = np.zeros_like(c0)
+        c2 = np.full_like(c0, np.uint64(stream))
+        c3 = np.zeros_like(c0)
+        k0, k1 = np.uint64(seed), np.uint64(0)
+        M0, M1 = np.uint64(0xD2E7470EE14C6C93), np.uint64(0xCA5A826395121157)
+        W0, W1 = np.uint64(0x9E3779B97F4A7C15), np.uint64(0xBB67AE8584CAA73B)
+        for _ in range(10):
+            hi0, lo0 = _mulhilo(M0, c0)
+            hi1, lo1 = _mulhilo(M1, c2)
+            c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+            k0, k1 = k0 + W0, k1 + W1
+        out = np.stack([c0, c1, c2, c3])
+    return out[(k % np.uint64(4)).astype(np.int64), np.arange(k.size)]
+
+
+def _unit_uniform(raw):
+    return -1.0 + 2.0 * ((raw >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0))
+
+
+def qubo_deg6_family(n: int, seed: int) -> tuple[QuboModel, IsingModel]:
+    """Host mirror of the device generator (csrc/generate.cu, family 0) for small n."""
+    S = 1 << 40
+    i = np.arange(n, dtype=np.uint64)
+    keys = []
+    for c in range(3):
+        off = np.uint64(1) + philox_raw(seed, S + c, i) % np.uint64(n - 1)
+        j = (i + off) % np.uint64(n)
+        lo, hi = np.minimum(i, j), np.maximum(i, j)
+        keys.append(lo * np.uint64(n) + hi)
+    key = np.unique(np.concatenate(keys))
+    r, c_ = (key // np.uint64(n)).astype(np.int64), (key % np.uint64(n)).astype(np.int64)
+    qoff = _unit_uniform(philox_raw(seed, S + 3, key))
+    qdiag = _unit_uniform(philox_raw(seed, S + 4, i))
+    rows = np.concatenate([r, np.arange(n)])
+    cols = np.concatenate([c_, np.arange(n)])
+    vals = np.concatenate([qoff, qdiag])
+    order = np.lexsort((cols, rows))
+    q = QuboModel(n=n, rows=rows[order], cols=cols[order], values=vals[order] + 0.0)
+    return q, qubo_to_ising(q)
+
+
 CONFIGS = {
     "cfg1": dict(desc="dense random QUBO N=100 -> Ising, R=64, T=1000", R=64, T=1000),
     "cfg2": dict(desc="dense Sherrington-Kirkpatrick N=10^4 (J=+-1/sqrt N), R=1024, T=1000",
@@ -113,5 +173,6 @@ def build(name: str, n: int | None = None) -> IsingModel:
     if name == "cfg4":
         return maxcut3(n or 1_000_000)
     if name == "cfg5":
-        return random_qubo_deg6(n or 200_000_000)
+        from .device import GeneratedModel
+        return GeneratedModel("qubo_deg6", n or 200_000_000, seed=5)
     raise KeyError(name)

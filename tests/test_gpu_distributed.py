@@ -52,3 +52,27 @@ def test_solve_rowpart_world1_public_api():
     assert [s.energy for s in ss.samples] == [s.energy for s in ref.samples]
     assert np.array_equal(ss.best.state, ref.best.state)
     assert ss.best.energy == O.energy_exact(m, ss.best.state)
+
+
+@pytest.mark.parametrize("n,seed", [(1000, 5), (40_000, 9)])
+def test_device_generator_matches_host_mirror(n, seed):
+    """Config-5 family generated on the GPU == the numpy mirror (QUBO -> qubo_to_ising):
+    couplings and fields bit-exact, offset == the exact sum of the terms (fsum)."""
+    import math
+
+    from paper_2501_19221_b200.device import GeneratedModel
+    from paper_2501_19221_b200.instances import qubo_deg6_family
+    g = GeneratedModel("qubo_deg6", n, seed)
+    m = g.export()
+    q, ref = qubo_deg6_family(n, seed)
+    for f in ("rows", "cols", "values", "h"):
+        assert np.array_equal(getattr(m, f), getattr(ref, f)), f
+    terms = [float(v) / (2.0 if i == j else 4.0) for i, j, v in zip(q.rows, q.cols, q.values)]
+    assert m.offset == math.fsum(terms)
+    assert abs(m.offset - ref.offset) <= 1e-12 * max(1.0, abs(ref.offset))
+    # solving the generated model == solving its exported host copy
+    p = vxq.PaParams(steps=20, replicas=32, seed=3)
+    a = vxq.run_pa(g, p)
+    b = vxq.run_pa(m, p)
+    assert np.array_equal(a.states, b.states) and np.array_equal(a.energies, b.energies)
+    assert np.array_equal(a.energies[:4], O.energies_exact(m, a.states[:4]))
