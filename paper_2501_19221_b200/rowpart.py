@@ -54,11 +54,13 @@ class GpuSession:
     """One rank's vxq_session (GPU kernels over rows [row_begin, row_end))."""
 
     def __init__(self, model, solver: str, params, row_begin, row_end, rows_alloc, bufs,
-                 precision="fp32", device=0, stream=None, replica_begin=0):
+                 precision="fp32", device=0, stream=None, replica_begin=0,
+                 outputs_on_device=False):
         L = _lib.load()
         dp = get_problem(model, device)
         self._dp = dp
-        opts = _opts(precision, "sparse", replica_begin, stream=stream)
+        opts = _opts(precision, "sparse", replica_begin, stream=stream,
+                     on_device=outputs_on_device)
         self._opts = opts
         pa = sbm = None
         if solver == "pa":
@@ -84,6 +86,14 @@ class GpuSession:
 
     def step(self, t: int):
         _lib.check(_lib.load().vxq_session_step(self.handle, int(t)))
+
+    def finish_device(self, states_ptr: int, energies_ptr: int, order_ptr: int = 0):
+        """finish() into caller-owned device buffers (session created with
+        outputs_on_device=True)."""
+        out = _lib.OutputsC()
+        out.states, out.energies = ctypes.c_void_p(states_ptr), ctypes.c_void_p(energies_ptr)
+        out.order = ctypes.c_void_p(order_ptr) if order_ptr else None
+        _lib.check(_lib.load().vxq_session_finish(self.handle, ctypes.byref(out)))
 
     def finish(self):
         st = np.empty((self.R, self.n), dtype=np.int8)
