@@ -44,7 +44,7 @@ extern "C" {
 #define VXQ_API
 #endif
 
-#define VXQ_ABI_VERSION 1
+#define VXQ_ABI_VERSION 2
 
 #define VXQ_OK 0
 #define VXQ_ERR_INVALID 1     /* -> ValidationError */
@@ -90,7 +90,8 @@ typedef struct {
     int32_t precision;         /* VXQ_FP32 | VXQ_FP64                            */
     int32_t path;              /* VXQ_PATH_*                                     */
     int32_t outputs_on_device; /* 1: vxq_outputs pointers are device pointers    */
-    int32_t track_best;        /* 1: return best-seen state per replica (opt-in) */
+    int32_t track_best;        /* 1: states/energies = best state seen per replica
+                                  (over s_0..s_T; sparse/resident paths; opt-in)   */
     int64_t replica_begin;     /* global index of local replica 0 (sharding)     */
     void* stream;              /* cudaStream_t; NULL => library stream           */
 } vxq_run_opts;
@@ -102,6 +103,9 @@ typedef struct {
     double* m;           /* [R][n] final M (PA) / P (SBM), optional          */
     int64_t* order;      /* [R] replicas by ascending energy, ties by index (optional;
                             argsort(kind="stable") of common.py:57)                  */
+    double* energy_trace; /* [T] optional: min over replicas of E(s_t), the energy of
+                             the spins entering step t (exact on the sparse paths and on
+                             the dense path with h = 0) -> time-to-target              */
     /* filled by the library */
     double lambda0_used; /* PA  */
     double c0_used;      /* SBM */

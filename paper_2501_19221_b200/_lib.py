@@ -53,7 +53,7 @@ class RunOptsC(ctypes.Structure):
 
 class OutputsC(ctypes.Structure):
     _fields_ = [("states", P), ("energies", P), ("x", P), ("m", P), ("order", P),
-                ("lambda0_used", f64), ("c0_used", f64), ("loop_ms", f64),
+                ("energy_trace", P), ("lambda0_used", f64), ("c0_used", f64), ("loop_ms", f64),
                 ("launches", i64), ("path_used", i32), ("reserved", i32)]
 
 

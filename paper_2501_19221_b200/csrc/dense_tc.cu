@@ -243,6 +243,7 @@ struct DenseRunArgs {
     int64_t plane_elems;     // elements per q-plane (R * ld) for kBf16x3
     int mode;                // 0: dynamics steps, 1: energy pass over b_buf[0] (q2), 2: no-op
     long long* q2;           // [R] 2 * sum_{i<j} K_ij s_i s_j  (mode 1)
+    long long* qtrace;       // [T][R] same for the spins s_t entering step t (optional)
     unsigned* done;          // [T][n_tiles] finished row-tiles per (step, replica block)
     int group;               // replica blocks interleaved per row block (A-panel reuse)
     unsigned long long* stats;  // optional [8] wait-cycle counters (VXQ_DENSE_STATS=1)
@@ -503,6 +504,15 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         const int64_t off = base + (int64_t)jj * a.ld;
                         const float f = O::mul(a.scale, __uint_as_float(v[jj]));
                         if constexpr (KD == Kind::kFp8) {
+                            if (a.qtrace) {  // exact per-step energy of s_t = sign(x_t)
+                                const int kk = (int)__uint_as_float(v[jj]);
+                                const int term = ok ? (xo[jj] >= 0.f ? kk : -kk) : 0;
+                                const int sum = __reduce_add_sync(0xffffffffu, term);
+                                if (lane == 0 && (r0 + jj) < a.R)
+                                    atomicAdd(reinterpret_cast<unsigned long long*>(a.qtrace) +
+                                                  (int64_t)t * a.R + r0 + jj,
+                                              (unsigned long long)(long long)sum);
+                            }
                             // PA: grad = (lam x + f) + h; m = alpha m - eta grad; x = clip
                             const float grad = O::add(O::add(O::mul(st, xo[jj]), f), hi);
                             const float mn = O::sub(O::mul(a.alpha, mo[jj]), O::mul(a.eta, grad));
@@ -585,6 +595,28 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 
 constexpr int TB = 256;
 inline unsigned nblk(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, TB)); }
+
+__global__ void k_any_nonzero(int64_t n, const double* v, int* flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && v[i] != 0.0) *flag = 1;
+}
+
+// trace[t] = min_r (offset + c * q_t[r] / 2) (h = 0; NaN otherwise: no exact h-term here)
+__global__ void k_trace_from_q(const long long* q, int64_t T, int64_t R, double c,
+                               double offset, const int* h_nonzero, double* trace) {
+    __shared__ double sh[256];
+    const int64_t t = blockIdx.x;
+    double v = INFINITY;
+    for (int64_t r = threadIdx.x; r < R; r += blockDim.x)
+        v = fmin(v, offset + c * (double)(q[t * R + r] / 2));
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = fmin(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) trace[t] = *h_nonzero ? NAN : sh[0];
+}
 
 int num_sms() {
     int nsm = 148, dev = 0;
@@ -779,7 +811,8 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
 void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                    const std::vector<double>& sched, float eta, float alpha, uint64_t seed,
                    int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, long long* q2,
-                   cudaStream_t s, double* loop_ms, int64_t* launches) {
+                   cudaStream_t s, double* loop_ms, int64_t* launches, double* trace_out,
+                   bool trace_on_dev) {
     DenseOperand* d = dense_operand(p, s, false);
     const int64_t n = p->n, ld = d->ld, T = (int64_t)sched.size();
     DevBuf<float> x(R * ld, s), m(R * ld, s);
@@ -825,8 +858,28 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
+    DevBuf<long long> qtr;
+    if (trace_out) {
+        qtr = DevBuf<long long>(std::max<int64_t>(T, 1) * R, s);
+        VXQ_CUDA(cudaMemsetAsync(qtr.get(), 0, std::max<int64_t>(T, 1) * R * sizeof(long long), s));
+        a.qtrace = qtr.get();
+    }
     *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, cl, s);
     *launches += 2;
+    if (trace_out) {
+        DevBuf<double> tr(std::max<int64_t>(T, 1), s);
+        DevBuf<int> hnz(1, s);
+        VXQ_CUDA(cudaMemsetAsync(hnz.get(), 0, sizeof(int), s));
+        k_any_nonzero<<<nblk(n), TB, 0, s>>>(n, p->h64, hnz.get());
+        k_trace_from_q<<<(unsigned)std::max<int64_t>(T, 1), 256, 0, s>>>(
+            qtr.get(), T, R, p->magnitude, p->offset, hnz.get(), tr.get());
+        VXQ_CHECK_LAUNCH();
+        VXQ_CUDA(cudaMemcpyAsync(trace_out, tr.get(), T * sizeof(double),
+                                 trace_on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 s));
+        VXQ_CUDA(cudaStreamSynchronize(s));
+        *launches += 2;
+    }
     if (q2) energy_pass(d, x.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(x.get(), n, R, ld, R_pad, V, x_il);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(m.get(), n, R, ld, R_pad, V, m_il);

@@ -648,6 +648,89 @@ struct EventTimer {
     }
 };
 
+// ---- improvement mode / energy trace (north star (3); SURVEY 8a note on best-seen)
+__global__ void k_trace_min(const double* __restrict__ e, int64_t R, double* __restrict__ out) {
+    __shared__ double sh[256];
+    double v = INFINITY;
+    for (int64_t r = threadIdx.x; r < R; r += blockDim.x) v = fmin(v, e[r]);
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = fmin(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+// strictly better => keep (the earliest state wins ties); mask bit r marks replica r
+__global__ void k_update_best(const double* __restrict__ e, int64_t R, double* __restrict__ best,
+                              uint32_t* __restrict__ mask) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool better = false;
+    if (r < R && e[r] < best[r]) {
+        best[r] = e[r];
+        better = true;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, better);
+    if ((threadIdx.x & 31) == 0 && r < R + 31) mask[r >> 5] = word;
+}
+
+__global__ void k_merge_bits(int64_t words, int64_t W, const uint32_t* __restrict__ mask,
+                             const uint32_t* __restrict__ sb, uint32_t* __restrict__ best_sb) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= words) return;
+    const uint32_t mk = mask[idx % W];
+    if (mk) best_sb[idx] = (best_sb[idx] & ~mk) | (sb[idx] & mk);
+}
+
+__global__ void k_fill(double* a, int64_t n, double v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = v;
+}
+
+struct Tracker {
+    bool trace = false, best = false;
+    int64_t n = 0, R = 0, W = 0;
+    DevBuf<double> e, best_e, tr;
+    DevBuf<uint32_t> mask, best_sb;
+    void init(Problem* p, const Layout& L, int64_t T, bool want_trace, bool want_best,
+              cudaStream_t s) {
+        trace = want_trace;
+        best = want_best;
+        n = L.n;
+        R = L.R;
+        W = L.W;
+        if (!trace && !best) return;
+        e = DevBuf<double>(R, s);
+        if (trace) tr = DevBuf<double>(std::max<int64_t>(T, 1), s);
+        if (best) {
+            best_e = DevBuf<double>(R, s);
+            k_fill<<<nblk(R), TB, 0, s>>>(best_e.get(), R, INFINITY);
+            mask = DevBuf<uint32_t>(W, s);
+            best_sb = DevBuf<uint32_t>(n * W, s);
+            VXQ_CUDA(cudaMemsetAsync(best_sb.get(), 0, n * W * sizeof(uint32_t), s));
+        }
+    }
+    // spins s_t (bit-packed, all rows) entering step t; t == T for the final state
+    void observe(Problem* p, const uint32_t* sb, int64_t t, int64_t T, cudaStream_t s) {
+        if (!trace && !best) return;
+        if (!best && t >= T) return;
+        energies_from_bits(p, sb, W, R, e.get(), s);
+        if (trace && t < T) k_trace_min<<<1, 256, 0, s>>>(e.get(), R, tr.get() + t);
+        if (best) {
+            k_update_best<<<(unsigned)ceil_div(W * 32, 256), 256, 0, s>>>(e.get(), R,
+                                                                         best_e.get(), mask.get());
+            k_merge_bits<<<nblk(n * W), TB, 0, s>>>(n * W, W, mask.get(), sb, best_sb.get());
+        }
+        VXQ_CHECK_LAUNCH();
+    }
+    void export_trace(vxq_outputs* out, int64_t T, bool on_dev, cudaStream_t s) {
+        if (!trace || !out->energy_trace) return;
+        VXQ_CUDA(cudaMemcpyAsync(out->energy_trace, tr.get(), T * sizeof(double),
+                                 on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    }
+};
+
 // Common tail: sign bits -> exact energies -> states / order / analog exports.
 template <typename T>
 void finish_outputs(Problem* p, const Layout& L, const uint32_t* sb, const T* xa, const T* ma,
@@ -756,9 +839,21 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         if (req == VXQ_PATH_DENSE)
             throw Error(VXQ_ERR_UNSUPPORTED, "dense tensor-core path is fp32 only");
     }
-    const bool dense = sizeof(T) == 4 && (req == VXQ_PATH_DENSE ||
-                                          (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+    const bool want_best = opts && opts->track_best;
+    const bool want_trace = out->energy_trace != nullptr;
+    if (want_best && req == VXQ_PATH_DENSE)
+        throw Error(VXQ_ERR_UNSUPPORTED, "track_best is not available on the dense path yet");
+    const bool dense = sizeof(T) == 4 && !want_best &&
+                       (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
     if (!dense) path = choose_path(req, L, smem, p->nnz);
+    // the resident kernel keeps spins in shared memory: tracking needs per-step spins
+    if (!dense && path == VXQ_PATH_RESIDENT && (want_best || want_trace)) {
+        if (req == VXQ_PATH_RESIDENT)
+            throw Error(VXQ_ERR_UNSUPPORTED, "tracking needs the sparse or dense path");
+        path = VXQ_PATH_SPARSE;
+    }
+    Tracker trk;
+    if (!dense) trk.init(p, L, T_, want_trace, want_best, s);
     EventTimer tm(s);
     const uint32_t* sb_final = nullptr;
     DevBuf<long long> q2;
@@ -766,7 +861,8 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         q2 = DevBuf<long long>(R, s);
         if constexpr (sizeof(T) == 4) {
             dense_pa_loop(p, R, L.R_pad, L.V, L.W, sched, eta, alpha, prm->seed, rbegin,
-                          x.get(), m.get(), sbA.get(), q2.get(), s, &out->loop_ms, &launches);
+                          x.get(), m.get(), sbA.get(), q2.get(), s, &out->loop_ms, &launches,
+                          out->energy_trace, opts && opts->outputs_on_device);
         }
         sb_final = sbA.get();
     } else if (path == VXQ_PATH_RESIDENT) {
@@ -794,6 +890,7 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         tm.start();
         uint32_t* bufs[2] = {sbA.get(), sbB.get()};
         for (int64_t t = 0; t < T_; ++t) {
+            trk.observe(p, bufs[t & 1], t, T_, s);  // E(s_t): exact, bit-packed spins
             launch_pa_step<T>(L, op, h, (T)sched[t], eta, alpha, x.get(), m.get(), bufs[t & 1],
                               bufs[(t + 1) & 1], s);
             ++launches;
@@ -802,8 +899,11 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         tm.stop();
         sb_final = bufs[T_ & 1];
         out->loop_ms = tm.ms();
+        trk.observe(p, sb_final, T_, T_, s);
+        trk.export_trace(out, T_, opts && opts->outputs_on_device, s);
+        if (trk.best) sb_final = trk.best_sb.get();
     }
-    out->path_used = path;
+    out->path_used = dense ? VXQ_PATH_DENSE : path;
     finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s, q2.get());
     out->launches = launches + 4;
 }
@@ -812,7 +912,8 @@ template <typename T>
 void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g,
                   const std::vector<double>& a_sched, double dt, double a0, double c0,
                   double q_cap, int requested_path, int64_t nnz, T* q, T* qalt, T* pm,
-                  vxq_outputs* out, int64_t& launches, cudaStream_t s, T** q_final) {
+                  vxq_outputs* out, int64_t& launches, cudaStream_t s, T** q_final,
+                  Tracker* trk = nullptr, uint32_t* sb_scratch = nullptr) {
     const int64_t n = L.n, T_ = (int64_t)a_sched.size();
     SbmScalars<T> sc;
     sc.a_t = 0;
@@ -824,6 +925,12 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
     int RG = resident_rg(L);
     size_t smem = resident_smem_sbm(L, RG, sizeof(T));
     int path = choose_path(requested_path, L, smem, nnz);
+    const bool tracking = trk && (trk->trace || trk->best);
+    if (tracking && path == VXQ_PATH_RESIDENT) {
+        if (requested_path == VXQ_PATH_RESIDENT)
+            throw Error(VXQ_ERR_UNSUPPORTED, "tracking needs the sparse or dense path");
+        path = VXQ_PATH_SPARSE;
+    }
     EventTimer tm(s);
     if (path == VXQ_PATH_RESIDENT) {
         DevBuf<T> ds(std::max<int64_t>(T_, 1), s);
@@ -846,6 +953,10 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
         tm.start();
         T* qs[2] = {q, qalt};
         for (int64_t t = 0; t < T_; ++t) {
+            if (tracking) {  // E(sign(q_t)), exact
+                launch_pack<T>(L, qs[t & 1], sb_scratch, s);
+                trk->observe(p, sb_scratch, t, T_, s);
+            }
             sc.a_t = (T)a_sched[t];
             launch_sbm_step<T>(L, op, g, sc, qs[t & 1], qs[(t + 1) & 1], pm, s);
             ++launches;
@@ -880,9 +991,20 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
         if (req == VXQ_PATH_DENSE)
             throw Error(VXQ_ERR_UNSUPPORTED, "dense tensor-core path is fp32 only");
     }
-    const bool dense = sizeof(T) == 4 && (req == VXQ_PATH_DENSE ||
-                                          (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+    const bool want_best = opts && opts->track_best;
+    const bool want_trace = out->energy_trace != nullptr;
+    if (want_best && req == VXQ_PATH_DENSE)
+        throw Error(VXQ_ERR_UNSUPPORTED, "track_best is not available on the dense path yet");
+    const bool dense = sizeof(T) == 4 && !want_best &&
+                       (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
     if (dense) {
+        if (want_trace) {  // no per-step energies on the dense SBM path (round 1): NaN
+            DevBuf<double> nan_tr(std::max<int64_t>(T_, 1), s);
+            k_fill<<<nblk(T_), TB, 0, s>>>(nan_tr.get(), T_, NAN);
+            VXQ_CUDA(cudaMemcpyAsync(out->energy_trace, nan_tr.get(), T_ * sizeof(double),
+                                     cudaMemcpyDefault, s));
+            VXQ_CUDA(cudaStreamSynchronize(s));
+        }
         DevBuf<long long> qq(R, s);
         if constexpr (sizeof(T) == 4) {
             dense_sbm_loop(p, R, L.R_pad, L.V, L.W, sched, prm->dt, prm->a0, c0, prm->q_cap,
@@ -897,11 +1019,15 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
     Operator<T> op = problem_operator<T>(p, (T)-1);  // B = -A
     const T* g = pick<T>(p->g64, p->g32);            // g = -h
     T* qf = nullptr;
+    Tracker trk;
+    trk.init(p, L, T_, want_trace, want_best, s);
     sbm_run_core<T>(p, L, op, g, sched, prm->dt, prm->a0, c0, prm->q_cap, req, p->nnz,
-                    q.get(), q2.get(), pm.get(), out, launches, s, &qf);
+                    q.get(), q2.get(), pm.get(), out, launches, s, &qf, &trk, sb.get());
     launch_pack<T>(L, qf, sb.get(), s);
     ++launches;
-    finish_outputs<T>(p, L, sb.get(), qf, pm.get(), opts, out, s);
+    trk.observe(p, sb.get(), T_, T_, s);
+    trk.export_trace(out, T_, opts && opts->outputs_on_device, s);
+    finish_outputs<T>(p, L, trk.best ? trk.best_sb.get() : sb.get(), qf, pm.get(), opts, out, s);
     out->launches = launches + 4;
 }
 

@@ -174,7 +174,8 @@ bool dense_eligible(const Problem* p, int64_t R);
 void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                    const std::vector<double>& sched, float eta, float alpha, uint64_t seed,
                    int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, long long* q2,
-                   cudaStream_t s, double* loop_ms, int64_t* launches);
+                   cudaStream_t s, double* loop_ms, int64_t* launches,
+                   double* trace_out = nullptr, bool trace_on_dev = false);
 
 void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                     const std::vector<double>& a_sched, double dt, double a0, double c0,

@@ -144,7 +144,7 @@ def _seed(seed) -> int:
 
 
 def _opts(precision: str, path: str, replica_begin: int, stream=None,
-          on_device: bool = False) -> _lib.RunOptsC:
+          on_device: bool = False, track_best: bool = False) -> _lib.RunOptsC:
     if precision not in ("fp32", "fp64"):
         raise ValidationError(f"precision must be 'fp32' or 'fp64', got {precision!r}")
     if path not in _lib.PATHS:
@@ -153,6 +153,7 @@ def _opts(precision: str, path: str, replica_begin: int, stream=None,
     o.precision = _lib.FP64 if precision == "fp64" else _lib.FP32
     o.path = _lib.PATHS[path]
     o.outputs_on_device = 1 if on_device else 0
+    o.track_best = 1 if track_best else 0
     o.replica_begin = int(replica_begin)
     o.stream = stream
     return o
@@ -167,7 +168,7 @@ class RunResult(NamedTuple):
     info: dict
 
 
-def _outputs(n, R, want_state):
+def _outputs(n, R, want_state, trace_steps=0):
     st = np.empty((R, n), dtype=np.int8)
     en = np.empty(R, dtype=np.float64)
     order = np.empty(R, dtype=np.int64)
@@ -176,38 +177,46 @@ def _outputs(n, R, want_state):
     out = _lib.OutputsC()
     out.states, out.energies, out.order = _lib.ptr(st), _lib.ptr(en), _lib.ptr(order)
     out.x, out.m = _lib.ptr(x), _lib.ptr(m)
-    return out, st, en, order, x, m
+    tr = np.empty(trace_steps) if trace_steps else None
+    out.energy_trace = _lib.ptr(tr)
+    return out, st, en, order, x, m, tr
 
 
 def run_pa(model, params, *, precision="fp32", path="auto", device=0, replica_begin=0,
-           want_state=False, cache=True) -> RunResult:
-    """One vxq_pa_solve call; returns per-replica arrays (no SampleSet assembly)."""
+           want_state=False, cache=True, trace=False, track_best=False) -> RunResult:
+    """One vxq_pa_solve call; returns per-replica arrays (no SampleSet assembly).
+    trace: info["energy_trace"][t] = min over replicas of E(s_t); track_best: states and
+    energies are each replica's best state seen over s_0..s_T (improvement mode)."""
     params.validate()
     dp = get_problem(model, device, cache=cache)
     c = _lib.PaParamsC(int(params.steps), float(params.learning_rate), float(params.momentum),
                        _lib.nan_if_none(params.lambda0), int(params.replicas), _seed(params.seed))
-    out, st, en, order, x, m = _outputs(model.n, int(params.replicas), want_state)
-    opts = _opts(precision, path, replica_begin)
+    out, st, en, order, x, m, tr = _outputs(model.n, int(params.replicas), want_state,
+                                            int(params.steps) if trace else 0)
+    opts = _opts(precision, path, replica_begin, track_best=track_best)
     _lib.check(_lib.load().vxq_pa_solve(dp.handle, ctypes.byref(c), ctypes.byref(opts),
                                         ctypes.byref(out)))
     info = {"lambda0": out.lambda0_used, "loop_ms": out.loop_ms, "launches": out.launches,
-            "path": _lib.PATH_NAMES.get(out.path_used, "?"), "precision": precision}
+            "path": _lib.PATH_NAMES.get(out.path_used, "?"), "precision": precision,
+            "energy_trace": tr, "track_best": track_best}
     return RunResult(st, en, order, x, m, info)
 
 
 def run_sbm(model, params, *, precision="fp32", path="auto", device=0, replica_begin=0,
-            want_state=False, cache=True) -> RunResult:
+            want_state=False, cache=True, trace=False, track_best=False) -> RunResult:
     params.validate()
     dp = get_problem(model, device, cache=cache)
     c = _lib.SbmParamsC(int(params.steps), float(params.dt), float(params.a0),
                         _lib.nan_if_none(params.c0), float(params.q_cap),
                         float(params.init_noise), int(params.replicas), _seed(params.seed))
-    out, st, en, order, x, m = _outputs(model.n, int(params.replicas), want_state)
-    opts = _opts(precision, path, replica_begin)
+    out, st, en, order, x, m, tr = _outputs(model.n, int(params.replicas), want_state,
+                                            int(params.steps) if trace else 0)
+    opts = _opts(precision, path, replica_begin, track_best=track_best)
     _lib.check(_lib.load().vxq_sbm_solve(dp.handle, ctypes.byref(c), ctypes.byref(opts),
                                          ctypes.byref(out)))
     info = {"c0": out.c0_used, "loop_ms": out.loop_ms, "launches": out.launches,
-            "path": _lib.PATH_NAMES.get(out.path_used, "?"), "precision": precision}
+            "path": _lib.PATH_NAMES.get(out.path_used, "?"), "precision": precision,
+            "energy_trace": tr, "track_best": track_best}
     return RunResult(st, en, order, x, m, info)
 
 
@@ -249,25 +258,36 @@ def sampleset_from(res: RunResult, R: int, seed, wall_time: float, replica_begin
 
 
 def solve_pa(model, params, *, precision: str = "fp32", path: str = "auto", device: int = 0,
-             replica_begin: int = 0) -> SampleSet:
+             replica_begin: int = 0, trace: bool = False, track_best: bool = False) -> SampleSet:
     """Parallel annealing on the B200 (drop-in for parallel_annealing.py:28-48)."""
     params.validate()
     t0 = time.perf_counter()
     res = run_pa(model, params, precision=precision, path=path, device=device,
-                 replica_begin=replica_begin)
+                 replica_begin=replica_begin, trace=trace, track_best=track_best)
     return sampleset_from(res, int(params.replicas), params.seed, time.perf_counter() - t0,
                           replica_begin)
 
 
 def solve_sbm(model, params, *, precision: str = "fp32", path: str = "auto", device: int = 0,
-              replica_begin: int = 0) -> SampleSet:
+              replica_begin: int = 0, trace: bool = False, track_best: bool = False) -> SampleSet:
     """Simulated bifurcation on the B200 (drop-in for bifurcation.py:50-67)."""
     params.validate()
     t0 = time.perf_counter()
     res = run_sbm(model, params, precision=precision, path=path, device=device,
-                  replica_begin=replica_begin)
+                  replica_begin=replica_begin, trace=trace, track_best=track_best)
     return sampleset_from(res, int(params.replicas), params.seed, time.perf_counter() - t0,
                           replica_begin)
+
+
+def time_to_target(trace, target: float, loop_ms: float):
+    """First step whose spins reach `target` (min over replicas) and the corresponding
+    time assuming uniform step cost: (step, ms) or (None, None)."""
+    tr = np.asarray(trace)
+    hit = np.nonzero(tr <= target)[0]
+    if hit.size == 0:
+        return None, None
+    t = int(hit[0])
+    return t, loop_ms * (t + 1) / tr.size
 
 
 def resolve_lambda0(model) -> float:

@@ -332,3 +332,73 @@ def test_zero_coupling_model():
     m = vxq.IsingModel.from_terms(4)
     r = vxq.solve_pa(m, vxq.PaParams(steps=10, replicas=2, seed=0))
     assert r.best.energy == 0.0
+
+
+# ---------------------------------------------------------------- improvement mode / trace
+def _oracle_pa_states_per_step(m, R, T, seed, dtype=np.float32):
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    lam = O.pa_schedule(O.resolve_lambda0(m), T)
+    X = O.pa_init(seed, R, m.n)
+    M = np.zeros_like(X)
+    states = [O.sign_pm(X)]
+    for t in range(T):
+        X, M = O.pa_run(ip, ix, dv, m.h, lam[t:t + 1], 0.05, 0.9, X, M, dtype)
+        states.append(O.sign_pm(X))
+    return states
+
+
+def test_energy_trace_and_best_tracking_sparse_pa():
+    m = gen_complete(44, 40, "uniform")
+    R, T = 24, 30
+    st = _oracle_pa_states_per_step(m, R, T, 6)
+    E = np.array([O.energies_exact(m, s) for s in st])  # (T+1, R), exact
+    r = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=6), trace=True, track_best=True)
+    assert r.info["path"] == "sparse"
+    assert np.array_equal(r.info["energy_trace"], E[:T].min(axis=1))
+    assert np.array_equal(r.energies, E.min(axis=0))       # best over s_0..s_T, exact
+    assert np.array_equal(r.energies, O.energies_exact(m, r.states))
+    plain = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=6))
+    assert np.all(r.energies <= plain.energies)
+    t, ms = vxq.solvers.time_to_target(r.info["energy_trace"], E.min() + 1e-9, 1.0)
+    assert t is not None and E[: t + 1].min() <= E.min() + 1e-9
+
+
+def test_energy_trace_sparse_sbm():
+    m = gen_complete(45, 32, "gaussian")
+    R, T = 16, 25
+    r = vxq.run_sbm(m, vxq.SbmParams(steps=T, dt=0.05, replicas=R, seed=3, c0=0.2), trace=True,
+                    track_best=True)
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    Q, P = O.sbm_init(3, R, m.n, 1.0)
+    a = O.sbm_schedule(1.0, T)
+    E = [O.energies_exact(m, O.sign_pm(Q))]
+    for t in range(T):
+        Q, P = O.sbm_run(ip, ix, -dv, -m.h, a[t:t + 1], 0.05, 1.0, 0.2, 1.0, Q, P, np.float32)
+        E.append(O.energies_exact(m, O.sign_pm(Q)))
+    E = np.array(E)
+    assert np.array_equal(r.info["energy_trace"], E[:T].min(axis=1))
+    assert np.array_equal(r.energies, E.min(axis=0))
+
+
+def test_energy_trace_dense_pa_exact():
+    m = sk_model(700, 8)
+    R, T = 200, 20
+    r = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=2), trace=True)
+    assert r.info["path"] == "dense"
+    n = m.n
+    K = np.zeros((n, n), dtype=np.int64)
+    K[m.rows, m.cols] = np.sign(m.values).astype(np.int64)
+    K[m.cols, m.rows] = np.sign(m.values).astype(np.int64)
+    c = np.float32(np.abs(m.values[0]))
+    X = O.pa_init(2, R, n).astype(np.float32)
+    M = np.zeros_like(X)
+    eta, alpha = np.float32(0.05), np.float32(0.9)
+    want = []
+    for lam in O.pa_schedule(O.resolve_lambda0(m), T).astype(np.float32):
+        S = np.where(X >= 0, 1, -1).astype(np.int64)
+        want.append(O.energies_exact(m, S.astype(np.int8)).min())
+        f = c * (S @ K.T).astype(np.float32)
+        grad = (lam * X + f) + m.h.astype(np.float32)
+        M = alpha * M - eta * grad
+        X = np.clip(X + M, np.float32(-1), np.float32(1))
+    assert np.array_equal(r.info["energy_trace"], np.array(want))
