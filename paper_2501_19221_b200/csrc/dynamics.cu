@@ -143,8 +143,11 @@ __global__ void k_pack_signs(const T* __restrict__ x, int64_t row0, int64_t nrow
 // row is read once for all of them and CPW x more loads are in flight per warp.
 // Rows [row0, row0 + nrows): x/m are indexed locally (row - row0), the CSR, h and the
 // sign-bit buffers by global row (a row-partitioned rank reads every row's spins).
+#ifndef VXQ_PA_MINB
+#define VXQ_PA_MINB 4
+#endif
 template <typename T, int V, int CPW>
-__global__ void __launch_bounds__(256) k_pa_step(int64_t row0, int64_t nrows, int64_t R_pad,
+__global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int64_t nrows, int64_t R_pad,
                                                  Operator<T> op, const T* __restrict__ h,
                                                  T lam, T eta, T alpha, T* __restrict__ x,
                                                  T* __restrict__ m,
