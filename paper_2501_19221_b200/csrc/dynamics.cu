@@ -377,26 +377,83 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
 }
 
 // ------------------------------------------------------------------ resident (small n)
-// One CTA owns RG replicas for all T steps; their state lives in shared memory, the
-// CSR streams from L1/L2.  One __syncthreads per step (double-buffered spins / q).
+// One CTA owns RG replicas for all T steps: their state and the whole CSR (row pointers,
+// indices, values) live in shared memory, so the only per-step synchronisation is one
+// __syncthreads (double-buffered spins / q).  Each row still sums its neighbours
+// sequentially in ascending column order (bit-identical to the sparse kernels).
 template <typename T>
-__global__ void k_pa_resident(int64_t n, int64_t R_pad, int V, int RG, Operator<T> op,
+struct ResidentSmem {
+    int32_t* ptr;
+    int32_t* idx;
+    T* val;
+    unsigned char* rest;
+};
+
+__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+
+template <typename T>
+__device__ ResidentSmem<T> stage_csr(unsigned char* smem, int n, int nnz, const Operator<T>& op) {
+    ResidentSmem<T> S;
+    S.ptr = reinterpret_cast<int32_t*>(smem);
+    S.idx = reinterpret_cast<int32_t*>(smem + align16((n + 1) * 4));
+    S.val = reinterpret_cast<T*>(smem + align16((n + 1) * 4) + align16((size_t)nnz * 4));
+    S.rest = smem + align16((n + 1) * 4) + align16((size_t)nnz * 4) + align16((size_t)nnz * sizeof(T));
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) S.ptr[i] = (int32_t)op.indptr[i];
+    for (int k = threadIdx.x; k < nnz; k += blockDim.x) {
+        S.idx[k] = op.indices[k];
+        S.val[k] = Ops<T>::mul(op.sign, op.data[k]);
+    }
+    return S;
+}
+
+template <typename T>
+__host__ __device__ inline size_t resident_csr_bytes(int64_t n, int64_t nnz) {
+    return align16((n + 1) * 4) + align16((size_t)nnz * 4) + align16((size_t)nnz * sizeof(T));
+}
+
+// f = sum_k val[k] * v(idx[k]) over [kb, ke) in order; v(j) provided by the callable
+template <typename T, typename F>
+__device__ __forceinline__ T row_sum(const ResidentSmem<T>& S, int kb, int ke, F&& v) {
+    using O = Ops<T>;
+    T f = (T)0;
+    int k = kb;
+    for (; k + 4 <= ke; k += 4) {
+        int j[4];
+        T a[4], w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            j[u] = S.idx[k + u];
+            a[u] = S.val[k + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = v(j[u], a[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) f = O::add(f, w[u]);
+    }
+    for (; k < ke; ++k) f = O::add(f, v(S.idx[k], S.val[k]));
+    return f;
+}
+
+template <typename T>
+__global__ void k_pa_resident(int64_t n64, int64_t R_pad, int V, int RG, int nnz, Operator<T> op,
                               const T* __restrict__ h, const T* __restrict__ lam_sched,
                               int64_t steps, T eta, T alpha, T* __restrict__ x,
                               T* __restrict__ m) {
     using O = Ops<T>;
     extern __shared__ __align__(16) unsigned char smem[];
-    T* xs = reinterpret_cast<T*>(smem);
-    T* ms = xs + (int64_t)RG * n;
-    uint8_t* s0 = reinterpret_cast<uint8_t*>(ms + (int64_t)RG * n);
-    uint8_t* s1 = s0 + (int64_t)RG * n;
+    const int n = (int)n64;
+    ResidentSmem<T> S = stage_csr<T>(smem, n, nnz, op);
+    T* xs = reinterpret_cast<T*>(S.rest);
+    T* ms = xs + RG * n;
+    uint8_t* s0 = reinterpret_cast<uint8_t*>(ms + RG * n);
+    uint8_t* s1 = s0 + RG * n;
     const int64_t r0 = (int64_t)blockIdx.x * RG;
-    const int64_t items = (int64_t)RG * n;
-    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
-        int64_t g = it / n, i = it % n;
-        int64_t r = r0 + g;
-        T xv = (r < R_pad) ? x[i * R_pad + pos_of(r, V)] : (T)0;
-        T mv = (r < R_pad) ? m[i * R_pad + pos_of(r, V)] : (T)0;
+    const int items = RG * n;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int g = it / n, i = it - g * n;
+        const int64_t r = r0 + g;
+        T xv = (r < R_pad) ? x[(int64_t)i * R_pad + pos_of(r, V)] : (T)0;
+        T mv = (r < R_pad) ? m[(int64_t)i * R_pad + pos_of(r, V)] : (T)0;
         xs[it] = xv;
         ms[it] = mv;
         s0[it] = xv >= (T)0;
@@ -406,17 +463,14 @@ __global__ void k_pa_resident(int64_t n, int64_t R_pad, int V, int RG, Operator<
         const T lam = lam_sched[t];
         const uint8_t* sc = (t & 1) ? s1 : s0;
         uint8_t* sn = (t & 1) ? s0 : s1;
-        for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
-            int64_t g = it / n, i = it % n;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+            const int g = it / n, i = it - g * n;
             const uint8_t* sg = sc + g * n;
-            T f = (T)0;
-            for (int64_t k = __ldg(op.indptr + i); k < __ldg(op.indptr + i + 1); ++k) {
-                T a = O::mul(op.sign, __ldg(op.data + k));
-                f = O::add(f, sg[__ldg(op.indices + k)] ? a : -a);
-            }
-            T xo = xs[it];
-            T grad = O::add(O::add(O::mul(lam, xo), f), __ldg(h + i));
-            T mn = O::sub(O::mul(alpha, ms[it]), O::mul(eta, grad));
+            const T f = row_sum<T>(S, S.ptr[i], S.ptr[i + 1],
+                                   [&](int j, T a) { return sg[j] ? a : -a; });
+            const T xo = xs[it];
+            const T grad = O::add(O::add(O::mul(lam, xo), f), __ldg(h + i));
+            const T mn = O::sub(O::mul(alpha, ms[it]), O::mul(eta, grad));
             T xn = O::add(xo, mn);
             xn = xn < (T)-1 ? (T)-1 : (xn > (T)1 ? (T)1 : xn);
             xs[it] = xn;
@@ -425,50 +479,49 @@ __global__ void k_pa_resident(int64_t n, int64_t R_pad, int V, int RG, Operator<
         }
         __syncthreads();
     }
-    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
-        int64_t g = it / n, i = it % n;
-        int64_t r = r0 + g;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int g = it / n, i = it - g * n;
+        const int64_t r = r0 + g;
         if (r < R_pad) {
-            x[i * R_pad + pos_of(r, V)] = xs[it];
-            m[i * R_pad + pos_of(r, V)] = ms[it];
+            x[(int64_t)i * R_pad + pos_of(r, V)] = xs[it];
+            m[(int64_t)i * R_pad + pos_of(r, V)] = ms[it];
         }
     }
 }
 
 template <typename T>
-__global__ void k_sbm_resident(int64_t n, int64_t R_pad, int V, int RG, Operator<T> op,
-                               const T* __restrict__ g, const T* __restrict__ a_sched,
-                               int64_t steps, SbmScalars<T> sc0, T* __restrict__ q,
-                               T* __restrict__ p) {
+__global__ void k_sbm_resident(int64_t n64, int64_t R_pad, int V, int RG, int nnz,
+                               Operator<T> op, const T* __restrict__ g,
+                               const T* __restrict__ a_sched, int64_t steps, SbmScalars<T> sc0,
+                               T* __restrict__ q, T* __restrict__ p) {
     using O = Ops<T>;
     extern __shared__ __align__(16) unsigned char smem[];
-    T* q0 = reinterpret_cast<T*>(smem);
-    T* q1 = q0 + (int64_t)RG * n;
-    T* ps = q1 + (int64_t)RG * n;
+    const int n = (int)n64;
+    ResidentSmem<T> S = stage_csr<T>(smem, n, nnz, op);
+    T* q0 = reinterpret_cast<T*>(S.rest);
+    T* q1 = q0 + RG * n;
+    T* ps = q1 + RG * n;
     const int64_t r0 = (int64_t)blockIdx.x * RG;
-    const int64_t items = (int64_t)RG * n;
-    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
-        int64_t gg = it / n, i = it % n;
-        int64_t r = r0 + gg;
-        q0[it] = (r < R_pad) ? q[i * R_pad + pos_of(r, V)] : (T)0;
-        ps[it] = (r < R_pad) ? p[i * R_pad + pos_of(r, V)] : (T)0;
+    const int items = RG * n;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int gg = it / n, i = it - gg * n;
+        const int64_t r = r0 + gg;
+        q0[it] = (r < R_pad) ? q[(int64_t)i * R_pad + pos_of(r, V)] : (T)0;
+        ps[it] = (r < R_pad) ? p[(int64_t)i * R_pad + pos_of(r, V)] : (T)0;
     }
     __syncthreads();
     for (int64_t t = 0; t < steps; ++t) {
         const T a_t = a_sched[t];
         const T* qc = (t & 1) ? q1 : q0;
         T* qn_arr = (t & 1) ? q0 : q1;
-        for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
-            int64_t gg = it / n, i = it % n;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+            const int gg = it / n, i = it - gg * n;
             const T* qg = qc + gg * n;
-            T f = (T)0;
-            for (int64_t k = __ldg(op.indptr + i); k < __ldg(op.indptr + i + 1); ++k) {
-                T a = O::mul(op.sign, __ldg(op.data + k));
-                f = O::add(f, O::mul(a, qg[__ldg(op.indices + k)]));
-            }
-            T qi = qc[it];
-            T inner = -O::sub(O::add(O::mul(qi, qi), sc0.a0), a_t);
-            T force = O::add(O::mul(inner, qi), O::mul(sc0.c0, O::add(f, __ldg(g + i))));
+            const T f = row_sum<T>(S, S.ptr[i], S.ptr[i + 1],
+                                   [&](int j, T a) { return O::mul(a, qg[j]); });
+            const T qi = qc[it];
+            const T inner = -O::sub(O::add(O::mul(qi, qi), sc0.a0), a_t);
+            const T force = O::add(O::mul(inner, qi), O::mul(sc0.c0, O::add(f, __ldg(g + i))));
             T pn = O::add(ps[it], O::mul(sc0.dt, force));
             T qn = O::add(qi, O::mul(sc0.dta0, pn));
             if (fabs(qn) > sc0.q_cap) {
@@ -481,12 +534,12 @@ __global__ void k_sbm_resident(int64_t n, int64_t R_pad, int V, int RG, Operator
         __syncthreads();
     }
     const T* qf = (steps & 1) ? q1 : q0;
-    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
-        int64_t gg = it / n, i = it % n;
-        int64_t r = r0 + gg;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int gg = it / n, i = it - gg * n;
+        const int64_t r = r0 + gg;
         if (r < R_pad) {
-            q[i * R_pad + pos_of(r, V)] = qf[it];
-            p[i * R_pad + pos_of(r, V)] = ps[it];
+            q[(int64_t)i * R_pad + pos_of(r, V)] = qf[it];
+            p[(int64_t)i * R_pad + pos_of(r, V)] = ps[it];
         }
     }
 }
@@ -544,11 +597,15 @@ int resident_rg(const Layout& L) {
     return rg;
 }
 
-size_t resident_smem_pa(const Layout& L, int RG, size_t tsz) {
-    return (size_t)RG * L.n * (2 * tsz + 2);
+size_t resident_smem_pa(const Layout& L, int RG, size_t tsz, int64_t nnz) {
+    const size_t csr = tsz == 8 ? resident_csr_bytes<double>(L.n, nnz)
+                                : resident_csr_bytes<float>(L.n, nnz);
+    return csr + (size_t)RG * L.n * (2 * tsz + 2);
 }
-size_t resident_smem_sbm(const Layout& L, int RG, size_t tsz) {
-    return (size_t)RG * L.n * (3 * tsz);
+size_t resident_smem_sbm(const Layout& L, int RG, size_t tsz, int64_t nnz) {
+    const size_t csr = tsz == 8 ? resident_csr_bytes<double>(L.n, nnz)
+                                : resident_csr_bytes<float>(L.n, nnz);
+    return csr + (size_t)RG * L.n * (3 * tsz);
 }
 
 constexpr size_t kResidentSmemMax = 200 * 1024;
@@ -835,7 +892,7 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     Operator<T> op = problem_operator<T>(p, (T)1);
     const T* h = pick<T>(p->h64, p->h32);
     int RG = resident_rg(L);
-    size_t smem = resident_smem_pa(L, RG, sizeof(T));
+    size_t smem = resident_smem_pa(L, RG, sizeof(T), p->nnz);
     const int req = opts ? opts->path : 0;
     int path = VXQ_PATH_DENSE;
     if constexpr (sizeof(T) == 8) {
@@ -878,7 +935,7 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         unsigned grid = (unsigned)ceil_div(L.R_pad, RG);
         tm.start();
         k_pa_resident<T><<<grid, block_threads((int64_t)RG * n), smem, s>>>(
-            n, L.R_pad, L.V, RG, op, h, ds.get(), T_, eta, alpha, x.get(), m.get());
+            n, L.R_pad, L.V, RG, (int)p->nnz, op, h, ds.get(), T_, eta, alpha, x.get(), m.get());
         VXQ_CHECK_LAUNCH();
         tm.stop();
         ++launches;
@@ -926,7 +983,7 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
     sc.dta0 = (T)(dt * a0);  // (dt * a0) in Python floats, then * P
     sc.q_cap = (T)q_cap;
     int RG = resident_rg(L);
-    size_t smem = resident_smem_sbm(L, RG, sizeof(T));
+    size_t smem = resident_smem_sbm(L, RG, sizeof(T), nnz);
     int path = choose_path(requested_path, L, smem, nnz);
     const bool tracking = trk && (trk->trace || trk->best);
     if (tracking && path == VXQ_PATH_RESIDENT) {
@@ -945,7 +1002,7 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
         unsigned grid = (unsigned)ceil_div(L.R_pad, RG);
         tm.start();
         k_sbm_resident<T><<<grid, block_threads((int64_t)RG * n), smem, s>>>(
-            n, L.R_pad, L.V, RG, op, g, ds.get(), T_, sc, q, pm);
+            n, L.R_pad, L.V, RG, (int)nnz, op, g, ds.get(), T_, sc, q, pm);
         VXQ_CHECK_LAUNCH();
         tm.stop();
         ++launches;
