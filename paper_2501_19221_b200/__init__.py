@@ -19,7 +19,8 @@ from .solvers import (PaParams, Sample, SampleSet, SbmParams, default_config, in
                       pa_schedule, params_from_dict, params_to_dict, replica_streams,
                       resolve_c0, resolve_lambda0, run_pa, run_sbm, sbm_schedule, solve_pa,
                       solve_sbm)
-from .device import clear_cache, energies
+from .device import GeneratedModel, clear_cache, energies
+from .instance_io import read_instance, write_instance
 
 __version__ = "0.1.0"
 
@@ -28,5 +29,6 @@ __all__ = [
     "bits_to_spins", "sign_pm", "spins_to_bits", "qubo_to_ising", "PaParams", "SbmParams",
     "Sample", "SampleSet", "default_config", "integrate", "params_from_dict", "params_to_dict",
     "replica_streams", "resolve_c0", "resolve_lambda0", "run_pa", "run_sbm", "solve_pa",
-    "solve_sbm", "pa_schedule", "sbm_schedule", "clear_cache", "energies",
+    "solve_sbm", "pa_schedule", "sbm_schedule", "clear_cache", "energies", "GeneratedModel",
+    "read_instance", "write_instance",
 ]
