@@ -14,6 +14,8 @@
  *       solvers/bifurcation.py:50-67
  *   integrate(B, g, Q, P, dt, a_schedule, a0, c0, q)   vxq_sbm_integrate
  *       solvers/bifurcation.py:37-47
+ *   solve_sa(model, SaParams) -> SampleSet             vxq_sa_solve
+ *       solvers/annealing.py:24-74
  *   IsingModel.energies(states)                        vxq_energies
  *       model.py:160-164 (here: correctly rounded exact sums)
  *   resolve_lambda0 / field_scale                      vxq_problem_lambda0
@@ -44,7 +46,7 @@ extern "C" {
 #define VXQ_API
 #endif
 
-#define VXQ_ABI_VERSION 2
+#define VXQ_ABI_VERSION 3
 
 #define VXQ_OK 0
 #define VXQ_ERR_INVALID 1     /* -> ValidationError */
@@ -86,6 +88,20 @@ typedef struct {
     uint64_t seed;
 } vxq_sbm_params;
 
+/* SaParams (common.py:74-92), geometric schedule.  T_init NaN => 2 * max(field_scale,
+ * 1e-12); T_final NaN => 1e-3 * T_init (annealing.py:29-30).  temps: optional HOST array
+ * [sweeps], the temperature of each sweep; the Python layer passes numpy's
+ * T_init * ratio ** arange(sweeps) so it is bit-identical with annealing.py:31-35
+ * (NULL => vxq_sa_schedule, C pow). */
+typedef struct {
+    int64_t sweeps;
+    double T_init;
+    double T_final;
+    int64_t replicas;
+    uint64_t seed;
+    const double* temps;
+} vxq_sa_params;
+
 typedef struct {
     int32_t precision;         /* VXQ_FP32 | VXQ_FP64                            */
     int32_t path;              /* VXQ_PATH_*                                     */
@@ -107,8 +123,8 @@ typedef struct {
                              the spins entering step t (exact on the sparse paths and on
                              the dense path with h = 0) -> time-to-target              */
     /* filled by the library */
-    double lambda0_used; /* PA  */
-    double c0_used;      /* SBM */
+    double lambda0_used; /* PA: lambda0;  SA: T_init  */
+    double c0_used;      /* SBM: c0;      SA: T_final */
     double loop_ms;      /* device time of the dynamics loop (CUDA events)   */
     int64_t launches;    /* kernels launched by this call                    */
     int32_t path_used;   /* VXQ_PATH_* actually run                          */
@@ -142,6 +158,16 @@ VXQ_API int vxq_pa_solve(vxq_problem* p, const vxq_pa_params* prm, const vxq_run
                  vxq_outputs* out);
 VXQ_API int vxq_sbm_solve(vxq_problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts,
                   vxq_outputs* out);
+
+/* Simulated annealing (annealing.py:24-74): R independent replicas, single-spin-flip
+ * Metropolis sweeps in fixed index order, each replica reports the best state seen
+ * (checked after every sweep).  Fields F = S A + h are kept per replica and updated in
+ * O(degree) per accepted flip.  Replica r draws from Philox(seed).jumped(r): spins from
+ * integers(0, 2, n), then one uniform per (sweep, spin).  energy_trace must be NULL;
+ * x/m must be NULL.  Path: RESIDENT keeps each warp's fields in shared memory (small n),
+ * SPARSE keeps them in HBM/L2 ([n][R] replica-contiguous). */
+VXQ_API int vxq_sa_solve(vxq_problem* p, const vxq_sa_params* prm, const vxq_run_opts* opts,
+                         vxq_outputs* out);
 
 /* integrate(B, g, Q, P, ...): B given as CSR of B^T (row i lists B[j,i]),
  * Q/P [R][n] fp64 host arrays updated in place; a_sched[T] host fp64. */
@@ -181,6 +207,9 @@ VXQ_API int vxq_energies(vxq_problem* p, const int8_t* states, int64_t R, double
  *   SBM: a_t   = numpy.linspace(0.0, a0, T)[t]  bifurcation.py:63          */
 VXQ_API int vxq_pa_schedule(double lambda0, int64_t T, double* out);
 VXQ_API int vxq_sbm_schedule(double a0, int64_t T, double* out);
+/*   SA : temps[k] = T_init * pow(pow(T_final / T_init, 1 / (sweeps - 1)), k)
+ *        (annealing.py:31-35; numpy may differ by an ulp -- pass params.temps for parity) */
+VXQ_API int vxq_sa_schedule(double T_init, double T_final, int64_t sweeps, double* out);
 
 VXQ_API const char* vxq_last_error(void);
 VXQ_API int vxq_abi_version(void);

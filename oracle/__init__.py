@@ -55,6 +55,9 @@ def lib():
                                       P, P, P]
         L.orc_sbm_run_f32.argtypes = [i64, i64, P, P, P, P, P, i64, f32, f32, f32, f32, f32,
                                       P, P, P]
+        L.orc_sa_init_spins.argtypes = [i64, u64, u64, P]
+        L.orc_sa_run_f64.argtypes = [i64, i64, P, P, P, P, P, i64, u64, i64, P, P, P, P, P]
+        L.orc_sa_run_f32.argtypes = [i64, i64, P, P, P, P, P, i64, u64, i64, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -267,6 +270,48 @@ def sbm_solve(model, steps, dt=0.01, a0=1.0, c0=None, q_cap=1.0, init_noise=1.0,
     Q, P = sbm_run(ip, ix, -dv, -np.asarray(model.h, dtype=np.float64),
                    sbm_schedule(a0, steps), dt, a0, c0, q_cap, Q, P, dtype)
     return sign_pm(Q), Q, P
+
+
+def sa_init(seed: int, R: int, n: int, replica_begin: int = 0) -> np.ndarray:
+    """Initial SA spins: stream r -> 2 * integers(0, 2, n) - 1 (annealing.py:40)."""
+    S = np.empty((R, n), dtype=np.int8)
+    for r in range(R):
+        lib().orc_sa_init_spins(n, seed, replica_begin + r, _p(S[r]))
+    return S
+
+
+def sa_schedule(T_init, T_final, sweeps) -> np.ndarray:
+    """annealing.py:31-35."""
+    if sweeps > 1:
+        ratio = (T_final / T_init) ** (1.0 / (sweeps - 1))
+        return T_init * ratio ** np.arange(sweeps)
+    return np.array([T_init], dtype=np.float64)
+
+
+def sa_solve(model, sweeps, T_init=None, T_final=None, replicas=32, seed=0,
+             dtype=np.float64, replica_begin=0):
+    """solve_sa restated (annealing.py:24-74): returns (best states, tracked best E)."""
+    n = model.n
+    T0 = T_init if T_init is not None else 2.0 * resolve_lambda0(model)
+    T1 = T_final if T_final is not None else 1e-3 * T0
+    temps = np.ascontiguousarray(sa_schedule(T0, T1, sweeps), dtype=np.float64)
+    ip, ix, dv = symmetric_csr(n, model.rows, model.cols, model.values)
+    S0 = sa_init(seed, replicas, n, replica_begin)
+    E0 = np.array([energy_exact(model, s) - float(model.offset) for s in S0])
+    best = np.empty((replicas, n), dtype=np.int8)
+    bestE = np.empty(replicas)
+    work = np.empty(n, dtype=np.int8)
+    if dtype == np.float64:
+        F = np.empty(n)
+        hv = np.ascontiguousarray(model.h, dtype=np.float64)
+        fn, dd = lib().orc_sa_run_f64, np.ascontiguousarray(dv, dtype=np.float64)
+    else:
+        F = np.empty(n, dtype=np.float32)
+        hv = np.ascontiguousarray(model.h, dtype=np.float32)
+        fn, dd = lib().orc_sa_run_f32, np.ascontiguousarray(dv, dtype=np.float32)
+    fn(n, replicas, _p(ip), _p(ix), _p(dd), _p(hv), _p(temps), int(sweeps), int(seed),
+       int(replica_begin), _p(E0), _p(best), _p(bestE), _p(F), _p(work))
+    return best, bestE
 
 
 # --------------------------------------------------------------------------

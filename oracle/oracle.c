@@ -157,3 +157,88 @@ void orc_sbm_run_f32(int64_t n, int64_t R, const int64_t* indptr, const int32_t*
                      float dta0, float* Q, float* P, float* pnew) {
     SBM_BODY(float)
 }
+
+/* ---------------- SA, solvers/annealing.py:24-74 ----------------
+ * Replica r = stream rng_stream(seed, rbegin + r):
+ *   S = 2 * integers(0, 2, n) - 1   (32-bit half i of the raw draws, low half first; the
+ *                                    Lemire step for range 2 is the top bit, no rejection)
+ *   U[s, i] = random() from raw draw ceil(n/2) + s*n + i    (chunking keeps stream order)
+ *   F = S @ A + h  (CSR ascending column from 0.0, then + h; annealing.py:42-43)
+ *   E = energies(S) - offset  (passed in as E0: correctly rounded exact, see energy_exact)
+ * sweep s, spin i (annealing.py:56-70):
+ *   dE = -2.0 * S_i * F_i;  accept = U < exp(minimum(-dE / T_s, 0.0))
+ *   accept: S_i = -S_i; E += dE; F_j += 2.0 * S_i * A_ij  (j in row i)
+ *   after each sweep: E < best_E -> best = (E, S)                                      */
+void orc_sa_init_spins(int64_t n, uint64_t seed, uint64_t replica, int8_t* S) {
+    uint64_t blk[4], q_cached = ~0ULL;
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t q = (uint64_t)i >> 1;
+        if ((q >> 2) != q_cached) {
+            uint64_t ctr[4] = {(q >> 2) + 1, 0, replica, 0};
+            philox4x64_10(ctr, seed, 0, blk);
+            q_cached = q >> 2;
+        }
+        uint64_t raw = blk[q & 3];
+        uint64_t bit = (i & 1) ? (raw >> 63) : ((raw >> 31) & 1ULL);
+        S[i] = bit ? 1 : -1;
+    }
+}
+
+#define SA_BODY(T)                                                                       \
+    for (int64_t r = 0; r < R; ++r) {                                                    \
+        const uint64_t rg = (uint64_t)(rbegin + r);                                      \
+        int8_t* S = S_work;                                                              \
+        orc_sa_init_spins(n, seed, rg, S);                                               \
+        for (int64_t i = 0; i < n; ++i) {                                                \
+            T f = (T)0;                                                                  \
+            for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k)                          \
+                f = f + (S[indices[k]] > 0 ? data[k] : -data[k]);                        \
+            F[i] = f + hv[i];                                                            \
+        }                                                                                \
+        double E = E0[r], bestE = E;                                                     \
+        memcpy(best + r * n, S, (size_t)n);                                              \
+        uint64_t kdraw = (uint64_t)(n + 1) / 2, blk[4], qc = ~0ULL;                      \
+        for (int64_t s = 0; s < sweeps; ++s) {                                           \
+            const double Tt = temps[s];                                                  \
+            for (int64_t i = 0; i < n; ++i) {                                            \
+                const uint64_t q = kdraw >> 2;                                           \
+                if (q != qc) {                                                           \
+                    uint64_t ctr[4] = {q + 1, 0, rg, 0};                                 \
+                    philox4x64_10(ctr, seed, 0, blk);                                    \
+                    qc = q;                                                              \
+                }                                                                        \
+                const uint64_t raw = blk[kdraw & 3];                                     \
+                ++kdraw;                                                                 \
+                const double u = (double)(raw >> 11) * (1.0 / 9007199254740992.0);      \
+                const double dE = (-2.0 * (double)S[i]) * (double)F[i];                  \
+                double x = -dE / Tt;                                                     \
+                if (!isnan(x) && !(x < 0.0)) x = 0.0;                                    \
+                if (u < exp(x)) {                                                        \
+                    S[i] = (int8_t)-S[i];                                                \
+                    E = E + dE;                                                          \
+                    const T d2 = (T)(2 * S[i]);                                          \
+                    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k)                   \
+                        F[indices[k]] = F[indices[k]] + d2 * data[k];                    \
+                }                                                                        \
+            }                                                                            \
+            if (E < bestE) {                                                             \
+                bestE = E;                                                               \
+                memcpy(best + r * n, S, (size_t)n);                                      \
+            }                                                                            \
+        }                                                                                \
+        bestE_out[r] = bestE;                                                            \
+    }
+
+void orc_sa_run_f64(int64_t n, int64_t R, const int64_t* indptr, const int32_t* indices,
+                    const double* data, const double* hv, const double* temps, int64_t sweeps,
+                    uint64_t seed, int64_t rbegin, const double* E0, int8_t* best,
+                    double* bestE_out, double* F, int8_t* S_work) {
+    SA_BODY(double)
+}
+
+void orc_sa_run_f32(int64_t n, int64_t R, const int64_t* indptr, const int32_t* indices,
+                    const float* data, const float* hv, const double* temps, int64_t sweeps,
+                    uint64_t seed, int64_t rbegin, const double* E0, int8_t* best,
+                    double* bestE_out, float* F, int8_t* S_work) {
+    SA_BODY(float)
+}

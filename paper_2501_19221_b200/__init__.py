@@ -2,7 +2,8 @@
 
 Drop-in for the hot path of the reference ``qubokit`` package (arXiv 2501.19221
 comparison solvers): ``solve_pa`` (Parallel Annealing) and ``solve_sbm``
-(Simulated Bifurcation), QUBO/Ising in, bitstrings + exact energies out.
+(Simulated Bifurcation), plus ``solve_sa`` (simulated annealing, the reference's other
+batched-replica solver); QUBO/Ising in, bitstrings + exact energies out.
 The loop runs as hand-written sm_100a CUDA kernels behind the C-ABI in
 ``include/vxq.h`` (``_lib/libvxq.so``); there is no CPU fallback.
 
@@ -15,10 +16,10 @@ from .errors import QubokitError, ValidationError
 from .model import (IsingModel, QuboModel, as_bits, as_spins, bits_to_spins, sign_pm,
                     spins_to_bits)
 from .transforms import qubo_to_ising
-from .solvers import (PaParams, Sample, SampleSet, SbmParams, default_config, integrate,
-                      pa_schedule, params_from_dict, params_to_dict, replica_streams,
-                      resolve_c0, resolve_lambda0, run_pa, run_sbm, sbm_schedule, solve_pa,
-                      solve_sbm)
+from .solvers import (PaParams, SaParams, Sample, SampleSet, SbmParams, default_config,
+                      integrate, pa_schedule, params_from_dict, params_to_dict,
+                      replica_streams, resolve_c0, resolve_lambda0, run_pa, run_sa, run_sbm,
+                      sa_schedule, sbm_schedule, solve_pa, solve_sa, solve_sbm)
 from .device import GeneratedModel, clear_cache, energies
 from .instance_io import read_instance, write_instance
 
@@ -30,5 +31,6 @@ __all__ = [
     "Sample", "SampleSet", "default_config", "integrate", "params_from_dict", "params_to_dict",
     "replica_streams", "resolve_c0", "resolve_lambda0", "run_pa", "run_sbm", "solve_pa",
     "solve_sbm", "pa_schedule", "sbm_schedule", "clear_cache", "energies", "GeneratedModel",
+    "SaParams", "solve_sa", "run_sa", "sa_schedule",
     "read_instance", "write_instance",
 ]

@@ -33,6 +33,7 @@ EXPORTS = (
     "vxq_pa_schedule", "vxq_sbm_schedule", "vxq_last_error", "vxq_abi_version",
     "vxq_device_count", "vxq_exchange_row_bytes", "vxq_session_create", "vxq_session_step",
     "vxq_session_finish", "vxq_session_destroy", "vxq_problem_generate", "vxq_problem_export",
+    "vxq_sa_solve", "vxq_sa_schedule",
 )
 
 
@@ -44,6 +45,11 @@ class PaParamsC(ctypes.Structure):
 class SbmParamsC(ctypes.Structure):
     _fields_ = [("steps", i64), ("dt", f64), ("a0", f64), ("c0", f64), ("q_cap", f64),
                 ("init_noise", f64), ("replicas", i64), ("seed", u64)]
+
+
+class SaParamsC(ctypes.Structure):
+    _fields_ = [("sweeps", i64), ("T_init", f64), ("T_final", f64), ("replicas", i64),
+                ("seed", u64), ("temps", P)]
 
 
 class RunOptsC(ctypes.Structure):
@@ -90,6 +96,9 @@ def load():
                                     ctypes.POINTER(OutputsC)]
         L.vxq_sbm_integrate.argtypes = [i64, P, P, P, P, i64, P, P, P, i64, f64, f64, f64, f64,
                                         ctypes.POINTER(RunOptsC)]
+        L.vxq_sa_solve.argtypes = [P, ctypes.POINTER(SaParamsC), ctypes.POINTER(RunOptsC),
+                                   ctypes.POINTER(OutputsC)]
+        L.vxq_sa_schedule.argtypes = [f64, f64, i64, P]
         L.vxq_energies.argtypes = [P, P, i64, P, ctypes.POINTER(RunOptsC)]
         L.vxq_pa_schedule.argtypes = [f64, i64, P]
         L.vxq_sbm_schedule.argtypes = [f64, i64, P]

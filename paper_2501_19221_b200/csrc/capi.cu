@@ -84,6 +84,13 @@ int vxq_sbm_schedule(double a0, int64_t T, double* out) {
     });
 }
 
+int vxq_sa_schedule(double T_init, double T_final, int64_t sweeps, double* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(sweeps >= 0 && (sweeps == 0 || out), "invalid schedule arguments");
+        vxq::sa_schedule(T_init, T_final, sweeps, out);
+    });
+}
+
 int vxq_problem_create(int64_t n, int64_t num_couplings, const int64_t* rows,
                        const int64_t* cols, const double* values, const double* h,
                        double offset, int device, vxq_problem** out) {
@@ -170,6 +177,23 @@ int vxq_pa_solve(vxq_problem* p, const vxq_pa_params* prm, const vxq_run_opts* o
         DeviceGuard dg(p->p->device);
         vxq::StreamScope ss(opts ? opts->stream : nullptr);
         vxq::pa_solve(p->p, prm, opts, out, ss.s);
+    });
+}
+
+int vxq_sa_solve(vxq_problem* p, const vxq_sa_params* prm, const vxq_run_opts* opts,
+                 vxq_outputs* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && prm, "null argument");
+        check_outputs(out);
+        // SaParams.validate (common.py:84-91)
+        VXQ_REQUIRE(prm->sweeps > 0, "sweeps must be positive");
+        VXQ_REQUIRE(prm->replicas > 0, "replicas must be positive");
+        if (!std::isnan(prm->T_init) && !std::isnan(prm->T_final))
+            VXQ_REQUIRE(prm->T_init >= prm->T_final && prm->T_final > 0,
+                        "need T_init >= T_final > 0");
+        DeviceGuard dg(p->p->device);
+        vxq::StreamScope ss(opts ? opts->stream : nullptr);
+        vxq::sa_solve(p->p, prm, opts, out, ss.s);
     });
 }
 

@@ -823,7 +823,9 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                                                        s0.get());
     VXQ_CHECK_LAUNCH();
     const int bn = choose_bn(n, R, 1, KindTraits<Kind::kFp8>::kBnMax);
-    int cl = 2;  // B multicast across a 2-CTA cluster
+    // VXQ_DENSE_CLUSTER=2: B multicast across 2-CTA clusters (fewer cycles, same wall time
+    // under the 1 kW power cap; cluster + cooperative launches cannot be profiled by ncu)
+    int cl = 1;
     if (const char* e = getenv("VXQ_DENSE_CLUSTER")) cl = atoi(e) == 2 ? 2 : 1;
     if (ceil_div(n, DBM) < 2) cl = 1;
     CUtensorMap tmB0 = make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW,

@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
 #pragma unroll
     for (int g = 0; g < CPW; ++g) {
         const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
-        xv[g] = *reinterpret_cast<const Vec<T, V>*>(x + base);
-        mv[g] = *reinterpret_cast<const Vec<T, V>*>(m + base);
+        xv[g] = ld_cs<T, V>(x + base);
+        mv[g] = ld_cs<T, V>(m + base);
     }
     T f[NB];
 #pragma unroll
@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
             if (lane == g * V + b) sb_out[i * W + c0 * V + g * V + b] = word;
         }
         const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
-        *reinterpret_cast<Vec<T, V>*>(x + base) = xv[g];
-        *reinterpret_cast<Vec<T, V>*>(m + base) = mv[g];
+        st_cs<T, V>(x + base, xv[g]);
+        st_cs<T, V>(m + base, mv[g]);
     }
 }
 
@@ -260,15 +260,15 @@ __global__ void __launch_bounds__(256) k_pa_step_coop(int64_t row0, int64_t nrow
 #pragma unroll
     for (int u = 0; u < RPW; ++u) {
         const int64_t il = u < nr ? il0 + u : il0;
-        xv[u] = x[il * 32 + lane];
-        mv[u] = m[il * 32 + lane];
+        xv[u] = __ldcs(x + il * 32 + lane);
+        mv[u] = __ldcs(m + il * 32 + lane);
     }
     // cooperative loads of entries [kbase, kbase + 64)
     const int64_t k0 = kbase + lane, k1 = kbase + 32 + lane;
     const bool v0 = k0 < kend, v1 = k1 < kend;
-    const int j0 = v0 ? __ldg(op.indices + k0) : 0, j1 = v1 ? __ldg(op.indices + k1) : 0;
-    const T a0 = v0 ? O::mul(op.sign, __ldg(op.data + k0)) : (T)0;
-    const T a1 = v1 ? O::mul(op.sign, __ldg(op.data + k1)) : (T)0;
+    const int j0 = v0 ? __ldcs(op.indices + k0) : 0, j1 = v1 ? __ldcs(op.indices + k1) : 0;
+    const T a0 = v0 ? O::mul(op.sign, __ldcs(op.data + k0)) : (T)0;
+    const T a1 = v1 ? O::mul(op.sign, __ldcs(op.data + k1)) : (T)0;
     const uint32_t w0 = v0 ? __ldg(sb_in + j0) : 0u, w1 = v1 ? __ldg(sb_in + j1) : 0u;
 #pragma unroll
     for (int u = 0; u < RPW; ++u) {
@@ -296,8 +296,8 @@ __global__ void __launch_bounds__(256) k_pa_step_coop(int64_t row0, int64_t nrow
         const T mn = O::sub(O::mul(alpha, mv[u]), O::mul(eta, grad));
         T xn = O::add(xo, mn);
         xn = xn < (T)-1 ? (T)-1 : (xn > (T)1 ? (T)1 : xn);
-        x[il * 32 + lane] = xn;
-        m[il * 32 + lane] = mn;
+        __stcs(x + il * 32 + lane, xn);
+        __stcs(m + il * 32 + lane, mn);
         const uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
         if (lane == 0) sb_out[i] = word;
     }
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a, qv.v[b]));
     }
     Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(q_in + base);
-    Vec<T, V> pv = *reinterpret_cast<const Vec<T, V>*>(p + pbase);
+    Vec<T, V> pv = ld_cs<T, V>(p + pbase);
     const T gi = __ldg(g + i);
 #pragma unroll
     for (int b = 0; b < V; ++b) {
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         pv.v[b] = pn;
     }
     *reinterpret_cast<Vec<T, V>*>(q_out + base) = qv;
-    *reinterpret_cast<Vec<T, V>*>(p + pbase) = pv;
+    st_cs<T, V>(p + pbase, pv);
 }
 
 // ------------------------------------------------------------------ resident (small n)
@@ -687,26 +687,6 @@ void launch_pack(const Layout& L, const T* x, uint32_t* sb, cudaStream_t s) {
     VXQ_CHECK_LAUNCH();
 }
 
-struct EventTimer {
-    cudaEvent_t a = nullptr, b = nullptr;
-    cudaStream_t s;
-    explicit EventTimer(cudaStream_t st) : s(st) {
-        VXQ_CUDA(cudaEventCreate(&a));
-        VXQ_CUDA(cudaEventCreate(&b));
-    }
-    void start() { VXQ_CUDA(cudaEventRecord(a, s)); }
-    void stop() { VXQ_CUDA(cudaEventRecord(b, s)); }
-    double ms() {
-        float v = 0;
-        VXQ_CUDA(cudaEventSynchronize(b));
-        VXQ_CUDA(cudaEventElapsedTime(&v, a, b));
-        return v;
-    }
-    ~EventTimer() {
-        if (a) cudaEventDestroy(a);
-        if (b) cudaEventDestroy(b);
-    }
-};
 
 // ---- improvement mode / energy trace (north star (3); SURVEY 8a note on best-seen)
 __global__ void k_trace_min(const double* __restrict__ e, int64_t R, double* __restrict__ out) {
@@ -1092,6 +1072,15 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
 }
 
 }  // namespace
+
+void finish_from_bits(Problem* p, int64_t R, int64_t W, const uint32_t* sb,
+                      const vxq_run_opts* opts, vxq_outputs* out, cudaStream_t s) {
+    VXQ_REQUIRE(!out->x && !out->m, "x/m outputs are not available for this solver");
+    Layout L = make_layout(p->n, R, false);
+    L.W = W;
+    L.R_pad = W * 32;
+    finish_outputs<float>(p, L, sb, nullptr, nullptr, opts, out, s);
+}
 
 void pa_solve(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, vxq_outputs* out,
               cudaStream_t s) {

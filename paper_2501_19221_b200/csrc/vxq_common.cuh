@@ -98,4 +98,61 @@ struct alignas(sizeof(T) * V) Vec {
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Streaming (evict-first, ld/st.global.cs) accesses for the per-step state x/m/p and the
+// CSR: they are touched once per step, so they should not evict the gathered spin / q
+// tables from L2.  (Within one launch every state element belongs to one warp.)
+template <typename T, int V>
+__device__ __forceinline__ Vec<T, V> ld_cs(const T* p) {
+    Vec<T, V> v;
+    if constexpr (sizeof(T) * V == 16) {
+        if constexpr (sizeof(T) == 4) {
+            float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+            memcpy(&v, &t, 16);
+        } else {
+            double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+            memcpy(&v, &t, 16);
+        }
+    } else if constexpr (sizeof(T) * V == 8) {
+        if constexpr (sizeof(T) == 4) {
+            float2 t = __ldcs(reinterpret_cast<const float2*>(p));
+            memcpy(&v, &t, 8);
+        } else {
+            double t = __ldcs(reinterpret_cast<const double*>(p));
+            memcpy(&v, &t, 8);
+        }
+    } else {
+        float t = __ldcs(reinterpret_cast<const float*>(p));
+        memcpy(&v, &t, 4);
+    }
+    return v;
+}
+template <typename T, int V>
+__device__ __forceinline__ void st_cs(T* p, const Vec<T, V>& v) {
+    if constexpr (sizeof(T) * V == 16) {
+        if constexpr (sizeof(T) == 4) {
+            float4 t;
+            memcpy(&t, &v, 16);
+            __stcs(reinterpret_cast<float4*>(p), t);
+        } else {
+            double2 t;
+            memcpy(&t, &v, 16);
+            __stcs(reinterpret_cast<double2*>(p), t);
+        }
+    } else if constexpr (sizeof(T) * V == 8) {
+        if constexpr (sizeof(T) == 4) {
+            float2 t;
+            memcpy(&t, &v, 8);
+            __stcs(reinterpret_cast<float2*>(p), t);
+        } else {
+            double t;
+            memcpy(&t, &v, 8);
+            __stcs(reinterpret_cast<double*>(p), t);
+        }
+    } else {
+        float t;
+        memcpy(&t, &v, 4);
+        __stcs(reinterpret_cast<float*>(p), t);
+    }
+}
+
 }  // namespace vxq

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -72,6 +73,9 @@ inline void retain_mempool() {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    // L2 fetch granularity hint (bytes, 0-128) for the random spin-word gathers
+    if (const char* e = getenv("VXQ_L2_FETCH"))
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
     done[dev] = true;
 }
 
@@ -147,7 +151,33 @@ void bits_to_states(const uint32_t* sb, int64_t n, int64_t R, int64_t W, int8_t*
                     cudaStream_t s);
 void stable_order(const double* energies_dev, int64_t R, int64_t* order_dev, cudaStream_t s);
 
+// CUDA-event timer on one stream (the library's loop_ms)
+struct EventTimer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s;
+    explicit EventTimer(cudaStream_t st) : s(st) {
+        VXQ_CUDA(cudaEventCreate(&a));
+        VXQ_CUDA(cudaEventCreate(&b));
+    }
+    void start() { VXQ_CUDA(cudaEventRecord(a, s)); }
+    void stop() { VXQ_CUDA(cudaEventRecord(b, s)); }
+    double ms() {
+        float v = 0;
+        VXQ_CUDA(cudaEventSynchronize(b));
+        VXQ_CUDA(cudaEventElapsedTime(&v, a, b));
+        return v;
+    }
+    ~EventTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
 // ---- dynamics.cu
+// exact energies, +-1 states and best-first order from bit-packed spins sb[n][W]
+// (x/m outputs must be NULL); the common tail of every solver
+void finish_from_bits(Problem* p, int64_t R, int64_t W, const uint32_t* sb,
+                      const vxq_run_opts* opts, vxq_outputs* out, cudaStream_t s);
 void pa_solve(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, vxq_outputs* out,
               cudaStream_t s);
 void sbm_solve(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts,
@@ -186,5 +216,10 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
 // ---- host schedules (bit-exact with the reference's Python expressions)
 void pa_schedule(double lam0, int64_t T, double* out);   // lam0 * (1.0 - t / T)
 void sbm_schedule(double a0, int64_t T, double* out);    // np.linspace(0.0, a0, T)
+
+// ---- anneal.cu (simulated annealing, annealing.py:24-74)
+void sa_solve(Problem* p, const vxq_sa_params* prm, const vxq_run_opts* opts, vxq_outputs* out,
+              cudaStream_t s);
+void sa_schedule(double T_init, double T_final, int64_t sweeps, double* out);
 
 }  // namespace vxq

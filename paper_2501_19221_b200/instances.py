@@ -7,9 +7,9 @@ O(terms) Python dict.  Used by bench.py and the tests.
   cfg1  dense random QUBO N=100 on all i<=j pairs, Q ~ U[-1,1] (drawn like gen_random,
         generators.py:321-323) -> qubo_to_ising (transforms.py:36-56)
   cfg2  Sherrington-Kirkpatrick N=10^4: J_ij = +-1/sqrt(N) i.i.d., h = 0
-  cfg3  Pegasus-like N=5640 with 40,484 couplers (P16 fabric counts), J, h ~ U[-1,1].
-        The reference ships no Pegasus generator; this is a random graph
-        with P16's node and edge counts, not the Pegasus topology itself.
+  cfg3  Pegasus P16 (5640 fabric qubits, 40,484 couplers; pegasus_edges), J, h ~ U[-1,1]
+        drawn like gen_random("edge_list", "uniform") (generators.py:289-333).  The
+        reference ships no Pegasus generator; pegasus_edges builds it.
   cfg4  3-regular MaxCut N=10^6 (configuration model, loops/multi-edges dropped),
         J = +1, h = 0: minimising sum s_i s_j maximises the cut, cut = (|E| - H) / 2
   cfg5  random QUBO, mean degree 6, diagonal and off-diagonal ~ U[-1,1] -> Ising
@@ -59,12 +59,80 @@ def random_edges(n: int, m: int, seed: int):
     return keys // n, keys % n
 
 
-def pegasus_like(n: int = 5640, m: int = 40_484, seed: int = 16) -> IsingModel:
-    r, c = random_edges(n, m, seed)
+# Pegasus P(m) offsets (the standard shift pattern, offsets index 0): vertical qubit k of
+# a tile meets horizontal qubits shifted by _PEG_OFF0[k]; horizontal qubit k is shifted by
+# _PEG_OFF1[k].
+_PEG_OFF0 = (2, 2, 2, 2, 10, 10, 10, 10, 6, 6, 6, 6)
+_PEG_OFF1 = (6, 6, 6, 6, 2, 2, 2, 2, 10, 10, 10, 10)
+
+
+def pegasus_edges(m: int = 16) -> tuple[int, np.ndarray]:
+    """Edge list of the Pegasus graph P(m), fabric nodes only (the D-Wave Advantage
+    topology the paper's instances use; the reference has no generator for it,
+    SPEC.md:239).
+
+    A qubit is (u, w, k, z): orientation u (0 vertical, 1 horizontal), perpendicular
+    offset w < m, qubit index k < 12, parallel offset z < m-1.  Three coupler classes:
+      external  (u,w,k,z)-(u,w,k,z+1)            same line, consecutive segments
+      odd       (u,w,k,z)-(u,w,k+1,z), k even     paired neighbours
+      internal  (0,w,k,z)-(1, z+[kk<OFF0[k]], kk, w-[k<OFF1[kk]])   crossing lines
+    restricted to the fabric (qubits with at least one internal coupler: for u, tiles
+    w=0 drop k < min(OFF), tiles w=m-1 drop k >= 12-(12-max(OFF))).  Qubits are
+    relabelled 0..n-1 in (u, w, k, z) order.  P(16): 5640 qubits, 40,484 couplers,
+    maximum degree 15.  Returns (n, edges[E, 2]) in generation order
+    (external, odd, internal).
+    """
+    if m < 2:
+        raise ValueError("pegasus needs m >= 2")
+    m1 = m - 1
+    start = (min(_PEG_OFF1), min(_PEG_OFF0))
+    end = (12 - max(_PEG_OFF1), 12 - max(_PEG_OFF0))
+
+    def krange(u, w):
+        return range(start[u] if w == 0 else 0, 12 - (end[u] if w == m1 else 0))
+
+    def lin(u, w, k, z):
+        return ((u * m + w) * 12 + k) * m1 + z
+
+    def fabric(u, w, k, z):
+        return (w > 0 or k >= start[u]) and (w < m1 or k < 12 - end[u])
+
+    e = []
+    for u in (0, 1):
+        for w in range(m):
+            for k in krange(u, w):
+                for z in range(m1 - 1):
+                    e.append((lin(u, w, k, z), lin(u, w, k, z + 1)))
+    for u in (0, 1):
+        for w in range(m):
+            for k in krange(u, w)[::2]:
+                for z in range(m1):
+                    e.append((lin(u, w, k, z), lin(u, w, k + 1, z)))
+    for w in range(m):
+        for kk in range(12):
+            for k in range(0 if w else _PEG_OFF1[kk], 12 if w < m1 else _PEG_OFF1[kk]):
+                for z in range(m1):
+                    a = (0, w, k, z)
+                    b = (1, z + (kk < _PEG_OFF0[k]), kk, w - (k < _PEG_OFF1[kk]))
+                    if fabric(*a) and fabric(*b):
+                        e.append((lin(*a), lin(*b)))
+    e = np.asarray(e, dtype=np.int64)
+    used, e = np.unique(e, return_inverse=True)
+    return int(used.size), e.reshape(-1, 2)
+
+
+def pegasus(m: int = 16, seed: int = 16) -> IsingModel:
+    """gen_random("edge_list", "uniform", seed, edges=pegasus_edges(m)) restated
+    (generators.py:289-333): couplings drawn first in edge-list order, then biases, from
+    one Philox stream; J, h ~ U[-1, 1]."""
+    from .model import canonical_pairs
+
+    n, e = pegasus_edges(m)
     rng = _philox(seed)
-    J = rng.uniform(-1.0, 1.0, m)
-    h = rng.uniform(-1.0, 1.0, n)
-    return IsingModel(n=n, h=h, rows=r, cols=c, values=J + 0.0)
+    J = rng.uniform(-1.0, 1.0, size=e.shape[0])
+    h = rng.uniform(-1.0, 1.0, size=n)
+    r, c, v = canonical_pairs(e[:, 0], e[:, 1], J, n, allow_diagonal=False)
+    return IsingModel(n=n, h=h, rows=r, cols=c, values=v)
 
 
 def maxcut3(n: int = 1_000_000, seed: int = 4) -> IsingModel:
@@ -156,7 +224,7 @@ CONFIGS = {
     "cfg1": dict(desc="dense random QUBO N=100 -> Ising, R=64, T=1000", R=64, T=1000),
     "cfg2": dict(desc="dense Sherrington-Kirkpatrick N=10^4 (J=+-1/sqrt N), R=1024, T=1000",
                  R=1024, T=1000),
-    "cfg3": dict(desc="Pegasus-like N=5640 (40,484 couplers, P16 counts), R=4096, T=1000",
+    "cfg3": dict(desc="Pegasus P16 N=5640 (40,484 couplers), R=4096, T=1000",
                  R=4096, T=1000),
     "cfg4": dict(desc="3-regular MaxCut N=10^6, R=256, T=1000", R=256, T=1000),
     "cfg5": dict(desc="random QUBO N=2x10^8 mean degree 6, R=32", R=32, T=100),
@@ -169,7 +237,7 @@ def build(name: str, n: int | None = None) -> IsingModel:
     if name == "cfg2":
         return sk(n or 10_000)
     if name == "cfg3":
-        return pegasus_like()
+        return pegasus()
     if name == "cfg4":
         return maxcut3(n or 1_000_000)
     if name == "cfg5":

@@ -1,10 +1,12 @@
-"""Drop-in solvers: ``solve_pa`` / ``solve_sbm`` / ``integrate`` on the B200.
+"""Drop-in solvers: ``solve_pa`` / ``solve_sbm`` / ``integrate`` / ``solve_sa`` on the B200.
 
 Same names, arguments, results and error behaviour as the reference's
 ``qubokit.solve_pa`` (solvers/parallel_annealing.py:28-48), ``qubokit.solve_sbm``
 (solvers/bifurcation.py:50-67) and ``qubokit.solvers.bifurcation.integrate``
 (bifurcation.py:37-47); parameter records mirror ``PaParams`` / ``SbmParams``
-(solvers/common.py:94-144) and accept the reference's own records too.
+(solvers/common.py:94-144) and accept the reference's own records too.  ``solve_sa``
+(solvers/annealing.py:24-74, ``SaParams`` common.py:74-92) is the other batched-replica
+solver of the reference.
 
 Each call is one ``vxq_pa_solve`` / ``vxq_sbm_solve`` through the C-ABI: the
 replica streams are drawn on the device (bit-exact numpy Philox), the loop runs
@@ -111,7 +113,28 @@ class SbmParams:
         _positive("replicas", self.replicas)
 
 
-PARAM_CLASSES = {"pa": PaParams, "sbm": SbmParams}
+@dataclass
+class SaParams:
+    """Simulated annealing parameters (common.py:74-92)."""
+
+    sweeps: int = 1000
+    T_init: float | None = None      # None: 2 * model field scale
+    T_final: float | None = None     # None: 1e-3 * resolved T_init
+    schedule: str = "geometric"
+    replicas: int = 32
+    seed: int = 0
+
+    def validate(self):
+        _positive("sweeps", self.sweeps)
+        _positive("replicas", self.replicas)
+        if self.schedule != "geometric":
+            raise ValidationError("only the geometric schedule is supported")
+        if self.T_init is not None and self.T_final is not None:
+            if not (self.T_init >= self.T_final > 0):
+                raise ValidationError("need T_init >= T_final > 0")
+
+
+PARAM_CLASSES = {"sa": SaParams, "pa": PaParams, "sbm": SbmParams}
 
 
 def params_to_dict(params) -> dict:
@@ -220,6 +243,40 @@ def run_sbm(model, params, *, precision="fp32", path="auto", device=0, replica_b
     return RunResult(st, en, order, x, m, info)
 
 
+def sa_schedule(T_init: float, T_final: float, sweeps: int) -> np.ndarray:
+    """Geometric temperatures, the reference's expression (annealing.py:31-35)."""
+    if sweeps > 1:
+        ratio = (T_final / T_init) ** (1.0 / (sweeps - 1))
+        return T_init * ratio ** np.arange(sweeps)
+    return np.array([T_init], dtype=np.float64)
+
+
+def _sa_temps(model, params, device):
+    T_init = params.T_init if params.T_init is not None else \
+        2.0 * get_problem(model, device).lambda0()
+    T_final = params.T_final if params.T_final is not None else 1e-3 * T_init
+    return float(T_init), float(T_final), np.ascontiguousarray(
+        sa_schedule(float(T_init), float(T_final), int(params.sweeps)), dtype=np.float64)
+
+
+def run_sa(model, params, *, precision="fp32", path="auto", device=0, replica_begin=0,
+           cache=True) -> RunResult:
+    """One vxq_sa_solve call: per-replica best states / exact energies / order."""
+    params.validate()
+    dp = get_problem(model, device, cache=cache)
+    T0, T1, temps = _sa_temps(model, params, device)
+    c = _lib.SaParamsC(int(params.sweeps), T0, T1, int(params.replicas), _seed(params.seed),
+                       _lib.ptr(temps))
+    out, st, en, order, _, _, _ = _outputs(model.n, int(params.replicas), False)
+    opts = _opts(precision, path, replica_begin)
+    _lib.check(_lib.load().vxq_sa_solve(dp.handle, ctypes.byref(c), ctypes.byref(opts),
+                                        ctypes.byref(out)))
+    info = {"T_init": out.lambda0_used, "T_final": out.c0_used, "loop_ms": out.loop_ms,
+            "launches": out.launches, "path": _lib.PATH_NAMES.get(out.path_used, "?"),
+            "precision": precision}
+    return RunResult(st, en, order, None, None, info)
+
+
 def run_device(kind: str, model, params, states_ptr: int, energies_ptr: int, *,
                order_ptr: int | None = None, stream: int | None = None, precision="fp32",
                path="auto", device=0, replica_begin=0) -> dict:
@@ -275,6 +332,18 @@ def solve_sbm(model, params, *, precision: str = "fp32", path: str = "auto", dev
     t0 = time.perf_counter()
     res = run_sbm(model, params, precision=precision, path=path, device=device,
                   replica_begin=replica_begin, trace=trace, track_best=track_best)
+    return sampleset_from(res, int(params.replicas), params.seed, time.perf_counter() - t0,
+                          replica_begin)
+
+
+def solve_sa(model, params, *, precision: str = "fp32", path: str = "auto", device: int = 0,
+             replica_begin: int = 0) -> SampleSet:
+    """Simulated annealing on the B200 (drop-in for annealing.py:24-74): every replica
+    reports the best state seen along its trajectory."""
+    params.validate()
+    t0 = time.perf_counter()
+    res = run_sa(model, params, precision=precision, path=path, device=device,
+                 replica_begin=replica_begin)
     return sampleset_from(res, int(params.replicas), params.seed, time.perf_counter() - t0,
                           replica_begin)
 

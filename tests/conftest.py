@@ -10,6 +10,7 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
         sys.path.insert(0, p)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "reference_vectors.npz")
+GOLDEN_SA = os.path.join(ROOT, "tests", "golden", "reference_sa.npz")
 
 
 def pytest_configure(config):
@@ -19,6 +20,11 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden():
     return dict(np.load(GOLDEN))
+
+
+@pytest.fixture(scope="session")
+def golden_sa():
+    return dict(np.load(GOLDEN_SA))
 
 
 def has_gpu() -> bool:

@@ -27,13 +27,14 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
-    assert L.vxq_abi_version() == 2
+    assert L.vxq_abi_version() == 3
 
 
 def test_struct_layouts_match_header():
     # field order / sizes of the ctypes mirrors (x86-64 SysV)
     assert ctypes.sizeof(_lib.PaParamsC) == 48
     assert ctypes.sizeof(_lib.SbmParamsC) == 64
+    assert ctypes.sizeof(_lib.SaParamsC) == 48
     assert ctypes.sizeof(_lib.RunOptsC) == 32
     assert ctypes.sizeof(_lib.OutputsC) == 88
 
@@ -42,6 +43,16 @@ def test_struct_layouts_match_header():
 @pytest.mark.parametrize("a0", [1.0, 0.3, 7.77, 1e-300])
 def test_sbm_schedule_is_numpy_linspace(T, a0):
     assert np.array_equal(vxq.sbm_schedule(a0, T), np.linspace(0.0, a0, T))
+
+
+@pytest.mark.parametrize("sweeps", [1, 2, 1000])
+def test_sa_schedule_is_reference_expression(sweeps):
+    ratio = (0.002 / 2.0) ** (1.0 / (sweeps - 1)) if sweeps > 1 else 1.0
+    ref = 2.0 * ratio ** np.arange(sweeps) if sweeps > 1 else np.array([2.0])
+    assert np.array_equal(vxq.sa_schedule(2.0, 0.002, sweeps), ref)
+    out = np.empty(sweeps)
+    assert _lib.load().vxq_sa_schedule(2.0, 0.002, sweeps, _lib.ptr(out)) == 0
+    np.testing.assert_allclose(out, ref, rtol=4e-16, atol=0)  # C pow: within an ulp
 
 
 @pytest.mark.parametrize("T", [1, 7, 1000, 4096])
@@ -90,6 +101,15 @@ def test_params_validation_before_the_call():
     assert vxq.params_from_dict("pa", vxq.params_to_dict(p)) == p
     q = vxq.SbmParams(steps=10, dt=0.2, c0=0.5)
     assert vxq.params_from_dict("sbm", vxq.params_to_dict(q)) == q
+    # SaParams.validate (common.py:84-91)
+    for bad in (dict(sweeps=0), dict(replicas=0), dict(schedule="linear"),
+                dict(T_init=1.0, T_final=2.0), dict(T_init=1.0, T_final=0.0)):
+        with pytest.raises(vxq.ValidationError):
+            vxq.SaParams(**bad).validate()
+    a = vxq.SaParams(sweeps=77, T_init=3.0, T_final=0.5, replicas=8, seed=2)
+    assert vxq.params_from_dict("sa", vxq.params_to_dict(a)) == a
+    with pytest.raises(vxq.ValidationError):
+        vxq.params_from_dict("sa", {"swups": 10})
     # model validation (model.py:81-104)
     with pytest.raises(vxq.ValidationError):
         vxq.IsingModel.from_terms(3, couplings=[(1, 1, 2.0)])

@@ -63,3 +63,39 @@ def test_replica_streams_match_reference_layout():
     g = vxq.replica_streams(123, 3)
     bg = np.random.Philox(key=np.uint64(123)).jumped(2)
     assert np.array_equal(g[2].uniform(-1, 1, 5), np.random.Generator(bg).uniform(-1, 1, 5))
+
+
+def test_harness_gap_and_spectrum_mirror_reference():
+    from paper_2501_19221_b200 import harness
+    assert harness.optimality_gap(-9.0, -10.0) == pytest.approx(0.1)
+    assert harness.optimality_gap(-11.0, -10.0) == pytest.approx(-0.1)
+    with pytest.raises(vxq.ValidationError):
+        harness.optimality_gap(1.0, 0.0)
+    e, c = harness.spectrum(np.array([1.0, 2.0, 2.0, 4.0]), 3)
+    assert c.sum() == 4 and e[0] == 1.0 and e[-1] == 4.0
+    e, c = harness.spectrum(np.array([3.0, 3.0]), 5)
+    assert list(c) == [2]
+    with pytest.raises(vxq.ValidationError):
+        harness.spectrum(np.array([]), 2)
+
+
+def test_use_in_reference_patches_every_lookup(monkeypatch):
+    import sys
+    import types
+    from paper_2501_19221_b200 import harness
+    pkg = types.ModuleType("fakeqk")
+    subs = {}
+    for sub in ("solvers", "bench", "cli"):
+        m = types.ModuleType(f"fakeqk.{sub}")
+        for name in ("solve_pa", "solve_sbm", "solve_sa"):
+            setattr(m, name, name)
+        subs[sub] = m
+        monkeypatch.setitem(sys.modules, f"fakeqk.{sub}", m)
+    for name in ("solve_pa", "solve_sbm", "solve_sa"):
+        setattr(pkg, name, name)
+    harness.use_in_reference(pkg)
+    for m in [pkg, *subs.values()]:
+        assert m.solve_pa is vxq.solve_pa and m.solve_sa is vxq.solve_sa
+    harness.use_in_reference(pkg, restore=True)
+    for m in [pkg, *subs.values()]:
+        assert m.solve_pa == "solve_pa" and m.solve_sbm == "solve_sbm"

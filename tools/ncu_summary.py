@@ -17,7 +17,10 @@ def launches(path, top=15):
         name = r[ki].split("(")[0][-60:]
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
-        a[1] += float(r[vi].replace(",", ""))
+        try:
+            a[1] += float(r[vi].replace(",", ""))
+        except ValueError:
+            pass
     tot = sum(v[1] for v in agg.values())
     out = []
     for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
@@ -53,11 +56,18 @@ def full(rep):
     if len(rows) > 3:
         h = rows[1]
         si, sc = h.index("Warp Stall Sampling (All Samples)"), h.index("Source")
-        data = rows[2:]
-        tot = sum(float(r[si] or 0) for r in data) or 1.0
+        def num(x):
+            try:
+                return float(x or 0)
+            except ValueError:
+                return 0.0
+        data = [r for r in rows[2:] if len(r) > max(si, sc)]
+        for r in data:
+            r[si] = num(r[si])
+        tot = sum(r[si] for r in data) or 1.0
         out.append("  top stall sites (share of warp samples):")
         for r in sorted(data, key=lambda r: -float(r[si] or 0))[:12]:
-            out.append(f"    {100 * float(r[si]) / tot:5.1f}%  {r[sc][:100]}")
+            out.append(f"    {100 * r[si] / tot:5.1f}%  {r[sc][:100]}")
     return "\n".join(out)
 
 

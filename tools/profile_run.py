@@ -38,7 +38,9 @@ def main():
     print(f"build {t1 - t0:.2f}s  upload+csr {t2 - t1:.2f}s  n={m.n} m={m.num_couplings}")
     for k in range(a.repeat):
         t3 = time.perf_counter()
-        if a.solver == "pa":
+        if a.solver == "sa":
+            r = vxq.run_sa(m, vxq.SaParams(sweeps=a.T, replicas=R, seed=k), path=a.path)
+        elif a.solver == "pa":
             r = vxq.run_pa(m, vxq.PaParams(steps=a.T, replicas=R, seed=k), path=a.path)
         else:
             r = vxq.run_sbm(m, vxq.SbmParams(steps=a.T, dt=0.05, replicas=R, seed=k),
