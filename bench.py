@@ -70,14 +70,16 @@ def peaks():
     return FALLBACK_HBM_GBS, 1400.0, "fallback"
 
 
-def measured_traffic(kernel: str):
-    """DRAM bytes per dynamics step of `kernel` from the newest committed ncu capture."""
+def measured_traffic(kernel: str, config: str):
+    """DRAM bytes per dynamics step of `kernel` on `config` (key "kernel@config") from the
+    newest committed ncu --set full capture (profiles/r*/traffic.json)."""
     import glob
+    key = f"{kernel}@{config}"
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")),
                        reverse=True):
         d = json.load(open(path))
-        if kernel in d:
-            return d[kernel]["dram_bytes_per_step"], os.path.relpath(path, ROOT)
+        if key in d:
+            return d[key]["dram_bytes_per_step"], os.path.relpath(path, ROOT)
     return None, None
 
 
@@ -382,11 +384,11 @@ def run_ours(args):
         flops = 2.0 * n * R * n
         achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
         fp8_peak = 2.0 * bf16
-        tr, tsrc = measured_traffic("k_dense_pa_run")
+        tr, tsrc = measured_traffic("k_dense_run", args.config)
         roof = {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp8_peak, "traffic": tr, "traffic_unit": "bytes/step",
                 "traffic_source": tsrc,
-                "kernel": "k_dense_pa_run: tcgen05.mma kind::f8f6f4 J.S + fused PA epilogue (persistent)",
+                "kernel": "k_dense_run: tcgen05.mma kind::f8f6f4 J.S + fused PA epilogue (persistent)",
                 "peak_note": f"2 x measured bf16 sustained ({bf16} TF/s, {src})",
                 "frac_of_bf16_measured": achieved / bf16,
                 "flops_per_update": 2.0 * n, "units_per_launch": R * n,
@@ -394,11 +396,14 @@ def run_ours(args):
     else:
         B = bytes_per_update(args.solver, dbar, R)
         achieved = B * R * n / (mean_step_kernel_ms / 1e3) / 1e9
-        tr, tsrc = measured_traffic(f"k_{args.solver}_step")
+        kname = f"k_{args.solver}_step"
+        if args.solver == "pa" and R <= 32 and info.get("path") in ("sparse", "rowpart"):
+            kname = "k_pa_step_coop"  # one sign word per row: cooperative warp-CSR variant
+        tr, tsrc = measured_traffic(kname, args.config)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": tr, "traffic_unit": "bytes/step",
                 "traffic_source": tsrc,
-                "kernel": f"k_{args.solver}_step ({info.get('path')})",
+                "kernel": f"{kname} ({info.get('path')})",
                 "bytes_per_update": B, "units_per_launch": R * n,
                 "mean_launch_ms": mean_step_kernel_ms,
                 "frac_of_8TBs_nominal": achieved / 8000.0, "peak_source": src}
@@ -410,13 +415,22 @@ def run_ours(args):
     elif not args.no_e2e:
         solve = vxq.solve_pa if args.solver == "pa" else vxq.solve_sbm
         K = max(1, min(args.steps, 3))
-        rows = np.ascontiguousarray(model.rows)
-        h2d = int(model.rows.nbytes + model.cols.nbytes + model.values.nbytes + model.h.nbytes)
+
+        def pinned(a):  # the step's host inputs live in pinned memory (staged once)
+            a = np.ascontiguousarray(a)
+            t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+            v = t.numpy()
+            v[...] = a
+            return v, t
+
+        (rows, _t0), (cols, _t1), (vals, _t2), (hv, _t3) = (
+            pinned(model.rows), pinned(model.cols), pinned(model.values), pinned(model.h))
+        h2d = int(rows.nbytes + cols.nbytes + vals.nbytes + hv.nbytes)
         d2h = int(R * n + 16 * R)
         walls = []
         for k in range(K + 1):
-            fresh = vxq.IsingModel(n=n, h=model.h, rows=rows, cols=model.cols,
-                                   values=model.values, offset=model.offset)
+            fresh = vxq.IsingModel(n=n, h=hv, rows=rows, cols=cols, values=vals,
+                                   offset=model.offset)
             torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()

@@ -32,6 +32,8 @@ namespace vxq {
 namespace {
 
 constexpr int kSaSmemMax = 200 * 1024;
+constexpr int kPf = 4;  // field prefetch depth (spins ahead)
+constexpr int kB = 8;   // neighbour updates per batch
 
 __global__ void k_sa_init_spins(int64_t n, int64_t W, int64_t R_pad, uint64_t seed,
                                 int64_t rbegin, uint32_t* __restrict__ sb) {
@@ -133,15 +135,19 @@ __global__ void __launch_bounds__(32) k_sa_run(SaArgs a) {
     const double inv53 = 1.0 / 9007199254740992.0;
     for (int64_t s = 0; s < a.sweeps; ++s) {
         const double Tt = a.temps[s];
-        T fn = Fb[0];
+        // pf[d] = field of spin i + d (prefetched kPf spins ahead; patched when a flip of
+        // spin i updates one of them)
+        T pf[kPf];
+#pragma unroll
+        for (int d = 0; d < kPf; ++d) pf[d] = d < n ? Fb[d * fs] : (T)0;
         uint32_t wn = sbw[0];
         for (int64_t i = 0; i < n; ++i) {
-            const T f = fn;
+            const T f = pf[0];
+#pragma unroll
+            for (int d = 0; d + 1 < kPf; ++d) pf[d] = pf[d + 1];
+            pf[kPf - 1] = i + kPf < n ? Fb[(i + kPf) * fs] : (T)0;
             const uint32_t word = wn;
-            if (i + 1 < n) {  // prefetch the next spin's field and word
-                fn = Fb[(i + 1) * fs];
-                wn = sbw[(i + 1) * ws];
-            }
+            if (i + 1 < n) wn = sbw[(i + 1) * ws];
             const uint64_t q = k >> 2;
             if (q != kb) {
                 blk = philox4x64_10(q + 1, 0, rg, 0, a.seed, 0);
@@ -167,34 +173,54 @@ __global__ void __launch_bounds__(32) k_sa_run(SaArgs a) {
             if (acc) {
                 E = __dadd_rn(E, dE);
                 const T d2 = up ? (T)-2 : (T)2;  // 2 * s_new
-                int64_t e = indptr[i];
-                const int64_t e1 = indptr[i + 1];
-                for (; e + 4 <= e1; e += 4) {  // distinct columns: batch the RMWs
-                    const int j0 = indices[e], j1 = indices[e + 1], j2 = indices[e + 2],
-                              j3 = indices[e + 3];
-                    const T v0 = O::mul(d2, data[e]), v1 = O::mul(d2, data[e + 1]),
-                            v2 = O::mul(d2, data[e + 2]), v3 = O::mul(d2, data[e + 3]);
-                    T* p0 = Fb + j0 * fs;
-                    T* p1 = Fb + j1 * fs;
-                    T* p2 = Fb + j2 * fs;
-                    T* p3 = Fb + j3 * fs;
-                    const T f0 = *p0, f1 = *p1, f2 = *p2, f3 = *p3;
-                    *p0 = O::add(f0, v0);
-                    *p1 = O::add(f1, v1);
-                    *p2 = O::add(f2, v2);
-                    *p3 = O::add(f3, v3);
-                    const int64_t nx = i + 1;
-                    if (j0 == nx) fn = O::add(fn, v0);
-                    if (j1 == nx) fn = O::add(fn, v1);
-                    if (j2 == nx) fn = O::add(fn, v2);
-                    if (j3 == nx) fn = O::add(fn, v3);
+                // kB entries per batch: all index / value / field loads of a batch are
+                // issued before its stores (columns within a row are distinct); full
+                // batches unpredicated, the tail predicated
+                const int64_t nx = i + 1;
+                const int64_t e0 = indptr[i], e1 = indptr[i + 1];
+                auto patch = [&](int j, T v) {
+                    if ((uint64_t)(j - nx) < (uint64_t)kPf) {  // rare
+#pragma unroll
+                        for (int d = 0; d < kPf; ++d)
+                            if (j == nx + d) pf[d] = O::add(pf[d], v);
+                    }
+                };
+                int64_t e = e0;
+                for (; e + kB <= e1; e += kB) {
+                    int j[kB];
+                    T v[kB], fv[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        j[u] = indices[e + u];
+                        v[u] = O::mul(d2, data[e + u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) fv[u] = Fb[(int64_t)j[u] * fs];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        Fb[(int64_t)j[u] * fs] = O::add(fv[u], v[u]);
+                        patch(j[u], v[u]);
+                    }
                 }
-                for (; e < e1; ++e) {
-                    const int j = indices[e];
-                    const T v = O::mul(d2, data[e]);
-                    T* pj = Fb + j * fs;
-                    *pj = O::add(*pj, v);
-                    if (j == i + 1) fn = O::add(fn, v);
+                if (e < e1) {
+                    int j[kB];
+                    T v[kB], fv[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const bool ok = e + u < e1;
+                        j[u] = ok ? indices[e + u] : -1;
+                        v[u] = ok ? O::mul(d2, data[e + u]) : (T)0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kB; ++u)
+                        if (j[u] >= 0) fv[u] = Fb[(int64_t)j[u] * fs];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        if (j[u] >= 0) {
+                            Fb[(int64_t)j[u] * fs] = O::add(fv[u], v[u]);
+                            patch(j[u], v[u]);
+                        }
+                    }
                 }
             }
         }

@@ -5,7 +5,6 @@
 #include <stdint.h>
 
 #include <cmath>
-#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -73,9 +72,6 @@ inline void retain_mempool() {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    // L2 fetch granularity hint (bytes, 0-128) for the random spin-word gathers
-    if (const char* e = getenv("VXQ_L2_FETCH"))
-        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
     done[dev] = true;
 }
 
