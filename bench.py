@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="cfg5 row partition at N>1: NCCL all-gather or fused peer stores")
     return ap.parse_args()
 
 
@@ -311,13 +313,19 @@ def run_ours(args):
     if rowpart:
         # config 5: the instance is split by rows (strong scaling); every rank holds the
         # generated problem and all-gathers the bit-packed spins after each step (NCCL)
-        from paper_2501_19221_b200.rowpart import (GpuSession, drive, exchange_row_bytes,
-                                                    gather_inplace, row_split)
+        from paper_2501_19221_b200.rowpart import (GpuSession, PeerExchange, drive,
+                                                    exchange_row_bytes, gather_inplace,
+                                                    row_split)
         rbegin = 0
         spans, Bq = row_split(n, world)
         rbytes = exchange_row_bytes(args.solver, R, args.precision)
-        xbufs = [torch.zeros(Bq * world * rbytes, dtype=torch.uint8, device="cuda")
-                 for _ in range(2)]
+        px = None
+        if args.exchange == "p2p":  # IPC-shared buffers, allocated once
+            px = PeerExchange(Bq * world * rbytes, world, rank, local)
+            xbufs = px.bufs()
+        else:
+            xbufs = [torch.zeros(Bq * world * rbytes, dtype=torch.uint8, device="cuda")
+                     for _ in range(2)]
 
     def solve_dev():
         if rowpart:
@@ -327,11 +335,18 @@ def run_ours(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            drive(sess, xbufs, T, lambda b: gather_inplace(b, rank, world, Bq * rbytes))
+            if px is not None:
+                px.attach(sess)  # the step kernels store into every rank's buffers
+                for t in range(T):
+                    sess.step(t)
+            else:
+                drive(sess, xbufs, T, lambda b: gather_inplace(b, rank, world, Bq * rbytes))
             e1.record(stream)
             sess.finish_device(states.data_ptr(), energies.data_ptr(), order.data_ptr())
             sess.close()
             torch.cuda.synchronize()
+            if px is not None:  # no rank reuses the buffers while a peer is still finishing
+                dist.barrier()
             return {"loop_ms": e0.elapsed_time(e1), "launches": T + 4, "path": "rowpart"}
         return run_device(args.solver, model, params, states.data_ptr(), energies.data_ptr(),
                           order_ptr=order.data_ptr(), stream=stream.cuda_stream,
@@ -484,7 +499,10 @@ def run_ours(args):
                        "steps_per_solve": T, "path": info.get("path"),
                        "precision": args.precision,
                        "l2": "flushed between timed solves (256 MiB write)",
-                       "parallelism": (f"row-partitioned x{world} (NCCL all-gather of spins "
+                       "parallelism": (f"row-partitioned x{world} ("
+                                       + ("fused peer-memory stores" if args.exchange == "p2p"
+                                          else "NCCL all-gather")
+                                       + " of spins "
                                        f"per step)" if rowpart else f"replica-sharded x{world}"),
                        "instance_build_s": round(t_build, 2)},
             "roofline": roof,

@@ -196,6 +196,29 @@ VXQ_API int vxq_session_step(vxq_session* s, int64_t t);
 VXQ_API int vxq_session_finish(vxq_session* s, vxq_outputs* out);
 VXQ_API int vxq_session_destroy(vxq_session* s);
 
+/* ---- Fused exchange over NVLink peer memory (replaces the caller's all-gather) ----
+ * Every rank allocates its two exchange buffers and a flag array of `world` uint64 with
+ * vxq_exchange_alloc (zeroed, IPC-shareable), shares vxq_ipc_handle() of each with the
+ * other ranks (e.g. torch.distributed.all_gather_object) and opens the peers' handles with
+ * vxq_ipc_open.  vxq_session_set_peers(s, world, rank, xbuf0[world], xbuf1[world],
+ * flags[world]) (own pointers at [rank]) pushes state 0 of the local rows to every peer;
+ * from then on vxq_session_step stores each produced word / q vector directly into every
+ * rank's buffer from the step kernel, publishes "state t+1 complete" into every rank's
+ * flags[rank] (release, system scope) and, before step t, waits on its own flags for
+ * state t from all sources (acquire; bounded at 30 s -> VXQ_ERR_CUDA at finish).
+ * Flag values are (epoch << 32) + state + 1: reuse one exchange for several sessions with
+ * a larger epoch each time (same on every rank) and a barrier between sessions.
+ * No caller collective is needed between steps.                                        */
+#define VXQ_IPC_HANDLE_BYTES 64
+VXQ_API int vxq_exchange_alloc(int device, int64_t bytes, void** out);
+VXQ_API int vxq_exchange_free(void* ptr);
+VXQ_API int vxq_ipc_handle(const void* dev_ptr, void* handle_out);
+VXQ_API int vxq_ipc_open(const void* handle, int device, void** dev_ptr);
+VXQ_API int vxq_ipc_close(void* dev_ptr);
+VXQ_API int vxq_session_set_peers(vxq_session* s, int32_t world, int32_t rank,
+                                  uint32_t epoch, void* const* xbuf0, void* const* xbuf1,
+                                  uint64_t* const* flags);
+
 /* Exact energies of R spin states [R][n] int8 (host, or device if
  * opts->outputs_on_device) -> energies[R] (same residency). */
 VXQ_API int vxq_energies(vxq_problem* p, const int8_t* states, int64_t R, double* energies,

@@ -33,8 +33,10 @@ EXPORTS = (
     "vxq_pa_schedule", "vxq_sbm_schedule", "vxq_last_error", "vxq_abi_version",
     "vxq_device_count", "vxq_exchange_row_bytes", "vxq_session_create", "vxq_session_step",
     "vxq_session_finish", "vxq_session_destroy", "vxq_problem_generate", "vxq_problem_export",
-    "vxq_sa_solve", "vxq_sa_schedule",
+    "vxq_sa_solve", "vxq_sa_schedule", "vxq_session_set_peers", "vxq_exchange_alloc",
+    "vxq_exchange_free", "vxq_ipc_handle", "vxq_ipc_open", "vxq_ipc_close",
 )
+IPC_HANDLE_BYTES = 64
 
 
 class PaParamsC(ctypes.Structure):
@@ -109,6 +111,12 @@ def load():
         L.vxq_session_step.argtypes = [P, i64]
         L.vxq_session_finish.argtypes = [P, ctypes.POINTER(OutputsC)]
         L.vxq_session_destroy.argtypes = [P]
+        L.vxq_session_set_peers.argtypes = [P, i32, i32, ctypes.c_uint32, P, P, P]
+        L.vxq_exchange_alloc.argtypes = [ctypes.c_int, i64, ctypes.POINTER(P)]
+        L.vxq_exchange_free.argtypes = [P]
+        L.vxq_ipc_handle.argtypes = [P, P]
+        L.vxq_ipc_open.argtypes = [P, ctypes.c_int, ctypes.POINTER(P)]
+        L.vxq_ipc_close.argtypes = [P]
         L.vxq_last_error.restype = ctypes.c_char_p
         L.vxq_abi_version.restype = ctypes.c_int
         L.vxq_device_count.restype = ctypes.c_int

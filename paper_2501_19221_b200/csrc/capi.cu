@@ -314,6 +314,65 @@ int vxq_session_finish(vxq_session* s, vxq_outputs* out) {
     });
 }
 
+int vxq_session_set_peers(vxq_session* s, int32_t world, int32_t rank, uint32_t epoch,
+                          void* const* xbuf0, void* const* xbuf1, uint64_t* const* flags) {
+    return guarded([&] {
+        VXQ_REQUIRE(s, "null session");
+        SessionBox* b = reinterpret_cast<SessionBox*>(s);
+        VXQ_CUDA(cudaSetDevice(b->device));
+        vxq::session_set_peers(b->S, world, rank, epoch, xbuf0, xbuf1, flags);
+    });
+}
+
+int vxq_exchange_alloc(int device, int64_t bytes, void** out) {
+    return guarded([&] {
+        VXQ_REQUIRE(out && bytes > 0, "invalid exchange allocation");
+        *out = nullptr;
+        DeviceGuard dg(device);
+        void* p = nullptr;
+        VXQ_CUDA(cudaMalloc(&p, (size_t)bytes));  // plain cudaMalloc: IPC-shareable
+        cudaError_t e = cudaMemset(p, 0, (size_t)bytes);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            VXQ_CUDA(e);
+        }
+        *out = p;
+    });
+}
+
+int vxq_exchange_free(void* ptr) {
+    return guarded([&] {
+        if (ptr) VXQ_CUDA(cudaFree(ptr));
+    });
+}
+
+int vxq_ipc_handle(const void* dev_ptr, void* handle_out) {
+    return guarded([&] {
+        VXQ_REQUIRE(dev_ptr && handle_out, "null argument");
+        static_assert(sizeof(cudaIpcMemHandle_t) == VXQ_IPC_HANDLE_BYTES, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        VXQ_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+        memcpy(handle_out, &h, sizeof(h));
+    });
+}
+
+int vxq_ipc_open(const void* handle, int device, void** dev_ptr) {
+    return guarded([&] {
+        VXQ_REQUIRE(handle && dev_ptr, "null argument");
+        *dev_ptr = nullptr;
+        DeviceGuard dg(device);
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handle, sizeof(h));
+        VXQ_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int vxq_ipc_close(void* dev_ptr) {
+    return guarded([&] {
+        if (dev_ptr) VXQ_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    });
+}
+
 int vxq_session_destroy(vxq_session* s) {
     return guarded([&] {
         if (!s) return;

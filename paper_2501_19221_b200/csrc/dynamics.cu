@@ -138,6 +138,24 @@ __global__ void k_pack_signs(const T* __restrict__ x, int64_t row0, int64_t nrow
     }
 }
 
+// Output of a step: the local exchange buffer plus, for a row-partitioned rank with
+// peers, every peer's copy of it (CUDA IPC pointers over NVLink).  Each produced word /
+// vector is stored to all n destinations from registers, so the exchange overlaps the
+// step instead of following it as a separate all-gather.
+constexpr int kMaxDests = 8;
+template <typename P>
+struct Dests {
+    P* p[kMaxDests];
+    int n;
+};
+template <typename P>
+inline Dests<P> one_dest(P* ptr) {
+    Dests<P> d{};
+    d.p[0] = ptr;
+    d.n = 1;
+    return d;
+}
+
 // ------------------------------------------------------------------ PA step (sparse)
 // One warp owns row i and CPW consecutive replica chunks (CPW * 32 * V replicas): the CSR
 // row is read once for all of them and CPW x more loads are in flight per warp.
@@ -152,7 +170,7 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
                                                  T lam, T eta, T alpha, T* __restrict__ x,
                                                  T* __restrict__ m,
                                                  const uint32_t* __restrict__ sb_in,
-                                                 uint32_t* __restrict__ sb_out) {
+                                                 const Dests<uint32_t> sb_out) {
     using O = Ops<T>;
     constexpr int NB = V * CPW;  // values per lane == sign words per (row, warp)
     const int lane = threadIdx.x & 31;
@@ -226,7 +244,8 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
             xv[g].v[b] = xn;
             mv[g].v[b] = mn;
             uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
-            if (lane == g * V + b) sb_out[i * W + c0 * V + g * V + b] = word;
+            if (lane == g * V + b)
+                for (int d = 0; d < sb_out.n; ++d) sb_out.p[d][i * W + c0 * V + g * V + b] = word;
         }
         const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
         st_cs<T, V>(x + base, xv[g]);
@@ -245,7 +264,7 @@ __global__ void __launch_bounds__(256) k_pa_step_coop(int64_t row0, int64_t nrow
                                                       T lam, T eta, T alpha, T* __restrict__ x,
                                                       T* __restrict__ m,
                                                       const uint32_t* __restrict__ sb_in,
-                                                      uint32_t* __restrict__ sb_out) {
+                                                      const Dests<uint32_t> sb_out) {
     using O = Ops<T>;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -299,7 +318,8 @@ __global__ void __launch_bounds__(256) k_pa_step_coop(int64_t row0, int64_t nrow
         __stcs(x + il * 32 + lane, xn);
         __stcs(m + il * 32 + lane, mn);
         const uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
-        if (lane == 0) sb_out[i] = word;
+        if (lane == 0)
+            for (int d = 0; d < sb_out.n; ++d) sb_out.p[d][i] = word;
     }
 }
 
@@ -314,7 +334,7 @@ template <typename T, int V>
 __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, int64_t R_pad,
                                                   Operator<T> op, const T* __restrict__ g,
                                                   SbmScalars<T> sc, const T* __restrict__ q_in,
-                                                  T* __restrict__ q_out, T* __restrict__ p) {
+                                                  const Dests<T> q_out, T* __restrict__ p) {
     using O = Ops<T>;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -372,7 +392,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         qv.v[b] = qn;
         pv.v[b] = pn;
     }
-    *reinterpret_cast<Vec<T, V>*>(q_out + base) = qv;
+    for (int d = 0; d < q_out.n; ++d) *reinterpret_cast<Vec<T, V>*>(q_out.p[d] + base) = qv;
     st_cs<T, V>(p + pbase, pv);
 }
 
@@ -631,7 +651,7 @@ int block_threads(int64_t items) {
 
 template <typename T>
 void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T eta, T alpha,
-                    T* x, T* m, const uint32_t* sbi, uint32_t* sbo, cudaStream_t s) {
+                    T* x, T* m, const uint32_t* sbi, const Dests<uint32_t>& sbo, cudaStream_t s) {
     const int64_t chunks = L.R_pad / (32 * L.V);
     if (L.R_pad == 32) {  // one sign word per row: cooperative warp-CSR over 8 rows
         constexpr int RPW = 8;
@@ -657,10 +677,15 @@ void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T
     }
 #undef VXQ_PA_STEP
 }
+template <typename T>
+void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T eta, T alpha,
+                    T* x, T* m, const uint32_t* sbi, uint32_t* sbo, cudaStream_t s) {
+    launch_pa_step<T>(L, op, h, lam, eta, alpha, x, m, sbi, one_dest(sbo), s);
+}
 
 template <typename T>
 void launch_sbm_step(const Layout& L, const Operator<T>& op, const T* g, SbmScalars<T> sc,
-                     const T* qi, T* qo, T* p, cudaStream_t s) {
+                     const T* qi, const Dests<T>& qo, T* p, cudaStream_t s) {
     int64_t warps = L.nrows * (L.R_pad / (32 * L.V));
     unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
     switch (L.V) {
@@ -671,6 +696,11 @@ void launch_sbm_step(const Layout& L, const Operator<T>& op, const T* g, SbmScal
                 k_sbm_step<T, 4><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, qo, p);
             break;
     }
+}
+template <typename T>
+void launch_sbm_step(const Layout& L, const Operator<T>& op, const T* g, SbmScalars<T> sc,
+                     const T* qi, T* qo, T* p, cudaStream_t s) {
+    launch_sbm_step<T>(L, op, g, sc, qi, one_dest(qo), p, s);
 }
 
 template <typename T>
@@ -1169,7 +1199,54 @@ void sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t* bt_indice
 //   SBM: q          [rows_alloc][R_pad] fp32/64 (interleaved replica layout)
 // Buffer k & 1 holds state k; init writes state 0 (local rows), step t reads buffer t & 1
 // and writes the local rows of buffer (t + 1) & 1.
+//
+// Fused exchange (set_peers): instead of a caller all-gather, the step kernels store every
+// produced word / q vector straight into all ranks' copies of the exchange buffer (CUDA
+// IPC pointers over NVLink), and the ranks synchronise through one flag per (rank, source):
+// after writing state k a rank release-stores k + 1 into flags[rank] of every peer; before
+// step t it acquire-polls its own flags until every source shows >= t + 1 (state t
+// complete).  A rank therefore starts step t only after every peer has finished step t - 1,
+// i.e. stopped reading the buffer that step t overwrites, so two buffers suffice.
 namespace vxq {
+
+namespace {
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// state k complete on this rank: publish k + 1 to every rank's flag slot `rank`
+// (stream order puts the step kernel's stores -- local and remote -- before this kernel)
+__global__ void k_signal(const Dests<uint64_t> flags, int rank, uint64_t v) {
+    if ((int)threadIdx.x < flags.n) {
+        __threadfence_system();
+        st_release_sys(flags.p[threadIdx.x] + rank, v);
+    }
+}
+
+// wait until every source rank has published >= need; bounded (30 s), then reports
+// through *status instead of hanging the GPU
+__global__ void k_wait(const uint64_t* flags, int n, uint64_t need, int* status) {
+    if ((int)threadIdx.x >= n) return;
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_sys(flags + threadIdx.x) < need) {
+        __nanosleep(200);
+        if (global_ns() - t0 > 30ull * 1000000000ull) {
+            atomicExch(status, 1);
+            return;
+        }
+    }
+}
+}  // namespace
 
 struct Session {
     Problem* p = nullptr;
@@ -1186,9 +1263,18 @@ struct Session {
     double dt = 0, a0 = 0, c0 = 0, q_cap = 0, amp = 0;            // SBM
     cudaStream_t s = nullptr;
     bool own_stream = false;
+    // fused exchange (set_peers)
+    int world = 1, rank = 0;
+    bool peers = false;
+    Dests<void> pxb[2] = {};      // every rank's exchange buffers (own at [rank])
+    Dests<uint64_t> pflags = {};  // every rank's flag array (own at [rank])
+    int* status = nullptr;        // device: 1 = peer wait timed out
+    uint64_t epoch = 0;           // flag values are (epoch << 32) + state + 1
+    int64_t row_bytes = 0;
     ~Session() {
         if (x) cudaFree(x);
         if (m) cudaFree(m);
+        if (status) cudaFree(status);
         if (own_stream && s) cudaStreamDestroy(s);
     }
 };
@@ -1219,14 +1305,30 @@ void session_init_t(Session* S) {
     }
 }
 
+template <typename P>
+Dests<P> cast_dests(const Dests<void>& d) {
+    Dests<P> o{};
+    for (int k = 0; k < d.n; ++k) o.p[k] = static_cast<P*>(d.p[k]);
+    o.n = d.n;
+    return o;
+}
+
 template <typename T>
 void session_step_t(Session* S, int64_t t) {
     const Layout& L = S->L;
+    const int nb = (t + 1) & 1;
+    if (S->peers) {  // state t complete on every rank
+        k_wait<<<1, 32, 0, S->s>>>(S->pflags.p[S->rank], S->world, S->epoch + (uint64_t)t + 1,
+                                   S->status);
+        VXQ_CHECK_LAUNCH();
+    }
     if (S->solver == 0) {
         Operator<T> op = problem_operator<T>(S->p, (T)1);
+        const Dests<uint32_t> out = S->peers ? cast_dests<uint32_t>(S->pxb[nb])
+                                             : one_dest((uint32_t*)S->xb[nb]);
         launch_pa_step<T>(L, op, pick<T>(S->p->h64, S->p->h32), (T)S->sched[t], (T)S->eta,
-                          (T)S->alpha, (T*)S->x, (T*)S->m, (const uint32_t*)S->xb[t & 1],
-                          (uint32_t*)S->xb[(t + 1) & 1], S->s);
+                          (T)S->alpha, (T*)S->x, (T*)S->m, (const uint32_t*)S->xb[t & 1], out,
+                          S->s);
     } else {
         SbmScalars<T> sc;
         sc.a_t = (T)S->sched[t];
@@ -1236,15 +1338,30 @@ void session_step_t(Session* S, int64_t t) {
         sc.dta0 = (T)(S->dt * S->a0);
         sc.q_cap = (T)S->q_cap;
         Operator<T> op = problem_operator<T>(S->p, (T)-1);
+        const Dests<T> out = S->peers ? cast_dests<T>(S->pxb[nb]) : one_dest((T*)S->xb[nb]);
         launch_sbm_step<T>(L, op, pick<T>(S->p->g64, S->p->g32), sc, (const T*)S->xb[t & 1],
-                           (T*)S->xb[(t + 1) & 1], (T*)S->x, S->s);
+                           out, (T*)S->x, S->s);
     }
     VXQ_CHECK_LAUNCH();
+    if (S->peers) {
+        k_signal<<<1, 32, 0, S->s>>>(S->pflags, S->rank, S->epoch + (uint64_t)t + 2);
+        VXQ_CHECK_LAUNCH();
+    }
 }
 
 template <typename T>
 void session_finish_t(Session* S, int64_t T_, vxq_outputs* out, const vxq_run_opts* opts) {
     // full final state: PA sign bits / SBM q in buffer T & 1 (all rows, after the gather)
+    if (S->peers) {
+        k_wait<<<1, 32, 0, S->s>>>(S->pflags.p[S->rank], S->world, S->epoch + (uint64_t)T_ + 1,
+                                   S->status);
+        VXQ_CHECK_LAUNCH();
+        int st = 0;
+        VXQ_CUDA(cudaMemcpyAsync(&st, S->status, sizeof(int), cudaMemcpyDeviceToHost, S->s));
+        VXQ_CUDA(cudaStreamSynchronize(S->s));
+        if (st) throw Error(VXQ_ERR_CUDA, "row-partition exchange: a peer did not publish its "
+                                          "rows within 30 s");
+    }
     Layout F = S->L;
     F.row0 = 0;
     F.nrows = S->p->n;
@@ -1288,6 +1405,7 @@ Session* session_create(Problem* p, int solver, const vxq_pa_params* pa,
     S->xb[0] = xbuf0;
     S->xb[1] = xbuf1;
     S->s = s;
+    S->row_bytes = exchange_row_bytes(solver, R, S->prec);
     S->sched.resize(T_);
     if (solver == 0) {
         S->seed = pa->seed;
@@ -1321,6 +1439,39 @@ void session_finish(Session* S, vxq_outputs* out, const vxq_run_opts* opts) {
     else session_finish_t<float>(S, T_, out, opts);
     out->lambda0_used = S->lam0;
     out->c0_used = S->c0;
+}
+
+void session_set_peers(Session* S, int world, int rank, uint32_t epoch, void* const* xbuf0,
+                       void* const* xbuf1, uint64_t* const* flags) {
+    VXQ_REQUIRE(world >= 1 && world <= kMaxDests, "world must be in [1, 8]");
+    VXQ_REQUIRE(rank >= 0 && rank < world, "rank out of range");
+    VXQ_REQUIRE(xbuf0 && xbuf1 && flags, "peer pointer arrays required");
+    VXQ_REQUIRE(xbuf0[rank] == S->xb[0] && xbuf1[rank] == S->xb[1],
+                "xbuf0/xbuf1[rank] must be this session's own exchange buffers");
+    VXQ_REQUIRE(!S->peers, "peers already set");
+    VXQ_REQUIRE((uint64_t)S->sched.size() + 2 < (1ull << 32), "too many steps for the flag epoch");
+    S->world = world;
+    S->rank = rank;
+    S->epoch = (uint64_t)epoch << 32;
+    for (int k = 0; k < world; ++k) {
+        VXQ_REQUIRE(xbuf0[k] && xbuf1[k] && flags[k], "null peer pointer");
+        S->pxb[0].p[k] = xbuf0[k];
+        S->pxb[1].p[k] = xbuf1[k];
+        S->pflags.p[k] = flags[k];
+    }
+    S->pxb[0].n = S->pxb[1].n = S->pflags.n = world;
+    VXQ_CUDA(cudaMalloc(&S->status, sizeof(int)));
+    VXQ_CUDA(cudaMemsetAsync(S->status, 0, sizeof(int), S->s));
+    // state 0 (written to the local rows by create) -> every peer, then publish it
+    const int64_t off = S->L.row0 * S->row_bytes, bytes = S->L.nrows * S->row_bytes;
+    for (int k = 0; k < world; ++k)
+        if (k != rank && bytes > 0)
+            VXQ_CUDA(cudaMemcpyAsync(static_cast<char*>(S->pxb[0].p[k]) + off,
+                                     static_cast<const char*>(S->xb[0]) + off, bytes,
+                                     cudaMemcpyDefault, S->s));
+    S->peers = true;
+    k_signal<<<1, 32, 0, S->s>>>(S->pflags, S->rank, S->epoch + 1);
+    VXQ_CHECK_LAUNCH();
 }
 
 void session_destroy(Session* S) { delete S; }

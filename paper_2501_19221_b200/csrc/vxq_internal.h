@@ -192,6 +192,8 @@ Session* session_create(Problem* p, int solver, const vxq_pa_params* pa,
                         cudaStream_t s);
 void session_step(Session* S, int64_t t);
 void session_finish(Session* S, vxq_outputs* out, const vxq_run_opts* opts);
+void session_set_peers(Session* S, int world, int rank, uint32_t epoch, void* const* xbuf0,
+                       void* const* xbuf1, uint64_t* const* flags);
 void session_destroy(Session* S);
 void session_set_own_stream(Session* S, bool own);
 

@@ -8,6 +8,13 @@ all-gather the exchange buffer (NCCL over NVLink):
     PA : the bit-packed spins, n * R / 8 bytes per step (1 bit per replica-variable)
     SBM: the fp32 positions q,  4 * n * R bytes per step (32x larger: SBM is exchange-bound)
 
+Two exchanges:
+  "nccl"  the caller all-gathers each new state in place (NCCL all_gather_into_tensor);
+  "p2p"   fused: every rank's exchange buffers are shared over CUDA IPC (NVLink peer
+          memory) and the step kernels store their rows straight into every rank's copy,
+          with a per-step release/acquire flag barrier (vxq_session_set_peers) -- no
+          collective between steps, the transfer overlaps the step.
+
 Buffer k & 1 holds state k.  `drive()` is the per-step loop; it takes any session with
 `step(t)` and an in-place gather, so the multi-rank logic is exercised on CPU with gloo
 (tests/test_distributed.py) while the product path runs `vxq_session_*` kernels on the
@@ -120,12 +127,87 @@ def exchange_row_bytes(solver: str, replicas: int, precision: str = "fp32") -> i
     return int(v.value)
 
 
-def solve_rowpart(solver: str, model, params, group=None, precision: str = "fp32",
-                  timing: dict | None = None) -> SampleSet:
-    """Row-partitioned PA/SBM over the ranks of `group` (one GPU per rank, NCCL exchange).
+class _RawBuf:
+    """Device pointer with the tensor-like data_ptr() GpuSession expects."""
 
-    Every rank returns the same best-first SampleSet.  With a single rank this is the
-    ordinary sparse path (bit-identical)."""
+    def __init__(self, ptr: int):
+        self.ptr = int(ptr)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
+class PeerExchange:
+    """IPC-shared exchange buffers + flags of one rank for the fused ("p2p") exchange.
+
+    Allocates this rank's two exchange buffers and its flag array with vxq_exchange_alloc,
+    shares their IPC handles with every rank (all_gather_object) and opens the peers'.
+    ``ptrs[k][g]`` is rank g's buffer k (0, 1 = exchange buffers, 2 = flags)."""
+
+    def __init__(self, buf_bytes: int, world: int, rank: int, device: int, group=None):
+        import torch.distributed as dist
+        L = _lib.load()
+        self.world, self.rank, self.device, self.group = world, rank, device, group
+        self.own, self.opened = [], []
+        self.epoch = 0  # bumped per attached session (flag values carry it)
+        for nbytes in (buf_bytes, buf_bytes, 8 * world):
+            p = ctypes.c_void_p()
+            _lib.check(L.vxq_exchange_alloc(device, int(nbytes), ctypes.byref(p)))
+            self.own.append(int(p.value))
+        handles = []
+        for p in self.own:
+            h = (ctypes.c_ubyte * _lib.IPC_HANDLE_BYTES)()
+            _lib.check(L.vxq_ipc_handle(ctypes.c_void_p(p), h))
+            handles.append(bytes(h))
+        if world > 1:
+            every = [None] * world
+            dist.all_gather_object(every, handles, group=group)
+        else:
+            every = [handles]
+        self.ptrs = [[0] * world for _ in range(3)]
+        for g in range(world):
+            for k in range(3):
+                if g == rank:
+                    self.ptrs[k][g] = self.own[k]
+                    continue
+                p = ctypes.c_void_p()
+                h = (ctypes.c_ubyte * _lib.IPC_HANDLE_BYTES).from_buffer_copy(every[g][k])
+                _lib.check(L.vxq_ipc_open(h, device, ctypes.byref(p)))
+                self.ptrs[k][g] = int(p.value)
+                self.opened.append(int(p.value))
+
+    def bufs(self):
+        return [_RawBuf(self.own[0]), _RawBuf(self.own[1])]
+
+    def attach(self, session: "GpuSession"):
+        """Bind a new session (every rank attaches its sessions in the same order; callers
+        reusing the exchange put a barrier between sessions)."""
+        self.epoch += 1
+        arr = ctypes.c_void_p * self.world
+        _lib.check(_lib.load().vxq_session_set_peers(
+            session.handle, self.world, self.rank, self.epoch, arr(*self.ptrs[0]),
+            arr(*self.ptrs[1]), arr(*self.ptrs[2])))
+
+    def close(self):
+        import torch.distributed as dist
+        L = _lib.load()
+        for p in self.opened:
+            L.vxq_ipc_close(ctypes.c_void_p(p))
+        self.opened = []
+        if self.world > 1:  # no rank frees memory a peer may still have mapped
+            dist.barrier(group=self.group)
+        for p in self.own:
+            L.vxq_exchange_free(ctypes.c_void_p(p))
+        self.own = []
+
+
+def solve_rowpart(solver: str, model, params, group=None, precision: str = "fp32",
+                  timing: dict | None = None, exchange: str = "nccl") -> SampleSet:
+    """Row-partitioned PA/SBM over the ranks of `group` (one GPU per rank).
+
+    exchange="nccl": in-place all-gather after every step; "p2p": the fused peer-memory
+    exchange (PeerExchange).  Every rank returns the same best-first SampleSet.  With a
+    single rank this is the ordinary sparse path (bit-identical)."""
     import torch
     import torch.distributed as dist
 
@@ -139,8 +221,15 @@ def solve_rowpart(solver: str, model, params, group=None, precision: str = "fp32
     spans, B = row_split(n, world)
     rb = exchange_row_bytes(solver, params.replicas, precision)
     rows_alloc = B * world
-    bufs = [torch.zeros(rows_alloc * rb, dtype=torch.uint8, device=f"cuda:{dev}")
-            for _ in range(2)]
+    if exchange not in ("nccl", "p2p"):
+        raise ValidationError("exchange must be 'nccl' or 'p2p'")
+    px = None
+    if exchange == "p2p":
+        px = PeerExchange(rows_alloc * rb, world, rank, dev, group)
+        bufs = px.bufs()
+    else:
+        bufs = [torch.zeros(rows_alloc * rb, dtype=torch.uint8, device=f"cuda:{dev}")
+                for _ in range(2)]
     stream = torch.cuda.current_stream()
     t0 = time.perf_counter()
     sess = GpuSession(model, solver, params, spans[rank][0], spans[rank][1], rows_alloc, bufs,
@@ -148,11 +237,18 @@ def solve_rowpart(solver: str, model, params, group=None, precision: str = "fp32
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    drive(sess, bufs, int(params.steps),
-          lambda b: gather_inplace(b, rank, world, B * rb, group))
+    if px is not None:
+        px.attach(sess)  # pushes state 0 to the peers; steps then exchange by themselves
+        for t in range(int(params.steps)):
+            sess.step(t)
+    else:
+        drive(sess, bufs, int(params.steps),
+              lambda b: gather_inplace(b, rank, world, B * rb, group))
     ev1.record(stream)
     st, en, order, info = sess.finish()
     sess.close()
+    if px is not None:
+        px.close()
     if timing is not None:
         torch.cuda.synchronize()
         timing["loop_ms"] = ev0.elapsed_time(ev1)
@@ -161,4 +257,4 @@ def solve_rowpart(solver: str, model, params, group=None, precision: str = "fp32
     return SampleSet(samples=samples, replica_count=int(params.replicas), seed=params.seed,
                      wall_time=time.perf_counter() - t0,
                      info={**info, "world": world, "rank": rank, "rows": spans[rank],
-                           "path": "rowpart"})
+                           "path": "rowpart", "exchange": exchange})

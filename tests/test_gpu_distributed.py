@@ -76,3 +76,93 @@ def test_device_generator_matches_host_mirror(n, seed):
     b = vxq.run_pa(m, p)
     assert np.array_equal(a.states, b.states) and np.array_equal(a.energies, b.energies)
     assert np.array_equal(a.energies[:4], O.energies_exact(m, a.states[:4]))
+
+
+# ---------------------------------------------------------------- fused peer exchange
+@pytest.mark.parametrize("solver", ["pa", "sbm"])
+def test_solve_rowpart_world1_fused_exchange(solver):
+    """exchange="p2p" (library-allocated IPC buffers, in-kernel stores + flag barrier) at
+    world 1 == the sparse path."""
+    from paper_2501_19221_b200.rowpart import solve_rowpart
+    m = maxcut_model(4000, 3, 6) if solver == "pa" else gen_complete(5, 200, "gaussian")
+    if solver == "pa":
+        p = vxq.PaParams(steps=25, replicas=64, seed=2)
+        ref = vxq.solve_pa(m, p, path="sparse")
+    else:
+        p = vxq.SbmParams(steps=25, dt=0.05, replicas=64, seed=2, c0=0.1)
+        ref = vxq.solve_sbm(m, p, path="sparse")
+    ss = solve_rowpart(solver, m, p, exchange="p2p")
+    assert ss.info["exchange"] == "p2p"
+    assert [s.replica for s in ss.samples] == [s.replica for s in ref.samples]
+    assert [s.energy for s in ss.samples] == [s.energy for s in ref.samples]
+    assert np.array_equal(ss.best.state, ref.best.state)
+
+
+@pytest.mark.parametrize("solver,R", [("pa", 32), ("pa", 96), ("sbm", 64)])
+def test_fused_exchange_stores_to_every_destination(solver, R):
+    """One session with three destinations on this GPU (its own buffers + two stand-in
+    peer copies): every step's rows land identically in all three copies, every copy's
+    flag slot [rank] ends at T + 1, and the solve equals the sparse path.  The stand-in
+    sources' flags are pre-published, so nothing waits on another process."""
+    import ctypes
+
+    import torch
+
+    from paper_2501_19221_b200 import _lib
+    from paper_2501_19221_b200.rowpart import GpuSession, exchange_row_bytes
+    m = maxcut_model(2500, 3, 8) if solver == "pa" else gen_complete(6, 150, "gaussian")
+    T = 12
+    if solver == "pa":
+        params = vxq.PaParams(steps=T, replicas=R, seed=7)
+        ref = vxq.run_pa(m, params, path="sparse")
+    else:
+        params = vxq.SbmParams(steps=T, dt=0.05, replicas=R, seed=7, c0=0.1)
+        ref = vxq.run_sbm(m, params, path="sparse")
+    rb = exchange_row_bytes(solver, R)
+    world, rank = 3, 0
+    mk = lambda: torch.zeros(m.n * rb, dtype=torch.uint8, device="cuda")  # noqa: E731
+    xb = [[mk() for _ in range(world)] for _ in range(2)]
+    flags = [torch.zeros(world, dtype=torch.int64, device="cuda") for _ in range(world)]
+    flags[rank][1:] = 1 << 60  # stand-in sources: already published every state
+    stream = torch.cuda.current_stream().cuda_stream
+    sess = GpuSession(m, solver, params, 0, m.n, m.n, [xb[0][rank], xb[1][rank]],
+                      stream=stream)
+    arr = ctypes.c_void_p * world
+    _lib.check(_lib.load().vxq_session_set_peers(
+        sess.handle, world, rank, 1, arr(*[b.data_ptr() for b in xb[0]]),
+        arr(*[b.data_ptr() for b in xb[1]]), arr(*[f.data_ptr() for f in flags])))
+    for t in range(T):
+        sess.step(t)
+    st, en, order, _ = sess.finish()
+    torch.cuda.synchronize()
+    for k in range(2):
+        for g in range(1, world):
+            assert torch.equal(xb[k][g], xb[k][rank]), (k, g)
+    for g in range(world):
+        assert int(flags[g][rank]) == (1 << 32) + T + 1
+    assert np.array_equal(st, ref.states)
+    assert np.array_equal(en, ref.energies)
+    assert np.array_equal(order, ref.order)
+    sess.close()
+
+
+def test_fused_exchange_rejects_foreign_own_buffers():
+    import ctypes
+
+    import torch
+
+    from paper_2501_19221_b200 import _lib
+    from paper_2501_19221_b200.rowpart import GpuSession, exchange_row_bytes
+    m = maxcut_model(500, 3, 1)
+    params = vxq.PaParams(steps=3, replicas=32, seed=1)
+    rb = exchange_row_bytes("pa", 32)
+    bufs = [torch.zeros(m.n * rb, dtype=torch.uint8, device="cuda") for _ in range(3)]
+    fl = torch.zeros(2, dtype=torch.int64, device="cuda")
+    sess = GpuSession(m, "pa", params, 0, m.n, m.n, bufs[:2],
+                      stream=torch.cuda.current_stream().cuda_stream)
+    arr = ctypes.c_void_p * 2
+    with pytest.raises(vxq.ValidationError):  # xbuf0[rank] must be the session's own
+        _lib.check(_lib.load().vxq_session_set_peers(
+            sess.handle, 2, 0, 1, arr(bufs[2].data_ptr(), bufs[0].data_ptr()),
+            arr(bufs[1].data_ptr(), bufs[1].data_ptr()), arr(fl.data_ptr(), fl.data_ptr())))
+    sess.close()
