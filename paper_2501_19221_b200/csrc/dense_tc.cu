@@ -71,7 +71,9 @@ static_assert(3 * stage_bytes<Kind::kBf16x3>() <= 192 * 1024, "bf16 ring");
 struct DenseOperand {
     int64_t n = 0, ld = 0;      // ld = n_pad (multiple of 128)
     float scale = 0.f;          // c (fp32)
-    uint8_t* K8 = nullptr;      // [ld][ld] fp8 E4M3 in {-1, 0, +1}
+    uint8_t* K8 = nullptr;      // [ld][ld] fp8 E4M3 in {-1, 0, +1}, or (fp4) packed E2M1
+                                //   nibbles [ld][ld/2] (element 2k in the low nibble)
+    uint32_t afmt = 0;          // A format in the f8f6f4 instruction descriptor (0 E4M3, 5 E2M1)
     __nv_bfloat16* K16 = nullptr;  // [ld][ld] bf16 in {-1, 0, +1} (SBM, built lazily)
     CUtensorMap tmA8, tmA16;
     ~DenseOperand() {
@@ -122,10 +124,31 @@ CUtensorMap make_map(const void* base, CUtensorMapDataType dt, int esize, uint64
     return m;
 }
 
+// K as packed E2M1 nibbles [rows][inner/2] bytes; TMA (16U4_ALIGN16B) unpacks each 16
+// nibbles into a 16-byte slot of shared memory -- the padded fp4 operand layout of
+// tcgen05.mma kind::f8f6f4 -- so tiles, descriptors and the MMA loop are those of fp8.
+CUtensorMap make_map_fp4(const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                         uint32_t box_outer) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner / 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 2,
+                              const_cast<void*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(VXQ_ERR_CUDA, "cuTensorMapEncodeTiled (fp4) failed");
+    return m;
+}
+
+constexpr uint32_t FP4_P1 = 0x2, FP4_M1 = 0xA;  // E2M1 +1 / -1
+
 __global__ void k_build_sign_matrix(int64_t n, int64_t ld, const int64_t* __restrict__ indptr,
                                     const int32_t* __restrict__ indices,
                                     const double* __restrict__ data, uint8_t* __restrict__ K8,
-                                    __nv_bfloat16* __restrict__ K16) {
+                                    __nv_bfloat16* __restrict__ K16, uint32_t* __restrict__ K4) {
     int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -133,6 +156,10 @@ __global__ void k_build_sign_matrix(int64_t n, int64_t ld, const int64_t* __rest
         const bool pos = data[k] > 0;
         if (K8) K8[row * ld + indices[k]] = pos ? FP8_P1 : FP8_M1;
         if (K16) K16[row * ld + indices[k]] = __float2bfloat16_rn(pos ? 1.f : -1.f);
+        if (K4) {  // neighbours share bytes: OR the nibble into its 32-bit word
+            const int64_t e = row * ld + indices[k];
+            atomicOr(K4 + (e >> 3), (pos ? FP4_P1 : FP4_M1) << (4 * (e & 7)));
+        }
     }
 }
 
@@ -247,6 +274,8 @@ struct DenseRunArgs {
     unsigned* done;          // [T][n_tiles] finished row-tiles per (step, replica block)
     int group;               // replica blocks interleaved per row block (A-panel reuse)
     unsigned long long* stats;  // optional [8] wait-cycle counters (VXQ_DENSE_STATS=1)
+    uint32_t idesc_extra;    // OR-ed into the instruction descriptor (A operand format)
+    uint32_t a_tx_bytes;     // transaction bytes of one A box (packed fp4 counts global bytes)
 };
 
 // stats slots: 0 producer<-empty, 1 producer<-dependency, 2 mma<-full, 3 mma<-tempty,
@@ -352,7 +381,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     ptx::mbar_wait(empty + stage, ph ^ 1);
                     if (a.stats) st_empty += clk() - c0;
                     uint8_t* sa = smem + stage * SBYTES;
-                    ptx::mbar_arrive_expect_tx(full + stage, DA_BYTES + TR::kPlanes * b_plane_bytes);
+                    ptx::mbar_arrive_expect_tx(full + stage,
+                                               a.a_tx_bytes + TR::kPlanes * b_plane_bytes);
                     const int kcol = kb * (DROW / TR::kElemBytes);
                     ptx::tma_load_2d_hint(sa, &tmA, full + stage, kcol, mb * DBM, keep);
                     if (kb == 0 && t > 0) {
@@ -399,7 +429,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer (single thread issues for the CTA)
         const uint32_t idesc =
-            TR::kIdescBase | ((uint32_t)(a.bn >> 3) << 17) | ((uint32_t)(DBM >> 4) << 24);
+            TR::kIdescBase | a.idesc_extra | ((uint32_t)(a.bn >> 3) << 17) |
+            ((uint32_t)(DBM >> 4) << 24);
         int stage = 0;
         uint32_t ph = 0;
         int lt = 0;
@@ -712,11 +743,25 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, bool need_bf16) {
         const int64_t ld = d->ld;
         uint8_t* k8 = nullptr;
         __nv_bfloat16* k16 = nullptr;
+        uint32_t* k4 = nullptr;
         if (!d->K8) {
-            VXQ_CUDA(cudaMalloc(&d->K8, ld * ld));
-            VXQ_CUDA(cudaMemsetAsync(d->K8, 0, ld * ld, s));
-            k8 = d->K8;
-            d->tmA8 = make_map(d->K8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, ld, 1, DROW, DBM, 1);
+            // default: K as packed E2M1 (51 MB at n = 10^4: stays L2-resident, -60 % DRAM
+            // traffic, higher clocks under the power cap); VXQ_DENSE_FP4=0 -> FP8 E4M3
+            const char* e4 = getenv("VXQ_DENSE_FP4");
+            const bool fp4 = !(e4 && atoi(e4) == 0);
+            const int64_t bytes = fp4 ? ld * ld / 2 : ld * ld;
+            VXQ_CUDA(cudaMalloc(&d->K8, bytes));
+            VXQ_CUDA(cudaMemsetAsync(d->K8, 0, bytes, s));
+            if (fp4) {
+                k4 = reinterpret_cast<uint32_t*>(d->K8);
+                d->afmt = 5;
+                d->tmA8 = make_map_fp4(d->K8, ld, ld, DROW, DBM);
+            } else {
+                k8 = d->K8;
+                d->afmt = 0;
+                d->tmA8 = make_map(d->K8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, ld, 1, DROW, DBM,
+                                   1);
+            }
         }
         if (need_bf16 && !d->K16) {
             VXQ_CUDA(cudaMalloc(&d->K16, ld * ld * 2));
@@ -725,9 +770,9 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, bool need_bf16) {
             d->tmA16 = make_map(d->K16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, ld, 1, DROW / 2,
                                 DBM, 1);
         }
-        if (k8 || k16) {
+        if (k8 || k16 || k4) {
             k_build_sign_matrix<<<(unsigned)ceil_div(p->n * 32, TB), TB, 0, s>>>(
-                p->n, ld, p->indptr, p->indices, p->data64, k8, k16);
+                p->n, ld, p->indptr, p->indices, p->data64, k8, k16, k4);
             VXQ_CHECK_LAUNCH();
             VXQ_CUDA(cudaStreamSynchronize(s));
         }
@@ -737,6 +782,12 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, bool need_bf16) {
     }
     p->dense = d;
     return d;
+}
+
+static uint32_t a_tx_bytes(const DenseOperand* d) {
+    if (d->afmt == 0) return DA_BYTES;
+    const char* e = getenv("VXQ_DENSE_FP4_TXFULL");
+    return (e && atoi(e)) ? DA_BYTES : DA_BYTES / 2;
 }
 
 // fp8 energy pass over the signs of `x` ([R][ld]) -> q2 = 2 sum_{i<j} K_ij s_i s_j
@@ -750,6 +801,8 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
     const int bn = choose_bn(n, R, 1, KindTraits<Kind::kFp8>::kBnMax);
     CUtensorMap tb = make_map(sg.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW, bn, 1);
     DenseRunArgs e{};
+    e.idesc_extra = d->afmt << 7;  // A = K (fp8 or packed fp4)
+    e.a_tx_bytes = a_tx_bytes(d);
     e.n = (int)n;
     e.R = (int)R;
     e.ld = (int)ld;
@@ -837,6 +890,8 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
     VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
     DenseRunArgs a{};
+    a.idesc_extra = d->afmt << 7;
+    a.a_tx_bytes = a_tx_bytes(d);
     a.n = (int)n;
     a.R = (int)R;
     a.ld = (int)ld;
@@ -917,6 +972,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
     VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
     DenseRunArgs a{};
+    a.a_tx_bytes = DA_BYTES;  // bf16 K planes: full boxes
     a.n = (int)n;
     a.R = (int)R;
     a.ld = (int)ld;
