@@ -182,12 +182,13 @@ __device__ __forceinline__ void split3(float v, __nv_bfloat16& q1, __nv_bfloat16
 // x0 ~ uniform(-1, 1) from replica stream r (same draws as k_init_pa), row-major [R][ld]
 __global__ void k_init_pa_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, int64_t rbegin,
                              float* __restrict__ x, float* __restrict__ m,
-                             uint8_t* __restrict__ s) {
+                             uint8_t* __restrict__ s, bool s_fp4) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nq = (n + 3) / 4;
     if (idx >= nq * R) return;
     int64_t r = idx / nq, q = idx % nq;
     U64x4 o = philox4x64_10((uint64_t)q + 1, 0, (uint64_t)(rbegin + r), 0, seed, 0);
+    uint32_t code[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
         int64_t i = 4 * q + w;
@@ -195,8 +196,14 @@ __global__ void k_init_pa_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, in
             float v = (float)uniform_from_raw(o.v[w], -1.0, 2.0);
             x[r * ld + i] = v;
             m[r * ld + i] = 0.f;
-            s[r * ld + i] = v >= 0.f ? FP8_P1 : FP8_M1;
+            if (s_fp4) code[w] = v >= 0.f ? FP4_P1 : FP4_M1;
+            else s[r * ld + i] = v >= 0.f ? FP8_P1 : FP8_M1;
         }
+    }
+    if (s_fp4) {  // 4 spins = 2 packed bytes (element 2k in the low nibble)
+        const int64_t e = (r * ld + 4 * q) >> 1;
+        s[e] = (uint8_t)(code[0] | (code[1] << 4));
+        s[e + 1] = (uint8_t)(code[2] | (code[3] << 4));
     }
 }
 
@@ -276,6 +283,7 @@ struct DenseRunArgs {
     unsigned long long* stats;  // optional [8] wait-cycle counters (VXQ_DENSE_STATS=1)
     uint32_t idesc_extra;    // OR-ed into the instruction descriptor (A operand format)
     uint32_t a_tx_bytes;     // transaction bytes of one A box (packed fp4 counts global bytes)
+    int b_fp4;               // B operand (spins) as packed E2M1 nibbles
 };
 
 // stats slots: 0 producer<-empty, 1 producer<-dependency, 2 mma<-full, 3 mma<-tempty,
@@ -381,8 +389,9 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     ptx::mbar_wait(empty + stage, ph ^ 1);
                     if (a.stats) st_empty += clk() - c0;
                     uint8_t* sa = smem + stage * SBYTES;
-                    ptx::mbar_arrive_expect_tx(full + stage,
-                                               a.a_tx_bytes + TR::kPlanes * b_plane_bytes);
+                    ptx::mbar_arrive_expect_tx(
+                        full + stage,
+                        a.a_tx_bytes + TR::kPlanes * (b_plane_bytes >> (a.b_fp4 ? 1 : 0)));
                     const int kcol = kb * (DROW / TR::kElemBytes);
                     ptx::tma_load_2d_hint(sa, &tmA, full + stage, kcol, mb * DBM, keep);
                     if (kb == 0 && t > 0) {
@@ -552,7 +561,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             if (ok) {
                                 ptx::st_stream(xg + off, xn, stream);
                                 ptx::st_stream(mg + off, mn, stream);
-                                nxt[off] = xn >= 0.f ? FP8_P1 : FP8_M1;
+                                if (!a.b_fp4) nxt[off] = xn >= 0.f ? FP8_P1 : FP8_M1;
+                            }
+                            if (a.b_fp4) {  // lanes 2k, 2k+1 = rows i, i+1: one packed byte
+                                const uint32_t code = ok ? (xn >= 0.f ? FP4_P1 : FP4_M1) : 0u;
+                                const uint32_t hi4 = __shfl_xor_sync(0xffffffffu, code, 1);
+                                if (!(lane & 1) && (code | hi4))
+                                    nxt[off >> 1] = (uint8_t)(code | (hi4 << 4));
                             }
                         } else {
                             // SBM with B = -A = -c K, g = -h (field = -f)
@@ -869,11 +884,15 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DenseOperand* d = dense_operand(p, s, false);
     const int64_t n = p->n, ld = d->ld, T = (int64_t)sched.size();
     DevBuf<float> x(R * ld, s), m(R * ld, s);
-    DevBuf<uint8_t> s0(R * ld, s), s1(R * ld, s);
-    VXQ_CUDA(cudaMemsetAsync(s0.get(), 0, R * ld, s));
-    VXQ_CUDA(cudaMemsetAsync(s1.get(), 0, R * ld, s));
+    // spins (the B operand): packed E2M1 nibbles with a packed-fp4 K (VXQ_DENSE_FP4S=0: fp8)
+    const char* es4 = getenv("VXQ_DENSE_FP4S");
+    const bool s_fp4 = d->afmt == 5 && !(es4 && atoi(es4) == 0);
+    const int64_t sbytes = s_fp4 ? R * ld / 2 : R * ld;
+    DevBuf<uint8_t> s0(sbytes, s), s1(sbytes, s);
+    VXQ_CUDA(cudaMemsetAsync(s0.get(), 0, sbytes, s));
+    VXQ_CUDA(cudaMemsetAsync(s1.get(), 0, sbytes, s));
     k_init_pa_rm<<<nblk(((n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, x.get(), m.get(),
-                                                       s0.get());
+                                                       s0.get(), s_fp4);
     VXQ_CHECK_LAUNCH();
     const int bn = choose_bn(n, R, 1, KindTraits<Kind::kFp8>::kBnMax);
     // VXQ_DENSE_CLUSTER=2: B multicast across 2-CTA clusters (fewer cycles, same wall time
@@ -881,17 +900,20 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     int cl = 1;
     if (const char* e = getenv("VXQ_DENSE_CLUSTER")) cl = atoi(e) == 2 ? 2 : 1;
     if (ceil_div(n, DBM) < 2) cl = 1;
-    CUtensorMap tmB0 = make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW,
-                                bn / cl, 1);
-    CUtensorMap tmB1 = make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW,
-                                bn / cl, 1);
+    CUtensorMap tmB0 = s_fp4 ? make_map_fp4(s0.get(), ld, R, DROW, bn / cl)
+                             : make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1,
+                                        DROW, bn / cl, 1);
+    CUtensorMap tmB1 = s_fp4 ? make_map_fp4(s1.get(), ld, R, DROW, bn / cl)
+                             : make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1,
+                                        DROW, bn / cl, 1);
     std::vector<float> s32(T);
     for (int64_t t = 0; t < T; ++t) s32[t] = (float)sched[t];
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
     VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
     DenseRunArgs a{};
-    a.idesc_extra = d->afmt << 7;
+    a.idesc_extra = (d->afmt << 7) | ((s_fp4 ? 5u : 0u) << 10);
     a.a_tx_bytes = a_tx_bytes(d);
+    a.b_fp4 = s_fp4 ? 1 : 0;
     a.n = (int)n;
     a.R = (int)R;
     a.ld = (int)ld;
