@@ -514,29 +514,52 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             const int i = mb * DBM + row;
             const bool row_ok = i < a.n;
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+            // x/m of this warp's chunks do not depend on the accumulator: the first chunk's
+            // loads are issued before waiting for the MMA, and each later chunk's while the
+            // previous one is computed (two register buffers, chunks c, c+2, c+4, ...)
+            const uint64_t stream = ptx::policy_evict_first();
+            float xA[16], mA[16], xB[16], mB[16];
+            auto load_chunk = [&](int c, float* xo, float* mo) {
+                const int r0 = nb * a.bn + c * 16;
+                const int64_t base = (int64_t)r0 * a.ld + i;
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    const bool ok = row_ok && (r0 + jj) < a.R;
+                    xo[jj] = ok ? ptx::ld_stream(xg + base + (int64_t)jj * a.ld, stream) : 0.f;
+                    mo[jj] = ok ? ptx::ld_stream(mg + base + (int64_t)jj * a.ld, stream) : 0.f;
+                }
+            };
+            if (a.mode == 0 && half < nch) {
+                // x/m of step t are written by the step-(t-1) tiles of this replica block
+                // (possibly on other CTAs): acquire their counter before the early load
+                if (t > 0) {
+                    const unsigned* cnt = a.done + (size_t)(t - 1) * a.n_tiles + nb;
+                    if (ld_acquire_gpu(cnt) < (unsigned)a.m_tiles) {
+                        uint64_t t0, tn;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                        while (ld_acquire_gpu(cnt) < (unsigned)a.m_tiles) {
+                            __nanosleep(64);
+                            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                            if (tn - t0 > 10ull * 1000 * 1000 * 1000) __trap();
+                        }
+                    }
+                }
+                load_chunk(half, xA, mA);
+            }
             long long c0 = (a.stats && ep_tid == 0) ? clk() : 0;
             ptx::mbar_wait(tfull + acc, acc_ph);
             long long c1 = (a.stats && ep_tid == 0) ? clk() : 0;
             if (a.stats && ep_tid == 0) ep_wait += c1 - c0;
             ptx::tc_fence_after();
             if (a.mode == 0) {
-                const uint64_t stream = ptx::policy_evict_first();
                 uint8_t* nxt = (t & 1) ? a.b_buf[0] : a.b_buf[1];  // B operand of step t+1
                 const float st = __ldg(a.sched + t);
                 const float hi = row_ok ? __ldg(a.h + i) : 0.f;
-#pragma unroll 1
-                for (int c = half; c < nch; c += 2) {
+                auto process = [&](int c, const float* xo, const float* mo) {
                     uint32_t v[16];
                     ptx::tmem_ld_32x32b_x16(tbase + c * 16, v);
                     const int r0 = nb * a.bn + c * 16;
                     const int64_t base = (int64_t)r0 * a.ld + i;
-                    float xo[16], mo[16];
-#pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {
-                        const bool ok = row_ok && (r0 + jj) < a.R;
-                        xo[jj] = ok ? ptx::ld_stream(xg + base + (int64_t)jj * a.ld, stream) : 0.f;
-                        mo[jj] = ok ? ptx::ld_stream(mg + base + (int64_t)jj * a.ld, stream) : 0.f;
-                    }
                     ptx::tmem_ld_wait();
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
@@ -593,6 +616,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             }
                         }
                     }
+                };
+#pragma unroll 1
+                for (int c = half; c < nch; c += 4) {  // xA/mA hold chunk c
+                    if (c + 2 < nch) load_chunk(c + 2, xB, mB);
+                    process(c, xA, mA);
+                    if (c + 4 < nch) load_chunk(c + 4, xA, mA);
+                    if (c + 2 < nch) process(c + 2, xB, mB);
                 }
             } else if (a.mode == 1) {
                 // energy pass (fp8 signs): 2 q_r = sum_i s_i (K s)_i, exact integers
