@@ -485,9 +485,15 @@ def run_ours(args):
             fn = _rp if args.solver == "pa" else _rs
             tr = fn(model, params, path=args.path, device=local, trace=True,
                     replica_begin=rbegin).info["energy_trace"]
+            if world > 1:  # best replica of the whole job = min over the replica shards
+                tt = torch.tensor(np.nan_to_num(tr, nan=np.inf), dtype=torch.float64,
+                                  device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MIN)
+                tr = tt.cpu().numpy()
             step_ms = tot_ms / args.steps / T
             hit = np.nonzero(tr <= target)[0]
-            ttt = {"target": target, "rule": "SK energy density E/N <= -0.70",
+            ttt = {"target": target, "rule": "SK energy density E/N <= -0.70 (best replica "
+                                              "of the whole job)",
                    "step": int(hit[0]) if hit.size else None,
                    "ms": float(step_ms * (hit[0] + 1)) if hit.size else None,
                    "best_trace_energy": float(np.nanmin(tr))}
