@@ -85,6 +85,26 @@ struct DenseOperand {
 void dense_destroy(DenseOperand* d) { delete d; }
 
 namespace {
+__global__ void k_any_nonzero_h(int64_t n, const double* v, int* flag);
+}
+
+bool problem_h_zero(Problem* p, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(p->mu);
+    if (p->h_zero < 0) {
+        DevBuf<int> f(1, s);
+        VXQ_CUDA(cudaMemsetAsync(f.get(), 0, sizeof(int), s));
+        k_any_nonzero_h<<<(unsigned)std::max<int64_t>(1, ceil_div(p->n, 256)), 256, 0, s>>>(
+            p->n, p->h64, f.get());
+        VXQ_CHECK_LAUNCH();
+        int v = 0;
+        VXQ_CUDA(cudaMemcpyAsync(&v, f.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        VXQ_CUDA(cudaStreamSynchronize(s));
+        p->h_zero = v ? 0 : 1;
+    }
+    return p->h_zero == 1;
+}
+
+namespace {
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -255,6 +275,47 @@ __global__ void k_pack_bits_rm(const float* __restrict__ x, int64_t n, int64_t R
     if (lane == 0) sb[i * W + w] = word;
 }
 
+__global__ void k_any_nonzero_h(int64_t n, const double* v, int* flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && v[i] != 0.0) *flag = 1;
+}
+
+// fused tracking, after the loop: decide s_{T-1} (still in its B buffer, energy q_{T-1}) and
+// s_T = sign(x_T) (energy from the final energy pass), strictly-better-wins in step order
+__global__ void k_track_finalize(int64_t n, int64_t R, int64_t ld, const long long* qlast,
+                                 const long long* qT, const long long* bestq,
+                                 const uint8_t* sprev, int fp4, const float* x,
+                                 int8_t* best_s) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n * R) return;
+    const int64_t r = idx / n, i = idx % n, off = r * ld + i;
+    long long b = bestq[r];
+    int8_t v = best_s[off];
+    if (qlast[r] < b) {
+        b = qlast[r];
+        if (fp4) {
+            const uint8_t by = sprev[off >> 1];
+            v = (((i & 1) ? (by >> 4) : by) & 0x8) ? -1 : 1;
+        } else {
+            v = (sprev[off] & 0x80) ? -1 : 1;
+        }
+    }
+    if (qT[r] < b) v = x[off] >= 0.f ? 1 : -1;
+    best_s[off] = v;
+}
+
+__global__ void k_pack_bits_i8(const int8_t* __restrict__ s, int64_t n, int64_t R, int64_t ld,
+                               int64_t W, uint32_t* __restrict__ sb) {
+    int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (gw >= n * W) return;
+    int64_t w = gw / n, i = gw % n;
+    int64_t r = w * 32 + lane;
+    bool up = r < R ? (s[r * ld + i] > 0) : true;
+    uint32_t word = __ballot_sync(0xffffffffu, up);
+    if (lane == 0) sb[i * W + w] = word;
+}
+
 __global__ void k_signs_fp8_rm(const float* __restrict__ x, int64_t n, int64_t R, int64_t ld,
                                uint8_t* __restrict__ s) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -284,6 +345,10 @@ struct DenseRunArgs {
     uint32_t idesc_extra;    // OR-ed into the instruction descriptor (A operand format)
     uint32_t a_tx_bytes;     // transaction bytes of one A box (packed fp4 counts global bytes)
     int b_fp4;               // B operand (spins) as packed E2M1 nibbles
+    // fused best-state tracking (improvement mode; needs qtrace, h = 0):
+    long long* bestq;        // [R] lowest 2 sum K s s of s_0..s_{t-2} (LLONG_MAX initially)
+    int8_t* best_s;          // [R][ld] best spins so far
+    unsigned* decided;       // [T][n_tiles] tiles that made their step-(t-1) decisions
 };
 
 // stats slots: 0 producer<-empty, 1 producer<-dependency, 2 mma<-full, 3 mma<-tempty,
@@ -326,6 +391,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     constexpr int STAGES = TR::kStages;
     constexpr int SBYTES = stage_bytes<KD>();
     extern __shared__ uint8_t smem_raw[];
+    __shared__ int s_last;  // fused tracking: this tile completed its step's decisions
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + 192 * 1024);
@@ -553,6 +619,31 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             ptx::tc_fence_after();
             if (a.mode == 0) {
                 uint8_t* nxt = (t & 1) ? a.b_buf[0] : a.b_buf[1];  // B operand of step t+1
+                if (a.bestq && t > 0) {
+                    // fused best tracking: q_{t-1} is final (every step-(t-1) tile published),
+                    // and this tile's rows of s_{t-1} are still in nxt until process() below
+                    // overwrites them with s_{t+1}: copy them for replicas that improved
+                    const long long* qp = a.qtrace + (int64_t)(t - 1) * a.R;
+                    for (int c = half; c < nch; c += 2) {
+#pragma unroll 4
+                        for (int jj = 0; jj < 16; ++jj) {
+                            const int r = nb * a.bn + c * 16 + jj;
+                            if (r >= a.R || !row_ok) continue;
+                            if (qp[r] < a.bestq[r]) {
+                                const int64_t off = (int64_t)r * a.ld + i;
+                                int8_t sv;
+                                if (a.b_fp4) {
+                                    const uint8_t by = nxt[off >> 1];
+                                    sv = (((i & 1) ? (by >> 4) : by) & 0x8) ? -1 : 1;
+                                } else {
+                                    sv = (nxt[off] & 0x80) ? -1 : 1;
+                                }
+                                a.best_s[off] = sv;
+                            }
+                        }
+                    }
+                    __syncwarp();  // lane pairs share packed bytes: read before any write
+                }
                 const float st = __ldg(a.sched + t);
                 const float hi = row_ok ? __ldg(a.h + i) : 0.f;
                 auto process = [&](int c, const float* xo, const float* mo) {
@@ -649,6 +740,22 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             if (a.stats && ep_tid == 0) ep_busy += clk() - c1;
             ptx::tc_fence_before();
             ptx::mbar_arrive(tempty + acc);
+            if (a.mode == 0 && a.bestq && t > 0 && tile_ok) {
+                // the tile that completes the step-t decisions of this replica block folds
+                // q_{t-1} into bestq -- before its own publish below, so step-(t+1) tiles
+                // (which acquire the done counter) see it
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (ep_tid == 0)
+                    s_last = atomicAdd(a.decided + (size_t)t * a.n_tiles + nb, 1u) ==
+                             (unsigned)a.m_tiles - 1;
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (s_last) {
+                    __threadfence();
+                    const long long* qp = a.qtrace + (int64_t)(t - 1) * a.R;
+                    for (int r = nb * a.bn + ep_tid; r < min(a.R, (nb + 1) * a.bn); r += 256)
+                        if (qp[r] < a.bestq[r]) a.bestq[r] = qp[r];
+                }
+            }
             if (a.mode != 1 && tile_ok && t + 1 < a.T) {
                 // publish: all 256 epilogue threads' stores, then one release increment
                 asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -910,7 +1017,7 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                    const std::vector<double>& sched, float eta, float alpha, uint64_t seed,
                    int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, long long* q2,
                    cudaStream_t s, double* loop_ms, int64_t* launches, double* trace_out,
-                   bool trace_on_dev) {
+                   bool trace_on_dev, uint32_t* sb_best) {
     DenseOperand* d = dense_operand(p, s, false);
     const int64_t n = p->n, ld = d->ld, T = (int64_t)sched.size();
     DevBuf<float> x(R * ld, s), m(R * ld, s);
@@ -967,11 +1074,26 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
-    DevBuf<long long> qtr;
-    if (trace_out) {
+    DevBuf<long long> qtr, bestq;
+    DevBuf<int8_t> best_s;
+    DevBuf<unsigned> decided;
+    if (trace_out || sb_best) {
         qtr = DevBuf<long long>(std::max<int64_t>(T, 1) * R, s);
         VXQ_CUDA(cudaMemsetAsync(qtr.get(), 0, std::max<int64_t>(T, 1) * R * sizeof(long long), s));
         a.qtrace = qtr.get();
+    }
+    if (sb_best) {  // fused best-state tracking (h = 0: q is the whole energy up to c, offset)
+        VXQ_REQUIRE(q2, "tracking needs the final energy pass");
+        bestq = DevBuf<long long>(R, s);
+        VXQ_CUDA(cudaMemsetAsync(bestq.get(), 0x7f, R * sizeof(long long), s));  // ~ +inf
+        best_s = DevBuf<int8_t>(R * ld, s);
+        VXQ_CUDA(cudaMemsetAsync(best_s.get(), 0, R * ld, s));
+        decided = DevBuf<unsigned>(std::max<int64_t>(T, 1) * a.n_tiles, s);
+        VXQ_CUDA(cudaMemsetAsync(decided.get(), 0,
+                                 std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
+        a.bestq = bestq.get();
+        a.best_s = best_s.get();
+        a.decided = decided.get();
     }
     *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, cl, s);
     *launches += 2;
@@ -990,6 +1112,16 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
         *launches += 2;
     }
     if (q2) energy_pass(d, x.get(), n, R, q2, s, launches);
+    if (sb_best && T > 0) {
+        const uint8_t* sprev = ((T - 1) & 1) ? s1.get() : s0.get();
+        k_track_finalize<<<nblk(n * R), TB, 0, s>>>(n, R, ld, qtr.get() + (T - 1) * R, q2,
+                                                     bestq.get(), sprev, s_fp4 ? 1 : 0, x.get(),
+                                                     best_s.get());
+        k_pack_bits_i8<<<(unsigned)ceil_div(n * W * 32, TB), TB, 0, s>>>(best_s.get(), n, R, ld,
+                                                                       W, sb_best);
+        VXQ_CHECK_LAUNCH();
+        *launches += 2;
+    }
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(x.get(), n, R, ld, R_pad, V, x_il);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(m.get(), n, R, ld, R_pad, V, m_il);
     k_pack_bits_rm<<<(unsigned)ceil_div(n * W * 32, TB), TB, 0, s>>>(x.get(), n, R, ld, W, sb);

@@ -911,10 +911,14 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     }
     const bool want_best = opts && opts->track_best;
     const bool want_trace = out->energy_trace != nullptr;
-    if (want_best && req == VXQ_PATH_DENSE)
-        throw Error(VXQ_ERR_UNSUPPORTED, "track_best is not available on the dense path yet");
-    const bool dense = sizeof(T) == 4 && !want_best &&
-                       (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+    // fused best tracking on the dense path uses the in-kernel exact coupling energies,
+    // which are the whole energy only when h == 0 (else: the sparse path's exact tracker)
+    const bool dense_cand =
+        sizeof(T) == 4 && (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+    const bool h0 = want_best && dense_cand ? problem_h_zero(p, s) : true;
+    if (want_best && req == VXQ_PATH_DENSE && !h0)
+        throw Error(VXQ_ERR_UNSUPPORTED, "track_best on the dense path needs h = 0");
+    const bool dense = dense_cand && (!want_best || h0);
     if (!dense) path = choose_path(req, L, smem, p->nnz);
     // the resident kernel keeps spins in shared memory: tracking needs per-step spins
     if (!dense && path == VXQ_PATH_RESIDENT && (want_best || want_trace)) {
@@ -927,14 +931,16 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     EventTimer tm(s);
     const uint32_t* sb_final = nullptr;
     DevBuf<long long> q2;
+    DevBuf<uint32_t> sb_best;
     if (dense) {
         q2 = DevBuf<long long>(R, s);
+        if (want_best) sb_best = DevBuf<uint32_t>(n * L.W, s);
         if constexpr (sizeof(T) == 4) {
             dense_pa_loop(p, R, L.R_pad, L.V, L.W, sched, eta, alpha, prm->seed, rbegin,
                           x.get(), m.get(), sbA.get(), q2.get(), s, &out->loop_ms, &launches,
-                          out->energy_trace, opts && opts->outputs_on_device);
+                          out->energy_trace, opts && opts->outputs_on_device, sb_best.get());
         }
-        sb_final = sbA.get();
+        sb_final = want_best ? sb_best.get() : sbA.get();
     } else if (path == VXQ_PATH_RESIDENT) {
         DevBuf<T> ds(std::max<int64_t>(T_, 1), s);
         std::vector<T> st(T_);
@@ -974,7 +980,9 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         if (trk.best) sb_final = trk.best_sb.get();
     }
     out->path_used = dense ? VXQ_PATH_DENSE : path;
-    finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s, q2.get());
+    // q2 (coupling energy counts of the final spins) only describes sb_final without tracking
+    finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s,
+                      dense && !want_best ? q2.get() : nullptr);
     out->launches = launches + 4;
 }
 

@@ -53,6 +53,7 @@ struct Problem {
     std::mutex mu;  // guards the lazy caches below
     double lambda0 = NAN;
     double c0 = NAN;
+    int h_zero = -1;  // cached problem_h_zero (-1 = unknown)
     DenseOperand* dense = nullptr;
 
     ~Problem();
@@ -203,7 +204,10 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                    const std::vector<double>& sched, float eta, float alpha, uint64_t seed,
                    int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, long long* q2,
                    cudaStream_t s, double* loop_ms, int64_t* launches,
-                   double* trace_out = nullptr, bool trace_on_dev = false);
+                   double* trace_out = nullptr, bool trace_on_dev = false,
+                   uint32_t* sb_best = nullptr);
+// h == 0 everywhere (cached per problem): the dense path's in-kernel energies are exact
+bool problem_h_zero(Problem* p, cudaStream_t s);
 
 void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                     const std::vector<double>& a_sched, double dt, double a0, double c0,

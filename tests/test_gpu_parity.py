@@ -402,3 +402,41 @@ def test_energy_trace_dense_pa_exact():
         M = alpha * M - eta * grad
         X = np.clip(X + M, np.float32(-1), np.float32(1))
     assert np.array_equal(r.info["energy_trace"], np.array(want))
+
+
+@pytest.mark.parametrize("n,R,T", [(700, 300, 40), (1000, 256, 25)])
+def test_dense_fused_best_tracking_matches_emulation(n, R, T):
+    """track_best on the tcgen05 path (fused in the epilogue: exact integer energies of every
+    s_t, t = 0..T, earliest minimum wins) == the fp32 emulation's best states."""
+    m = sk_model(n, 11)
+    r = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=8), track_best=True)
+    assert r.info["path"] == "dense"
+    K = np.zeros((n, n), dtype=np.int64)
+    K[m.rows, m.cols] = np.sign(m.values).astype(np.int64)
+    K[m.cols, m.rows] = np.sign(m.values).astype(np.int64)
+    c = np.float32(np.abs(m.values[0]))
+    X = O.pa_init(8, R, n).astype(np.float32)
+    M = np.zeros_like(X)
+    h = m.h.astype(np.float32)
+    eta, alpha = np.float32(0.05), np.float32(0.9)
+    best_q = np.full(R, np.iinfo(np.int64).max)
+    best_S = np.zeros((R, n), dtype=np.int8)
+
+    def observe(S):
+        q = np.einsum("ri,ri->r", S, S @ K.T)
+        imp = q < best_q
+        best_q[imp] = q[imp]
+        best_S[imp] = S[imp]
+
+    for lam in O.pa_schedule(O.resolve_lambda0(m), T).astype(np.float32):
+        S = np.where(X >= 0, 1, -1).astype(np.int64)
+        observe(S)
+        f = c * (S @ K.T).astype(np.float32)
+        M = alpha * M - eta * ((lam * X + f) + h)
+        X = np.clip(X + M, np.float32(-1), np.float32(1))
+    observe(np.where(X >= 0, 1, -1).astype(np.int64))
+    assert np.array_equal(r.states, best_S)
+    assert np.array_equal(r.energies, O.energies_exact(m, r.states))
+    # improvement mode never reports worse than the final states
+    plain = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=8))
+    assert np.all(r.energies <= plain.energies)
