@@ -42,7 +42,7 @@ __global__ void k_sa_init_spins(int64_t n, int64_t W, int64_t R_pad, uint64_t se
     const int64_t i = t / R_pad, r = t % R_pad;
     const uint64_t q = (uint64_t)i >> 1;  // raw draw holding 32-bit half i
     const U64x4 b = philox4x64_10((q >> 2) + 1, 0, (uint64_t)(rbegin + r), 0, seed, 0);
-    const uint64_t raw = b.v[q & 3];
+    const uint64_t raw = pick_word(b, (uint32_t)(q & 3));
     const bool up = (i & 1) ? (raw >> 63) != 0 : ((raw >> 31) & 1u) != 0;
     const uint32_t word = __ballot_sync(0xffffffffu, up);
     if ((r & 31) == 0) sb[i * W + (r >> 5)] = word;
@@ -153,9 +153,7 @@ __global__ void __launch_bounds__(32) k_sa_run(SaArgs a) {
                 blk = philox4x64_10(q + 1, 0, rg, 0, a.seed, 0);
                 kb = q;
             }
-            const uint32_t lo2 = (uint32_t)(k & 3);  // register select (no local array)
-            const uint64_t raw = lo2 == 0 ? blk.v[0] : lo2 == 1 ? blk.v[1]
-                                 : lo2 == 2 ? blk.v[2] : blk.v[3];
+            const uint64_t raw = pick_word(blk, (uint32_t)(k & 3));
             ++k;
             const bool up = (word >> lane) & 1u;
             const double dE = up ? -2.0 * (double)f : 2.0 * (double)f;  // -2 s F (exact)

@@ -164,6 +164,9 @@ inline Dests<P> one_dest(P* ptr) {
 #ifndef VXQ_PA_MINB
 #define VXQ_PA_MINB 4
 #endif
+#ifndef VXQ_PA_LATE_XM
+#define VXQ_PA_LATE_XM 1
+#endif
 template <typename T, int V, int CPW>
 __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int64_t nrows, int64_t R_pad,
                                                  Operator<T> op, const T* __restrict__ h,
@@ -182,12 +185,23 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
     const int64_t i = row0 + il;
     const int64_t W = R_pad / 32;
     Vec<T, V> xv[CPW], mv[CPW];
+#if VXQ_PA_LATE_XM
+    // x/m are not needed until the field is summed: prefetch them into L2 now and load them
+    // after the gathers (keeps 16 registers free for the gather batch)
+#pragma unroll
+    for (int g = 0; g < CPW; ++g) {
+        const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + base));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(m + base));
+    }
+#else
 #pragma unroll
     for (int g = 0; g < CPW; ++g) {
         const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
         xv[g] = ld_cs<T, V>(x + base);
         mv[g] = ld_cs<T, V>(m + base);
     }
+#endif
     T f[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) f[b] = (T)0;
@@ -232,6 +246,14 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
     }
 
     const T hi = __ldg(h + i);
+#if VXQ_PA_LATE_XM
+#pragma unroll
+    for (int g = 0; g < CPW; ++g) {
+        const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
+        xv[g] = ld_cs<T, V>(x + base);
+        mv[g] = ld_cs<T, V>(m + base);
+    }
+#endif
 #pragma unroll
     for (int g = 0; g < CPW; ++g) {
 #pragma unroll
@@ -244,8 +266,11 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
             xv[g].v[b] = xn;
             mv[g].v[b] = mn;
             uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
-            if (lane == g * V + b)
-                for (int d = 0; d < sb_out.n; ++d) sb_out.p[d][i * W + c0 * V + g * V + b] = word;
+            if (lane == g * V + b) {
+#pragma unroll
+                for (int d = 0; d < kMaxDests; ++d)  // constant indices: no local copy
+                    if (d < sb_out.n) sb_out.p[d][i * W + c0 * V + g * V + b] = word;
+            }
         }
         const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
         st_cs<T, V>(x + base, xv[g]);
@@ -318,8 +343,11 @@ __global__ void __launch_bounds__(256) k_pa_step_coop(int64_t row0, int64_t nrow
         __stcs(x + il * 32 + lane, xn);
         __stcs(m + il * 32 + lane, mn);
         const uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
-        if (lane == 0)
-            for (int d = 0; d < sb_out.n; ++d) sb_out.p[d][i] = word;
+        if (lane == 0) {
+#pragma unroll
+            for (int d = 0; d < kMaxDests; ++d)
+                if (d < sb_out.n) sb_out.p[d][i] = word;
+        }
     }
 }
 
@@ -392,7 +420,9 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         qv.v[b] = qn;
         pv.v[b] = pn;
     }
-    for (int d = 0; d < q_out.n; ++d) *reinterpret_cast<Vec<T, V>*>(q_out.p[d] + base) = qv;
+#pragma unroll
+    for (int d = 0; d < kMaxDests; ++d)
+        if (d < q_out.n) *reinterpret_cast<Vec<T, V>*>(q_out.p[d] + base) = qv;
     st_cs<T, V>(p + pbase, pv);
 }
 

@@ -27,7 +27,7 @@ inline unsigned nblk(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div
 
 __device__ __forceinline__ uint64_t raw_draw(uint64_t seed, uint64_t stream, uint64_t k) {
     U64x4 o = philox4x64_10(k / 4 + 1, 0, stream, 0, seed, 0);
-    return o.v[k % 4];
+    return pick_word(o, (uint32_t)(k % 4));
 }
 
 __device__ __forceinline__ double unit_uniform(uint64_t raw) {

@@ -66,6 +66,12 @@ __device__ __forceinline__ U64x4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_
     return o;
 }
 
+// word k (0..3) of a Philox block by register select (a dynamic index would put the block
+// in local memory)
+__device__ __forceinline__ uint64_t pick_word(const U64x4& o, uint32_t k) {
+    return k == 0 ? o.v[0] : k == 1 ? o.v[1] : k == 2 ? o.v[2] : o.v[3];
+}
+
 // numpy Generator.uniform(lo, hi) = lo + (hi - lo) * ((raw >> 11) * 2^-53), no FMA.
 __device__ __forceinline__ double uniform_from_raw(uint64_t raw, double lo, double range) {
     double u = __dmul_rn((double)(raw >> 11), 1.0 / 9007199254740992.0);
