@@ -167,12 +167,13 @@ inline Dests<P> one_dest(P* ptr) {
 #ifndef VXQ_PA_LATE_XM
 #define VXQ_PA_LATE_XM 1
 #endif
-template <typename T, int V, int CPW>
+template <typename T, int V, int CPW, bool MULTI = false>
 __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int64_t nrows, int64_t R_pad,
                                                  Operator<T> op, const T* __restrict__ h,
                                                  T lam, T eta, T alpha, T* __restrict__ x,
                                                  T* __restrict__ m,
                                                  const uint32_t* __restrict__ sb_in,
+                                                 uint32_t* __restrict__ sb_one,
                                                  const Dests<uint32_t> sb_out) {
     using O = Ops<T>;
     constexpr int NB = V * CPW;  // values per lane == sign words per (row, warp)
@@ -267,9 +268,13 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
             mv[g].v[b] = mn;
             uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
             if (lane == g * V + b) {
+                if constexpr (MULTI) {
 #pragma unroll
-                for (int d = 0; d < kMaxDests; ++d)  // constant indices: no local copy
-                    if (d < sb_out.n) sb_out.p[d][i * W + c0 * V + g * V + b] = word;
+                    for (int d = 0; d < kMaxDests; ++d)  // constant indices: no local copy
+                        if (d < sb_out.n) sb_out.p[d][i * W + c0 * V + g * V + b] = word;
+                } else {
+                    sb_one[i * W + c0 * V + g * V + b] = word;
+                }
             }
         }
         const int64_t base = lane_base(il, R_pad, c0 + g, lane, V);
@@ -283,12 +288,13 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
 // base + 32 + l), issues all their spin-word gathers at once, then every row walks its
 // entries in ascending order through warp shuffles -- 3 memory round trips per RPW rows
 // instead of ~2 per neighbour, same sequential per-row sum as k_pa_step (bit-identical).
-template <typename T, int RPW>
+template <typename T, int RPW, bool MULTI = false>
 __global__ void __launch_bounds__(256) k_pa_step_coop(int64_t row0, int64_t nrows,
                                                       Operator<T> op, const T* __restrict__ h,
                                                       T lam, T eta, T alpha, T* __restrict__ x,
                                                       T* __restrict__ m,
                                                       const uint32_t* __restrict__ sb_in,
+                                                      uint32_t* __restrict__ sb_one,
                                                       const Dests<uint32_t> sb_out) {
     using O = Ops<T>;
     const int lane = threadIdx.x & 31;
@@ -344,9 +350,13 @@ __global__ void __launch_bounds__(256) k_pa_step_coop(int64_t row0, int64_t nrow
         __stcs(m + il * 32 + lane, mn);
         const uint32_t word = __ballot_sync(0xffffffffu, xn >= (T)0);
         if (lane == 0) {
+            if constexpr (MULTI) {
 #pragma unroll
-            for (int d = 0; d < kMaxDests; ++d)
-                if (d < sb_out.n) sb_out.p[d][i] = word;
+                for (int d = 0; d < kMaxDests; ++d)
+                    if (d < sb_out.n) sb_out.p[d][i] = word;
+            } else {
+                sb_one[i] = word;
+            }
         }
     }
 }
@@ -358,11 +368,12 @@ struct SbmScalars {
 };
 
 // Rows [row0, row0 + nrows): q_in/q_out are full (global-row) buffers, p is local.
-template <typename T, int V>
+template <typename T, int V, bool MULTI = false>
 __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, int64_t R_pad,
                                                   Operator<T> op, const T* __restrict__ g,
                                                   SbmScalars<T> sc, const T* __restrict__ q_in,
-                                                  const Dests<T> q_out, T* __restrict__ p) {
+                                                  T* __restrict__ q_one, const Dests<T> q_out,
+                                                  T* __restrict__ p) {
     using O = Ops<T>;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -420,9 +431,13 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         qv.v[b] = qn;
         pv.v[b] = pn;
     }
+    if constexpr (MULTI) {
 #pragma unroll
-    for (int d = 0; d < kMaxDests; ++d)
-        if (d < q_out.n) *reinterpret_cast<Vec<T, V>*>(q_out.p[d] + base) = qv;
+        for (int d = 0; d < kMaxDests; ++d)
+            if (d < q_out.n) *reinterpret_cast<Vec<T, V>*>(q_out.p[d] + base) = qv;
+    } else {
+        *reinterpret_cast<Vec<T, V>*>(q_one + base) = qv;
+    }
     st_cs<T, V>(p + pbase, pv);
 }
 
@@ -679,23 +694,28 @@ int block_threads(int64_t items) {
     return (int)std::min<int64_t>(512, std::max<int64_t>(32, t));
 }
 
-template <typename T>
-void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T eta, T alpha,
-                    T* x, T* m, const uint32_t* sbi, const Dests<uint32_t>& sbo, cudaStream_t s) {
+// One destination (every solve except a peer-exchange session): the __restrict__ single
+// pointer variant (MULTI = false) -- the multi-destination loop is only compiled in for
+// row-partitioned ranks with peers.
+template <typename T, bool MULTI>
+void launch_pa_step_t(const Layout& L, const Operator<T>& op, const T* h, T lam, T eta,
+                      T alpha, T* x, T* m, const uint32_t* sbi, const Dests<uint32_t>& sbo,
+                      cudaStream_t s) {
     const int64_t chunks = L.R_pad / (32 * L.V);
+    uint32_t* one = sbo.p[0];
     if (L.R_pad == 32) {  // one sign word per row: cooperative warp-CSR over 8 rows
         constexpr int RPW = 8;
         const int64_t warps = ceil_div(L.nrows, RPW);
-        k_pa_step_coop<T, RPW><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, s>>>(
-            L.row0, L.nrows, op, h, lam, eta, alpha, x, m, sbi, sbo);
+        k_pa_step_coop<T, RPW, MULTI><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, s>>>(
+            L.row0, L.nrows, op, h, lam, eta, alpha, x, m, sbi, one, sbo);
         return;
     }
     const int cpw = (chunks % 2 == 0) ? 2 : 1;  // two chunks per warp when they pair up
     const int64_t warps = L.nrows * (chunks / cpw);
     const unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
 #define VXQ_PA_STEP(VV, CC)                                                                \
-    k_pa_step<T, VV, CC><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, h, lam, eta, \
-                                                alpha, x, m, sbi, sbo)
+    k_pa_step<T, VV, CC, MULTI><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, h,    \
+                                                       lam, eta, alpha, x, m, sbi, one, sbo)
     if (L.V == 1) {
         if (cpw == 2) VXQ_PA_STEP(1, 2); else VXQ_PA_STEP(1, 1);
     } else if (L.V == 2) {
@@ -709,23 +729,36 @@ void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T
 }
 template <typename T>
 void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T eta, T alpha,
+                    T* x, T* m, const uint32_t* sbi, const Dests<uint32_t>& sbo, cudaStream_t s) {
+    if (sbo.n > 1) launch_pa_step_t<T, true>(L, op, h, lam, eta, alpha, x, m, sbi, sbo, s);
+    else launch_pa_step_t<T, false>(L, op, h, lam, eta, alpha, x, m, sbi, sbo, s);
+}
+template <typename T>
+void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T eta, T alpha,
                     T* x, T* m, const uint32_t* sbi, uint32_t* sbo, cudaStream_t s) {
     launch_pa_step<T>(L, op, h, lam, eta, alpha, x, m, sbi, one_dest(sbo), s);
 }
 
+template <typename T, bool MULTI>
+void launch_sbm_step_t(const Layout& L, const Operator<T>& op, const T* g, SbmScalars<T> sc,
+                       const T* qi, const Dests<T>& qo, T* p, cudaStream_t s) {
+    int64_t warps = L.nrows * (L.R_pad / (32 * L.V));
+    unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
+    T* one = qo.p[0];
+    switch (L.V) {
+        case 1: k_sbm_step<T, 1, MULTI><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, one, qo, p); break;
+        case 2: k_sbm_step<T, 2, MULTI><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, one, qo, p); break;
+        default:
+            if constexpr (sizeof(T) == 4)
+                k_sbm_step<T, 4, MULTI><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, one, qo, p);
+            break;
+    }
+}
 template <typename T>
 void launch_sbm_step(const Layout& L, const Operator<T>& op, const T* g, SbmScalars<T> sc,
                      const T* qi, const Dests<T>& qo, T* p, cudaStream_t s) {
-    int64_t warps = L.nrows * (L.R_pad / (32 * L.V));
-    unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
-    switch (L.V) {
-        case 1: k_sbm_step<T, 1><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, qo, p); break;
-        case 2: k_sbm_step<T, 2><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, qo, p); break;
-        default:
-            if constexpr (sizeof(T) == 4)
-                k_sbm_step<T, 4><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, qo, p);
-            break;
-    }
+    if (qo.n > 1) launch_sbm_step_t<T, true>(L, op, g, sc, qi, qo, p, s);
+    else launch_sbm_step_t<T, false>(L, op, g, sc, qi, qo, p, s);
 }
 template <typename T>
 void launch_sbm_step(const Layout& L, const Operator<T>& op, const T* g, SbmScalars<T> sc,
