@@ -382,14 +382,22 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // CL = CTAs per cluster along the row dimension: the CL CTAs of a cluster process row
 // blocks mb = CL*p + rank of the same (step, replica block) and each TMA-multicasts 1/CL of
 // the shared B tile into all of them, cutting L2->SM traffic for B by CL.
-template <Kind KD, int CL>
+//
+// PAIR: the two CTAs of a cluster form a tcgen05 CTA pair (cta_group::2): tile = 256 rows
+// (128 per CTA, each CTA's TMEM holds its rows x all bn replicas) x bn replicas, each CTA
+// loads its A rows and HALF of B into its own smem (32 KB stages, 6 deep), only the leader
+// (rank 0) issues the M = 256 MMAs and its commits arrive in both CTAs.
+template <Kind KD, int CL, bool PAIR = false>
 __global__ void __launch_bounds__(DTHREADS, 1)
     k_dense_run(const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB0,
                 const __grid_constant__ CUtensorMap tmB1, DenseRunArgs a) {
     using TR = KindTraits<KD>;
-    constexpr int STAGES = TR::kStages;
-    constexpr int SBYTES = stage_bytes<KD>();
+    static_assert(!PAIR || (KD == Kind::kFp8 && CL == 1), "pair MMA: f8f6f4, no B multicast");
+    constexpr int NCTA = PAIR ? 2 : CL;
+    constexpr int STAGES = PAIR ? 6 : TR::kStages;
+    constexpr int SBYTES = PAIR ? DA_BYTES + TR::kBnMax / 2 * DROW : stage_bytes<KD>();
+    static_assert(STAGES * SBYTES <= 192 * 1024, "smem ring");
     extern __shared__ uint8_t smem_raw[];
     __shared__ int s_last;  // fused tracking: this tile completed its step's decisions
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -405,29 +413,34 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(full + s, 1);
-            ptx::mbar_init(empty + s, CL);  // released by the MMA of every CTA in the cluster
+            // released by the MMA of every CTA in the cluster (pair: the leader's only)
+            ptx::mbar_init(empty + s, PAIR ? 1 : CL);
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(tfull + s, 1);
-            ptx::mbar_init(tempty + s, 256);
+            ptx::mbar_init(tempty + s, PAIR ? 512 : 256);  // pair: both CTAs' epilogues
         }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB0);
         ptx::tma_prefetch(&tmB1);
     }
-    if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+    if (warp == 1) {
+        if constexpr (PAIR) ptx::tmem_alloc2<512>(tmem_slot);
+        else ptx::tmem_alloc<512>(tmem_slot);
+    }
     ptx::tc_fence_before();
-    if constexpr (CL > 1) ptx::cluster_sync();  // peers' barriers initialised before use
+    if constexpr (NCTA > 1) ptx::cluster_sync();  // peers' barriers initialised before use
     else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int crank = CL > 1 ? (int)ptx::cluster_ctarank() : 0;
-    const int wid0 = blockIdx.x / CL, wstride = gridDim.x / CL;  // cluster work index
-    const int mrows = (a.m_tiles + CL - 1) / CL;                 // row-block groups per step
-    const int tps = mrows * a.n_tiles;                           // work items per step
+    const int crank = NCTA > 1 ? (int)ptx::cluster_ctarank() : 0;
+    const int wid0 = blockIdx.x / NCTA, wstride = gridDim.x / NCTA;  // cluster work index
+    const int mrows = (a.m_tiles + NCTA - 1) / NCTA;                 // row-block groups per step
+    const int tps = mrows * a.n_tiles;                               // work items per step
     const int num_tiles = tps * a.T;
-    const uint32_t b_plane_bytes = (uint32_t)a.bn * DROW;
+    // B bytes per stage in this CTA's smem (pair: half of the bn replicas)
+    const uint32_t b_plane_bytes = (uint32_t)(PAIR ? a.bn / 2 : a.bn) * DROW;
     constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
     if (warp == 0) {
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             for (int g = wid0; g < num_tiles; g += wstride) {
                 int t, nb, mb;
                 decode_tile(a, g, tps, mrows, t, nb, mb);
-                mb = mb * CL + crank;
+                mb = mb * NCTA + crank;
                 const CUtensorMap* tmB = (t & 1) ? &tmB1 : &tmB0;
                 // A (the coupling panel) never depends on the dynamics: keep kPrefetch
                 // k-blocks of it on their way into L2 ahead of the smem loads
@@ -455,11 +468,18 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     ptx::mbar_wait(empty + stage, ph ^ 1);
                     if (a.stats) st_empty += clk() - c0;
                     uint8_t* sa = smem + stage * SBYTES;
-                    ptx::mbar_arrive_expect_tx(
-                        full + stage,
-                        a.a_tx_bytes + TR::kPlanes * (b_plane_bytes >> (a.b_fp4 ? 1 : 0)));
+                    const uint32_t tx =
+                        a.a_tx_bytes + TR::kPlanes * (b_plane_bytes >> (a.b_fp4 ? 1 : 0));
                     const int kcol = kb * (DROW / TR::kElemBytes);
-                    ptx::tma_load_2d_hint(sa, &tmA, full + stage, kcol, mb * DBM, keep);
+                    if constexpr (PAIR) {
+                        // the leader's barrier counts both CTAs' bytes; each CTA's loads land
+                        // in its own smem and complete on the leader's barrier
+                        if (crank == 0) ptx::mbar_arrive_expect_tx(full + stage, 2 * tx);
+                        ptx::tma_load_2d_2sm(sa, &tmA, full + stage, kcol, mb * DBM, keep);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(full + stage, tx);
+                        ptx::tma_load_2d_hint(sa, &tmA, full + stage, kcol, mb * DBM, keep);
+                    }
                     if (kb == 0 && t > 0) {
                         const long long c1 = a.stats ? clk() : 0;
                         // B_t[nb] complete? (release/acquire on the step t-1 counter, then a
@@ -477,7 +497,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                         if (a.stats) st_dep += clk() - c1;
                     }
-                    if constexpr (CL > 1) {
+                    if constexpr (PAIR) {
+                        ptx::tma_load_2d_2sm(sa + DA_BYTES, tmB, full + stage, kcol,
+                                             nb * a.bn + crank * (a.bn / 2), keep);
+                    } else if constexpr (CL > 1) {
                         static_assert(TR::kPlanes == 1, "B multicast: single-plane B only");
                         const int hrows = a.bn / CL;
                         ptx::tma_load_2d_mc(sa + DA_BYTES + crank * hrows * DROW, tmB,
@@ -502,10 +525,12 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (single thread issues for the CTA)
+        // ---------------- MMA issuer (single thread issues for the CTA / the pair's leader)
+        if (PAIR && crank != 0) goto mma_done;
+        {
         const uint32_t idesc =
             TR::kIdescBase | a.idesc_extra | ((uint32_t)(a.bn >> 3) << 17) |
-            ((uint32_t)(DBM >> 4) << 24);
+            ((uint32_t)((PAIR ? 2 * DBM : DBM) >> 4) << 24);
         int stage = 0;
         uint32_t ph = 0;
         int lt = 0;
@@ -533,13 +558,16 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 #pragma unroll
                         for (int k = 0; k < DROW / 32; ++k) {  // 32 B of K per MMA
                             const uint32_t accum = (kb | pl | k) != 0;
-                            if constexpr (KD == Kind::kFp8)
+                            if constexpr (PAIR)
+                                ptx::mma2_f8f6f4(d, da + 2 * k, db + 2 * k, idesc, accum);
+                            else if constexpr (KD == Kind::kFp8)
                                 ptx::mma_f8f6f4(d, da + 2 * k, db + 2 * k, idesc, accum);
                             else
                                 ptx::mma_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
                         }
                     }
-                    if constexpr (CL > 1) ptx::mma_commit_mc(empty + stage, kMask);
+                    if constexpr (PAIR) ptx::mma2_commit_mc(empty + stage, 0x3);
+                    else if constexpr (CL > 1) ptx::mma_commit_mc(empty + stage, kMask);
                     else ptx::mma_commit(empty + stage);
                 }
                 __syncwarp();
@@ -548,7 +576,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     ph ^= 1;
                 }
             }
-            if (ptx::elect_one()) ptx::mma_commit(tfull + acc);
+            if (ptx::elect_one()) {
+                if constexpr (PAIR) ptx::mma2_commit_mc(tfull + acc, 0x3);
+                else ptx::mma_commit(tfull + acc);
+            }
             __syncwarp();
         }
         if (a.stats && lane == 0) {
@@ -556,6 +587,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             atomicAdd(a.stats + 3, (unsigned long long)mm_tempty);
             atomicAdd(a.stats + 6, (unsigned long long)lt);
         }
+        }
+    mma_done:;
     } else {
         // ---------------- epilogue (8 warps): TMEM -> integrator -> next B operand
         // warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a lane quarter
@@ -573,7 +606,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         for (int g = wid0; g < num_tiles; g += wstride, ++lt) {
             int t, nb, mb;
             decode_tile(a, g, tps, mrows, t, nb, mb);
-            mb = mb * CL + crank;
+            mb = mb * NCTA + crank;
             const bool tile_ok = mb < a.m_tiles;  // last cluster row group may be partial
             const int acc = lt & 1;
             const uint32_t acc_ph = (lt >> 1) & 1;
@@ -739,7 +772,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             }
             if (a.stats && ep_tid == 0) ep_busy += clk() - c1;
             ptx::tc_fence_before();
-            ptx::mbar_arrive(tempty + acc);
+            if constexpr (PAIR) ptx::mbar_arrive_leader(tempty + acc);  // the MMA is there
+            else ptx::mbar_arrive(tempty + acc);
             if (a.mode == 0 && a.bestq && t > 0 && tile_ok) {
                 // the tile that completes the step-t decisions of this replica block folds
                 // q_{t-1} into bestq -- before its own publish below, so step-(t+1) tiles
@@ -772,8 +806,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     }
     __syncthreads();
     if (a.stats && threadIdx.x == 0) atomicMax(a.stats + 7, (unsigned long long)(clk() - t_start));
-    if constexpr (CL > 1) ptx::cluster_sync();  // no CTA exits while peers still signal it
-    if (warp == 1) ptx::tmem_dealloc<512>(tmem_base);
+    if constexpr (NCTA > 1) ptx::cluster_sync();  // no CTA exits while peers still signal it
+    if (warp == 1) {
+        if constexpr (PAIR) ptx::tmem_dealloc2<512>(tmem_base);
+        else ptx::tmem_dealloc<512>(tmem_base);
+    }
 }
 
 constexpr int TB = 256;
@@ -836,24 +873,25 @@ int pick_group(int n_tiles) {
     return gsz;
 }
 
-template <Kind KD, int CL>
+template <Kind KD, int CL, bool PAIR = false>
 void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorMap& tmB1,
                 DenseRunArgs a, int64_t steps_for_grid, cudaStream_t s, bool cooperative) {
-    auto kern = k_dense_run<KD, CL>;
+    constexpr int NCTA = PAIR ? 2 : CL;
+    auto kern = k_dense_run<KD, CL, PAIR>;
     VXQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM));
-    const int64_t items = (int64_t)((a.m_tiles + CL - 1) / CL) * a.n_tiles *
+    const int64_t items = (int64_t)((a.m_tiles + NCTA - 1) / NCTA) * a.n_tiles *
                           std::max<int64_t>(steps_for_grid, 1);
-    const int64_t clusters = std::min<int64_t>(items, num_sms() / CL);
+    const int64_t clusters = std::min<int64_t>(items, num_sms() / NCTA);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(clusters * CL));
+    cfg.gridDim = dim3((unsigned)(clusters * NCTA));
     cfg.blockDim = dim3(DTHREADS);
     cfg.dynamicSmemBytes = DSMEM;
     cfg.stream = s;
     cudaLaunchAttribute attrs[2];
     int na = 0;
-    if (CL > 1) {
+    if (NCTA > 1) {
         attrs[na].id = cudaLaunchAttributeClusterDimension;
-        attrs[na].val.clusterDim.x = CL;
+        attrs[na].val.clusterDim.x = NCTA;
         attrs[na].val.clusterDim.y = 1;
         attrs[na].val.clusterDim.z = 1;
         ++na;
@@ -973,7 +1011,8 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
 }
 
 static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap& tb0,
-                       const CUtensorMap& tb1, bool bf16, int cl, cudaStream_t s) {
+                       const CUtensorMap& tb1, bool bf16, int cl, cudaStream_t s,
+                       bool pair = false) {
     const char* want = getenv("VXQ_DENSE_STATS");
     DevBuf<unsigned long long> stats;
     if (want && want[0] == '1') {
@@ -987,6 +1026,7 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     VXQ_CUDA(cudaEventRecord(e0, s));
     if (a.T > 0) {
         if (bf16) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (pair) launch_run<Kind::kFp8, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
         else if (cl == 2) launch_run<Kind::kFp8, 2>(tmA, tb0, tb1, a, a.T, s, true);
         else launch_run<Kind::kFp8, 1>(tmA, tb0, tb1, a, a.T, s, true);
     }
@@ -1037,12 +1077,19 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     int cl = 1;
     if (const char* e = getenv("VXQ_DENSE_CLUSTER")) cl = atoi(e) == 2 ? 2 : 1;
     if (ceil_div(n, DBM) < 2) cl = 1;
-    CUtensorMap tmB0 = s_fp4 ? make_map_fp4(s0.get(), ld, R, DROW, bn / cl)
+    // tcgen05 CTA pairs (M = 256 tiles, each CTA holds half of B: half the smem operand
+    // traffic per MMA; cfg2 +9 %); VXQ_DENSE_2CTA=0 -> one CTA per 128-row tile
+    bool pair = true;
+    if (const char* e = getenv("VXQ_DENSE_2CTA")) pair = atoi(e) == 1;
+    if (ceil_div(n, DBM) < 2 || bn % 32 != 0) pair = false;
+    if (pair) cl = 1;
+    const int bbox = pair ? bn / 2 : bn / cl;  // B rows (replicas) per TMA box
+    CUtensorMap tmB0 = s_fp4 ? make_map_fp4(s0.get(), ld, R, DROW, bbox)
                              : make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1,
-                                        DROW, bn / cl, 1);
-    CUtensorMap tmB1 = s_fp4 ? make_map_fp4(s1.get(), ld, R, DROW, bn / cl)
+                                        DROW, bbox, 1);
+    CUtensorMap tmB1 = s_fp4 ? make_map_fp4(s1.get(), ld, R, DROW, bbox)
                              : make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1,
-                                        DROW, bn / cl, 1);
+                                        DROW, bbox, 1);
     std::vector<float> s32(T);
     for (int64_t t = 0; t < T; ++t) s32[t] = (float)sched[t];
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
@@ -1095,7 +1142,7 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
         a.best_s = best_s.get();
         a.decided = decided.get();
     }
-    *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, cl, s);
+    *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, cl, s, pair);
     *launches += 2;
     if (trace_out) {
         DevBuf<double> tr(std::max<int64_t>(T, 1), s);

@@ -440,3 +440,16 @@ def test_dense_fused_best_tracking_matches_emulation(n, R, T):
     # improvement mode never reports worse than the final states
     plain = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=8))
     assert np.all(r.energies <= plain.energies)
+
+
+@pytest.mark.parametrize("n", [384, 129, 1153])
+def test_dense_pair_odd_row_tiles(n):
+    """CTA-pair tiles (M = 256) with an odd number of 128-row tiles (the last pair's second
+    CTA has no rows): still bit-exact with the fp32 emulation."""
+    m = sk_model(n, 5)
+    R = 256
+    r = vxq.run_pa(m, vxq.PaParams(steps=12, replicas=R, seed=6), path="dense", want_state=True)
+    assert r.info["path"] == "dense"
+    X, M = _dense_pa_emulation(m, R, 12, 6)
+    assert np.array_equal(r.x, X.astype(np.float64))
+    assert np.array_equal(r.energies, O.energies_exact(m, r.states))
