@@ -38,8 +38,10 @@ namespace vxq {
 constexpr int DBM = 128;   // rows (i) per tile
 constexpr int DROW = 128;  // bytes per K-major smem row (one SWIZZLE_128B atom row)
 constexpr int DA_BYTES = DBM * DROW;
-constexpr int DTHREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
-constexpr int DSMEM = 192 * 1024 + 1024 + 256;
+constexpr int DTHREADS = 352;  // TMA warp, MMA warp, 8 epilogue warps, x/m loader warp
+constexpr int RING_BYTES = 224 * 1024;  // operand stages + x/m staging slots
+constexpr int XM_SLOT_BYTES = 2 * 16 * DBM * 4;  // x and m of 16 replicas x 128 rows (fp32)
+constexpr int DSMEM = RING_BYTES + 1024 + 256;
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
 enum class Kind : int { kFp8 = 0, kBf16x3 = 1 };
@@ -129,7 +131,8 @@ EncodeFn get_encode() {
 // up to 3-D tensor [planes][outer][inner] (elements of `esize` bytes), SW128 boxes
 CUtensorMap make_map(const void* base, CUtensorMapDataType dt, int esize, uint64_t inner,
                      uint64_t outer, uint64_t planes, uint32_t box_inner, uint32_t box_outer,
-                     uint32_t box_planes) {
+                     uint32_t box_planes,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     CUtensorMap m;
     const cuuint32_t rank = planes > 1 ? 3 : 2;
     cuuint64_t dims[3] = {inner, outer, planes};
@@ -137,7 +140,7 @@ CUtensorMap make_map(const void* base, CUtensorMapDataType dt, int esize, uint64
     cuuint32_t box[3] = {box_inner, box_outer, box_planes};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = get_encode()(&m, dt, rank, const_cast<void*>(base), dims, strides, box, es,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(VXQ_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -345,6 +348,7 @@ struct DenseRunArgs {
     uint32_t idesc_extra;    // OR-ed into the instruction descriptor (A operand format)
     uint32_t a_tx_bytes;     // transaction bytes of one A box (packed fp4 counts global bytes)
     int b_fp4;               // B operand (spins) as packed E2M1 nibbles
+    int xm;                  // PA steps: x/m staged by the loader warp (TMA) into smem
     // fused best-state tracking (improvement mode; needs qtrace, h = 0):
     long long* bestq;        // [R] lowest 2 sum K s s of s_0..s_{t-2} (LLONG_MAX initially)
     int8_t* best_s;          // [R][ld] best spins so far
@@ -387,26 +391,37 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // (128 per CTA, each CTA's TMEM holds its rows x all bn replicas) x bn replicas, each CTA
 // loads its A rows and HALF of B into its own smem (32 KB stages, 6 deep), only the leader
 // (rank 0) issues the M = 256 MMAs and its commits arrive in both CTAs.
+//
+// a.xm (PA steps): a loader warp TMA-loads each tile's x/m in 16-replica chunks into XMS
+// shared-memory slots ahead of the epilogue (after acquiring the step-(t-1) counter), so the
+// epilogue's inputs are in flight without occupying registers.
 template <Kind KD, int CL, bool PAIR = false>
 __global__ void __launch_bounds__(DTHREADS, 1)
     k_dense_run(const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB0,
-                const __grid_constant__ CUtensorMap tmB1, DenseRunArgs a) {
+                const __grid_constant__ CUtensorMap tmB1,
+                const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ CUtensorMap tmM, DenseRunArgs a) {
     using TR = KindTraits<KD>;
     static_assert(!PAIR || (KD == Kind::kFp8 && CL == 1), "pair MMA: f8f6f4, no B multicast");
     constexpr int NCTA = PAIR ? 2 : CL;
-    constexpr int STAGES = PAIR ? 6 : TR::kStages;
+    constexpr int STAGES = PAIR ? 5 : TR::kStages;
     constexpr int SBYTES = PAIR ? DA_BYTES + TR::kBnMax / 2 * DROW : stage_bytes<KD>();
-    static_assert(STAGES * SBYTES <= 192 * 1024, "smem ring");
+    constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
+    static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
+    static_assert(KD != Kind::kFp8 || XMS >= 2, "x/m staging slots");
     extern __shared__ uint8_t smem_raw[];
     __shared__ int s_last;  // fused tracking: this tile completed its step's decisions
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 192 * 1024);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* xfull = tempty + 2;                                    // [XMS]
+    uint64_t* xempty = xfull + (XMS > 0 ? XMS : 1);                  // [XMS]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + (XMS > 0 ? XMS : 1));
+    uint8_t* xm_smem = smem + STAGES * SBYTES;                       // XMS x XM_SLOT_BYTES
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long t_start = clk();
@@ -420,10 +435,18 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             ptx::mbar_init(tfull + s, 1);
             ptx::mbar_init(tempty + s, PAIR ? 512 : 256);  // pair: both CTAs' epilogues
         }
+        for (int s = 0; s < XMS; ++s) {
+            ptx::mbar_init(xfull + s, 1);
+            ptx::mbar_init(xempty + s, 4);  // the 4 epilogue warps of one half
+        }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB0);
         ptx::tma_prefetch(&tmB1);
+        if (a.xm) {
+            ptx::tma_prefetch(&tmX);
+            ptx::tma_prefetch(&tmM);
+        }
     }
     if (warp == 1) {
         if constexpr (PAIR) ptx::tmem_alloc2<512>(tmem_slot);
@@ -589,6 +612,49 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         }
         }
     mma_done:;
+    } else if (warp == 10) {
+        // ---------------- x/m loader (PA steps): chunk c of every tile this CTA owns
+        if (a.xm && a.mode == 0 && ptx::elect_one()) {
+            const uint64_t pol = ptx::policy_evict_first();
+            const int nch = a.bn / 16;
+            int slot = 0;
+            uint32_t ph = 0;
+            for (int g = wid0; g < num_tiles; g += wstride) {
+                int t, nb, mb;
+                decode_tile(a, g, tps, mrows, t, nb, mb);
+                mb = mb * NCTA + crank;
+                if (mb >= a.m_tiles) continue;  // no rows: the epilogue skips it too
+                if (t > 0) {
+                    // x/m of step t were written by the step-(t-1) tiles of this replica
+                    // block (any CTA): acquire their counter, then order the async-proxy
+                    // loads after it
+                    const unsigned* cnt = a.done + (size_t)(t - 1) * a.n_tiles + nb;
+                    if (ld_acquire_gpu(cnt) < (unsigned)a.m_tiles) {
+                        uint64_t t0, tn;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                        while (ld_acquire_gpu(cnt) < (unsigned)a.m_tiles) {
+                            __nanosleep(64);
+                            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                            if (tn - t0 > 10ull * 1000 * 1000 * 1000) __trap();
+                        }
+                    }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                for (int c = 0; c < nch; ++c) {
+                    ptx::mbar_wait(xempty + slot, ph ^ 1);
+                    uint8_t* xs = xm_smem + slot * XM_SLOT_BYTES;
+                    ptx::mbar_arrive_expect_tx(xfull + slot, XM_SLOT_BYTES);
+                    ptx::tma_load_2d_hint(xs, &tmX, xfull + slot, mb * DBM, nb * a.bn + c * 16,
+                                          pol);
+                    ptx::tma_load_2d_hint(xs + XM_SLOT_BYTES / 2, &tmM, xfull + slot, mb * DBM,
+                                          nb * a.bn + c * 16, pol);
+                    if (++slot == XMS) {
+                        slot = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
     } else {
         // ---------------- epilogue (8 warps): TMEM -> integrator -> next B operand
         // warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a lane quarter
@@ -601,7 +667,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         const int nch = a.bn / 16;
         float* __restrict__ xg = a.x;
         float* __restrict__ mg = a.m;
-        int lt = 0;
+        int lt = 0, xm_tiles = 0;
         long long ep_wait = 0, ep_busy = 0;
         for (int g = wid0; g < num_tiles; g += wstride, ++lt) {
             int t, nb, mb;
@@ -628,7 +694,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     mo[jj] = ok ? ptx::ld_stream(mg + base + (int64_t)jj * a.ld, stream) : 0.f;
                 }
             };
-            if (a.mode == 0 && half < nch) {
+            const bool xm = a.xm && a.mode == 0;
+            if (a.mode == 0 && !xm && half < nch) {
                 // x/m of step t are written by the step-(t-1) tiles of this replica block
                 // (possibly on other CTAs): acquire their counter before the early load
                 if (t > 0) {
@@ -741,12 +808,35 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         }
                     }
                 };
+                if (xm) {
+                    if (tile_ok) {
 #pragma unroll 1
-                for (int c = half; c < nch; c += 4) {  // xA/mA hold chunk c
-                    if (c + 2 < nch) load_chunk(c + 2, xB, mB);
-                    process(c, xA, mA);
-                    if (c + 4 < nch) load_chunk(c + 4, xA, mA);
-                    if (c + 2 < nch) process(c + 2, xB, mB);
+                        for (int c = half; c < nch; c += 2) {
+                            const int seq = xm_tiles * nch + c;
+                            const int slot = seq % XMS;
+                            ptx::mbar_wait(xfull + slot, (uint32_t)(seq / XMS) & 1u);
+                            const float* xs =
+                                reinterpret_cast<const float*>(xm_smem + slot * XM_SLOT_BYTES);
+                            const float* ms = xs + 16 * DBM;
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) {
+                                xA[jj] = xs[jj * DBM + row];
+                                mA[jj] = ms[jj * DBM + row];
+                            }
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(xempty + slot);  // slot refillable
+                            process(c, xA, mA);
+                        }
+                        ++xm_tiles;
+                    }
+                } else {
+#pragma unroll 1
+                    for (int c = half; c < nch; c += 4) {  // xA/mA hold chunk c
+                        if (c + 2 < nch) load_chunk(c + 2, xB, mB);
+                        process(c, xA, mA);
+                        if (c + 4 < nch) load_chunk(c + 4, xA, mA);
+                        if (c + 2 < nch) process(c + 2, xB, mB);
+                    }
                 }
             } else if (a.mode == 1) {
                 // energy pass (fp8 signs): 2 q_r = sum_i s_i (K s)_i, exact integers
@@ -875,7 +965,8 @@ int pick_group(int n_tiles) {
 
 template <Kind KD, int CL, bool PAIR = false>
 void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorMap& tmB1,
-                DenseRunArgs a, int64_t steps_for_grid, cudaStream_t s, bool cooperative) {
+                DenseRunArgs a, int64_t steps_for_grid, cudaStream_t s, bool cooperative,
+                const CUtensorMap* tmX = nullptr, const CUtensorMap* tmM = nullptr) {
     constexpr int NCTA = PAIR ? 2 : CL;
     auto kern = k_dense_run<KD, CL, PAIR>;
     VXQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM));
@@ -904,7 +995,9 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
     }
     cfg.attrs = attrs;
     cfg.numAttrs = na;
-    VXQ_CUDA(cudaLaunchKernelEx(&cfg, kern, tmA, tmB0, tmB1, a));
+    VXQ_REQUIRE(!a.xm || (tmX && tmM), "x/m staging needs their tensor maps");
+    VXQ_CUDA(cudaLaunchKernelEx(&cfg, kern, tmA, tmB0, tmB1, tmX ? *tmX : tmA, tmM ? *tmM : tmA,
+                                a));
     VXQ_CHECK_LAUNCH();
 }
 
@@ -1012,7 +1105,8 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
 
 static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap& tb0,
                        const CUtensorMap& tb1, bool bf16, int cl, cudaStream_t s,
-                       bool pair = false) {
+                       bool pair = false, const CUtensorMap* tmX = nullptr,
+                       const CUtensorMap* tmM = nullptr) {
     const char* want = getenv("VXQ_DENSE_STATS");
     DevBuf<unsigned long long> stats;
     if (want && want[0] == '1') {
@@ -1026,9 +1120,9 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     VXQ_CUDA(cudaEventRecord(e0, s));
     if (a.T > 0) {
         if (bf16) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
-        else if (pair) launch_run<Kind::kFp8, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
-        else if (cl == 2) launch_run<Kind::kFp8, 2>(tmA, tb0, tb1, a, a.T, s, true);
-        else launch_run<Kind::kFp8, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (pair) launch_run<Kind::kFp8, 1, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
+        else if (cl == 2) launch_run<Kind::kFp8, 2>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
+        else launch_run<Kind::kFp8, 1>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
     }
     VXQ_CUDA(cudaEventRecord(e1, s));
     float ms = 0;
@@ -1142,7 +1236,18 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
         a.best_s = best_s.get();
         a.decided = decided.get();
     }
-    *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, cl, s, pair);
+    // x/m staged into shared memory by the loader warp (VXQ_DENSE_XM=0: register loads)
+    bool xm = true;
+    if (const char* e = getenv("VXQ_DENSE_XM")) xm = atoi(e) == 1;
+    CUtensorMap tmX{}, tmM{};
+    if (xm && a.mode == 0) {
+        tmX = make_map(x.get(), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ld, R, 1, DBM, 16, 1,
+                       CU_TENSOR_MAP_SWIZZLE_NONE);
+        tmM = make_map(m.get(), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ld, R, 1, DBM, 16, 1,
+                       CU_TENSOR_MAP_SWIZZLE_NONE);
+        a.xm = 1;
+    }
+    *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, cl, s, pair, &tmX, &tmM);
     *launches += 2;
     if (trace_out) {
         DevBuf<double> tr(std::max<int64_t>(T, 1), s);
