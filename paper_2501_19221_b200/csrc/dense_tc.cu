@@ -349,6 +349,7 @@ struct DenseRunArgs {
     uint32_t a_tx_bytes;     // transaction bytes of one A box (packed fp4 counts global bytes)
     int b_fp4;               // B operand (spins) as packed E2M1 nibbles
     int xm;                  // PA steps: x/m staged by the loader warp (TMA) into smem
+    uint32_t b_tx_bytes;     // transaction bytes of one B box (per plane) as delivered
     // fused best-state tracking (improvement mode; needs qtrace, h = 0):
     long long* bestq;        // [R] lowest 2 sum K s s of s_0..s_{t-2} (LLONG_MAX initially)
     int8_t* best_s;          // [R][ld] best spins so far
@@ -395,7 +396,14 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // a.xm (PA steps): a loader warp TMA-loads each tile's x/m in 16-replica chunks into XMS
 // shared-memory slots ahead of the epilogue (after acquiring the step-(t-1) counter), so the
 // epilogue's inputs are in flight without occupying registers.
-template <Kind KD, int CL, bool PAIR = false>
+//
+// MX: kind::mxf4 (block-scaled E2M1, twice the f8f6f4 rate) with K and the spins packed two
+// per byte in smem too (a 128-byte smem row = 256 K elements: half the operand bytes per
+// flop); the scale factors are all 1 (UE8M0 0x7F), written once into TMEM columns
+// kSfCol..511, and the two accumulators sit at columns 0 / kAccMx (bn <= 240).
+constexpr uint32_t kAccMx = 240, kSfCol = 480;
+
+template <Kind KD, int CL, bool PAIR = false, bool MX = false>
 __global__ void __launch_bounds__(DTHREADS, 1)
     k_dense_run(const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB0,
@@ -404,6 +412,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const __grid_constant__ CUtensorMap tmM, DenseRunArgs a) {
     using TR = KindTraits<KD>;
     static_assert(!PAIR || (KD == Kind::kFp8 && CL == 1), "pair MMA: f8f6f4, no B multicast");
+    static_assert(!MX || (KD == Kind::kFp8 && CL == 1), "mxf4: fp8-kind layout, no multicast");
+    constexpr uint32_t ACC_COLS = MX ? kAccMx : 256;
     constexpr int NCTA = PAIR ? 2 : CL;
     constexpr int STAGES = PAIR ? 5 : TR::kStages;
     constexpr int SBYTES = PAIR ? DA_BYTES + TR::kBnMax / 2 * DROW : stage_bytes<KD>();
@@ -457,6 +467,15 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if constexpr (MX) {  // unit scale factors (UE8M0 0x7F) for every row / column block
+        if (warp >= 2 && warp < 6)
+            ptx::tmem_fill_32x32b_x32(tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + kSfCol,
+                                      0x7F7F7F7Fu);
+        ptx::tc_fence_before();
+        if constexpr (NCTA > 1) ptx::cluster_sync();
+        else __syncthreads();
+        ptx::tc_fence_after();
+    }
     const int crank = NCTA > 1 ? (int)ptx::cluster_ctarank() : 0;
     const int wid0 = blockIdx.x / NCTA, wstride = gridDim.x / NCTA;  // cluster work index
     const int mrows = (a.m_tiles + NCTA - 1) / NCTA;                 // row-block groups per step
@@ -491,8 +510,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     ptx::mbar_wait(empty + stage, ph ^ 1);
                     if (a.stats) st_empty += clk() - c0;
                     uint8_t* sa = smem + stage * SBYTES;
-                    const uint32_t tx =
-                        a.a_tx_bytes + TR::kPlanes * (b_plane_bytes >> (a.b_fp4 ? 1 : 0));
+                    const uint32_t tx = a.a_tx_bytes + TR::kPlanes * a.b_tx_bytes;
                     const int kcol = kb * (DROW / TR::kElemBytes);
                     if constexpr (PAIR) {
                         // the leader's barrier counts both CTAs' bytes; each CTA's loads land
@@ -551,9 +569,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         // ---------------- MMA issuer (single thread issues for the CTA / the pair's leader)
         if (PAIR && crank != 0) goto mma_done;
         {
+        // mxf4 (block-scaled descriptor): E2M1 = 1 for A and B, UE8M0 scales (bit 23),
+        // K = 64 per MMA, scale-factor ids 0; no accumulator-format field
         const uint32_t idesc =
-            TR::kIdescBase | a.idesc_extra | ((uint32_t)(a.bn >> 3) << 17) |
-            ((uint32_t)((PAIR ? 2 * DBM : DBM) >> 4) << 24);
+            (MX ? ((1u << 7) | (1u << 10) | (1u << 23)) : (TR::kIdescBase | a.idesc_extra)) |
+            ((uint32_t)(a.bn >> 3) << 17) | ((uint32_t)((PAIR ? 2 * DBM : DBM) >> 4) << 24);
         int stage = 0;
         uint32_t ph = 0;
         int lt = 0;
@@ -565,7 +585,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             ptx::mbar_wait(tempty + acc, acc_ph ^ 1);
             if (a.stats) mm_tempty += clk() - c0;
             ptx::tc_fence_after();
-            const uint32_t d = tmem_base + acc * 256;
+            const uint32_t d = tmem_base + acc * ACC_COLS;
             for (int kb = 0; kb < a.kblocks; ++kb) {
                 c0 = a.stats ? clk() : 0;
                 ptx::mbar_wait(full + stage, ph);
@@ -581,7 +601,15 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 #pragma unroll
                         for (int k = 0; k < DROW / 32; ++k) {  // 32 B of K per MMA
                             const uint32_t accum = (kb | pl | k) != 0;
-                            if constexpr (PAIR)
+                            if constexpr (MX && PAIR)
+                                ptx::mma2_mxf4(d, da + 2 * k, db + 2 * k, idesc,
+                                               tmem_base + kSfCol, tmem_base + kSfCol + 16,
+                                               accum);
+                            else if constexpr (MX)
+                                ptx::mma_mxf4(d, da + 2 * k, db + 2 * k, idesc,
+                                              tmem_base + kSfCol, tmem_base + kSfCol + 16,
+                                              accum);
+                            else if constexpr (PAIR)
                                 ptx::mma2_f8f6f4(d, da + 2 * k, db + 2 * k, idesc, accum);
                             else if constexpr (KD == Kind::kFp8)
                                 ptx::mma_f8f6f4(d, da + 2 * k, db + 2 * k, idesc, accum);
@@ -678,7 +706,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             const uint32_t acc_ph = (lt >> 1) & 1;
             const int i = mb * DBM + row;
             const bool row_ok = i < a.n;
-            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
             // x/m of this warp's chunks do not depend on the accumulator: the first chunk's
             // loads are issued before waiting for the MMA, and each later chunk's while the
             // previous one is computed (two register buffers, chunks c, c+2, c+4, ...)
@@ -963,12 +991,12 @@ int pick_group(int n_tiles) {
     return gsz;
 }
 
-template <Kind KD, int CL, bool PAIR = false>
+template <Kind KD, int CL, bool PAIR = false, bool MX = false>
 void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorMap& tmB1,
                 DenseRunArgs a, int64_t steps_for_grid, cudaStream_t s, bool cooperative,
                 const CUtensorMap* tmX = nullptr, const CUtensorMap* tmM = nullptr) {
     constexpr int NCTA = PAIR ? 2 : CL;
-    auto kern = k_dense_run<KD, CL, PAIR>;
+    auto kern = k_dense_run<KD, CL, PAIR, MX>;
     VXQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM));
     const int64_t items = (int64_t)((a.m_tiles + NCTA - 1) / NCTA) * a.n_tiles *
                           std::max<int64_t>(steps_for_grid, 1);
@@ -1086,6 +1114,7 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
     DenseRunArgs e{};
     e.idesc_extra = d->afmt << 7;  // A = K (fp8 or packed fp4)
     e.a_tx_bytes = a_tx_bytes(d);
+    e.b_tx_bytes = (uint32_t)bn * DROW;  // fp8 signs
     e.n = (int)n;
     e.R = (int)R;
     e.ld = (int)ld;
@@ -1106,7 +1135,7 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
 static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap& tb0,
                        const CUtensorMap& tb1, bool bf16, int cl, cudaStream_t s,
                        bool pair = false, const CUtensorMap* tmX = nullptr,
-                       const CUtensorMap* tmM = nullptr) {
+                       const CUtensorMap* tmM = nullptr, bool mx = false) {
     const char* want = getenv("VXQ_DENSE_STATS");
     DevBuf<unsigned long long> stats;
     if (want && want[0] == '1') {
@@ -1120,6 +1149,9 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     VXQ_CUDA(cudaEventRecord(e0, s));
     if (a.T > 0) {
         if (bf16) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (pair && mx)
+            launch_run<Kind::kFp8, 1, true, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
+        else if (mx) launch_run<Kind::kFp8, 1, false, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
         else if (pair) launch_run<Kind::kFp8, 1, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
         else if (cl == 2) launch_run<Kind::kFp8, 2>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
         else launch_run<Kind::kFp8, 1>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
@@ -1165,7 +1197,16 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     k_init_pa_rm<<<nblk(((n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, x.get(), m.get(),
                                                        s0.get(), s_fp4);
     VXQ_CHECK_LAUNCH();
-    const int bn = choose_bn(n, R, 1, KindTraits<Kind::kFp8>::kBnMax);
+    // kind::mxf4 (VXQ_DENSE_MXF4=1): packed E2M1 operands in smem at twice the f8f6f4 MMA
+    // rate; needs the packed K and spins, and bn <= 240 (TMEM holds the scale factors too)
+    bool mx = true;  // cfg2: 120 -> 139 Grv/s (less operand traffic and power per flop)
+    if (const char* e = getenv("VXQ_DENSE_MXF4")) mx = atoi(e) == 1;
+    if (!(d->afmt == 5 && s_fp4)) mx = false;
+    int bn = choose_bn(n, R, 1, KindTraits<Kind::kFp8>::kBnMax);
+    if (mx) {  // fewest <= 240-wide replica blocks, rounded up to 16 (pair N % 16 == 0)
+        const int64_t blocks = ceil_div(R, (int64_t)kAccMx);
+        bn = (int)std::min<int64_t>(kAccMx, ceil_div(ceil_div(R, blocks), 16) * 16);
+    }
     // VXQ_DENSE_CLUSTER=2: B multicast across 2-CTA clusters (fewer cycles, same wall time
     // under the 1 kW power cap; cluster + cooperative launches cannot be profiled by ncu)
     int cl = 1;
@@ -1176,26 +1217,33 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     bool pair = true;
     if (const char* e = getenv("VXQ_DENSE_2CTA")) pair = atoi(e) == 1;
     if (ceil_div(n, DBM) < 2 || bn % 32 != 0) pair = false;
-    if (pair) cl = 1;
+    if (pair || mx) cl = 1;
     const int bbox = pair ? bn / 2 : bn / cl;  // B rows (replicas) per TMA box
-    CUtensorMap tmB0 = s_fp4 ? make_map_fp4(s0.get(), ld, R, DROW, bbox)
-                             : make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1,
-                                        DROW, bbox, 1);
-    CUtensorMap tmB1 = s_fp4 ? make_map_fp4(s1.get(), ld, R, DROW, bbox)
-                             : make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1,
-                                        DROW, bbox, 1);
+    CUtensorMap tmB0, tmB1, tmAmx;
+    if (mx) {  // packed bytes as they are in global memory: 128-byte rows = 256 elements
+        tmB0 = make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld / 2, R, 1, DROW, bbox, 1);
+        tmB1 = make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld / 2, R, 1, DROW, bbox, 1);
+        tmAmx = make_map(d->K8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld / 2, ld, 1, DROW, DBM, 1);
+    } else if (s_fp4) {
+        tmB0 = make_map_fp4(s0.get(), ld, R, DROW, bbox);
+        tmB1 = make_map_fp4(s1.get(), ld, R, DROW, bbox);
+    } else {
+        tmB0 = make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW, bbox, 1);
+        tmB1 = make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 1, DROW, bbox, 1);
+    }
     std::vector<float> s32(T);
     for (int64_t t = 0; t < T; ++t) s32[t] = (float)sched[t];
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
     VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
     DenseRunArgs a{};
     a.idesc_extra = (d->afmt << 7) | ((s_fp4 ? 5u : 0u) << 10);
-    a.a_tx_bytes = a_tx_bytes(d);
+    a.a_tx_bytes = mx ? (uint32_t)DA_BYTES : a_tx_bytes(d);
+    a.b_tx_bytes = (uint32_t)bbox * (mx ? DROW : (s_fp4 ? DROW / 2 : DROW));
     a.b_fp4 = s_fp4 ? 1 : 0;
     a.n = (int)n;
     a.R = (int)R;
     a.ld = (int)ld;
-    a.kblocks = (int)(ld / DROW);
+    a.kblocks = (int)(mx ? ceil_div(ld, 2 * DROW) : ld / DROW);  // mxf4: 256 K per stage
     a.m_tiles = (int)ceil_div(n, DBM);
     a.n_tiles = (int)ceil_div(R, bn);
     a.bn = bn;
@@ -1247,7 +1295,8 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                        CU_TENSOR_MAP_SWIZZLE_NONE);
         a.xm = 1;
     }
-    *loop_ms = run_loop(a, d->tmA8, tmB0, tmB1, false, cl, s, pair, &tmX, &tmM);
+    *loop_ms = run_loop(a, mx ? tmAmx : d->tmA8, tmB0, tmB1, false, cl, s, pair, &tmX, &tmM,
+                        mx);
     *launches += 2;
     if (trace_out) {
         DevBuf<double> tr(std::max<int64_t>(T, 1), s);
@@ -1309,6 +1358,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
     DenseRunArgs a{};
     a.a_tx_bytes = DA_BYTES;  // bf16 K planes: full boxes
+    a.b_tx_bytes = (uint32_t)bn * DROW;
     a.n = (int)n;
     a.R = (int)R;
     a.ld = (int)ld;
