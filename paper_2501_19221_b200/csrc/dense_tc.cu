@@ -350,6 +350,7 @@ struct DenseRunArgs {
     int b_fp4;               // B operand (spins) as packed E2M1 nibbles
     int xm;                  // PA steps: x/m staged by the loader warp (TMA) into smem
     uint32_t b_tx_bytes;     // transaction bytes of one B box (per plane) as delivered
+    uint64_t timeout_ns;     // bound on every in-kernel wait (VXQ_WAIT_TIMEOUT_S, default 10)
     // fused best-state tracking (improvement mode; needs qtrace, h = 0):
     long long* bestq;        // [R] lowest 2 sum K s s of s_0..s_{t-2} (LLONG_MAX initially)
     int8_t* best_s;          // [R][ld] best spins so far
@@ -507,7 +508,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         ptx::tma_prefetch_2d(&tmA, (kb + kPrefetch) * (DROW / TR::kElemBytes),
                                              mb * DBM);
                     long long c0 = a.stats ? clk() : 0;
-                    ptx::mbar_wait(empty + stage, ph ^ 1);
+                    ptx::mbar_wait(empty + stage, ph ^ 1, a.timeout_ns);
                     if (a.stats) st_empty += clk() - c0;
                     uint8_t* sa = smem + stage * SBYTES;
                     const uint32_t tx = a.a_tx_bytes + TR::kPlanes * a.b_tx_bytes;
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             while (ld_acquire_gpu(cnt) < (unsigned)a.m_tiles) {
                                 __nanosleep(64);
                                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
-                                if (tn - t0 > 10ull * 1000 * 1000 * 1000) __trap();
+                                if (tn - t0 > a.timeout_ns) __trap();
                             }
                         }
                         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -582,13 +583,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             const int acc = lt & 1;
             const uint32_t acc_ph = (lt >> 1) & 1;
             long long c0 = a.stats ? clk() : 0;
-            ptx::mbar_wait(tempty + acc, acc_ph ^ 1);
+            ptx::mbar_wait(tempty + acc, acc_ph ^ 1, a.timeout_ns);
             if (a.stats) mm_tempty += clk() - c0;
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + acc * ACC_COLS;
             for (int kb = 0; kb < a.kblocks; ++kb) {
                 c0 = a.stats ? clk() : 0;
-                ptx::mbar_wait(full + stage, ph);
+                ptx::mbar_wait(full + stage, ph, a.timeout_ns);
                 if (a.stats) mm_full += clk() - c0;
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
@@ -663,13 +664,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         while (ld_acquire_gpu(cnt) < (unsigned)a.m_tiles) {
                             __nanosleep(64);
                             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
-                            if (tn - t0 > 10ull * 1000 * 1000 * 1000) __trap();
+                            if (tn - t0 > a.timeout_ns) __trap();
                         }
                     }
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 for (int c = 0; c < nch; ++c) {
-                    ptx::mbar_wait(xempty + slot, ph ^ 1);
+                    ptx::mbar_wait(xempty + slot, ph ^ 1, a.timeout_ns);
                     uint8_t* xs = xm_smem + slot * XM_SLOT_BYTES;
                     ptx::mbar_arrive_expect_tx(xfull + slot, XM_SLOT_BYTES);
                     ptx::tma_load_2d_hint(xs, &tmX, xfull + slot, mb * DBM, nb * a.bn + c * 16,
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         float* __restrict__ xg = a.x;
         float* __restrict__ mg = a.m;
         int lt = 0, xm_tiles = 0;
-        long long ep_wait = 0, ep_busy = 0;
+        long long ep_wait = 0, ep_busy = 0, ep_xwait = 0;
         for (int g = wid0; g < num_tiles; g += wstride, ++lt) {
             int t, nb, mb;
             decode_tile(a, g, tps, mrows, t, nb, mb);
@@ -734,14 +735,14 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         while (ld_acquire_gpu(cnt) < (unsigned)a.m_tiles) {
                             __nanosleep(64);
                             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
-                            if (tn - t0 > 10ull * 1000 * 1000 * 1000) __trap();
+                            if (tn - t0 > a.timeout_ns) __trap();
                         }
                     }
                 }
                 load_chunk(half, xA, mA);
             }
             long long c0 = (a.stats && ep_tid == 0) ? clk() : 0;
-            ptx::mbar_wait(tfull + acc, acc_ph);
+            ptx::mbar_wait(tfull + acc, acc_ph, a.timeout_ns);
             long long c1 = (a.stats && ep_tid == 0) ? clk() : 0;
             if (a.stats && ep_tid == 0) ep_wait += c1 - c0;
             ptx::tc_fence_after();
@@ -836,13 +837,48 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         }
                     }
                 };
+                // fast path (PA, packed spins, no per-step trace, a full 16-replica chunk):
+                // no per-element range checks, incrementally bumped pointers, the spin byte of
+                // rows (i, i+1) always written by the even lane (padding rows stay 0)
+                auto process_fast = [&](int c, const float* xo, const float* mo) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_32x32b_x16(tbase + c * 16, v);
+                    const int r0 = nb * a.bn + c * 16;
+                    const int64_t base = (int64_t)r0 * a.ld + i;
+                    float* px = xg + base;
+                    float* pm = mg + base;
+                    uint8_t* pb = nxt + (base >> 1);
+                    const int64_t ld = a.ld, ldb = a.ld >> 1;
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const float f = O::mul(a.scale, __uint_as_float(v[jj]));
+                        const float grad = O::add(O::add(O::mul(st, xo[jj]), f), hi);
+                        const float mn = O::sub(O::mul(a.alpha, mo[jj]), O::mul(a.eta, grad));
+                        float xn = O::add(xo[jj], mn);
+                        xn = xn < -1.f ? -1.f : (xn > 1.f ? 1.f : xn);
+                        if (row_ok) {
+                            ptx::st_stream(px, xn, stream);
+                            ptx::st_stream(pm, mn, stream);
+                        }
+                        const uint32_t code = row_ok ? (xn >= 0.f ? FP4_P1 : FP4_M1) : 0u;
+                        const uint32_t hi4 = __shfl_xor_sync(0xffffffffu, code, 1);
+                        if (!(lane & 1)) *pb = (uint8_t)(code | (hi4 << 4));
+                        px += ld;
+                        pm += ld;
+                        pb += ldb;
+                    }
+                };
+                const bool fast_ok = KD == Kind::kFp8 && a.b_fp4 && !a.qtrace;
                 if (xm) {
                     if (tile_ok) {
 #pragma unroll 1
                         for (int c = half; c < nch; c += 2) {
                             const int seq = xm_tiles * nch + c;
                             const int slot = seq % XMS;
-                            ptx::mbar_wait(xfull + slot, (uint32_t)(seq / XMS) & 1u);
+                            const long long cx = (a.stats && ep_tid == 0) ? clk() : 0;
+                            ptx::mbar_wait(xfull + slot, (uint32_t)(seq / XMS) & 1u, a.timeout_ns);
+                            if (a.stats && ep_tid == 0) ep_xwait += clk() - cx;
                             const float* xs =
                                 reinterpret_cast<const float*>(xm_smem + slot * XM_SLOT_BYTES);
                             const float* ms = xs + 16 * DBM;
@@ -853,7 +889,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             }
                             __syncwarp();
                             if (lane == 0) ptx::mbar_arrive(xempty + slot);  // slot refillable
-                            process(c, xA, mA);
+                            if (fast_ok && nb * a.bn + c * 16 + 16 <= a.R) process_fast(c, xA, mA);
+                            else process(c, xA, mA);
                         }
                         ++xm_tiles;
                     }
@@ -920,6 +957,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         if (a.stats && ep_tid == 0) {
             atomicAdd(a.stats + 4, (unsigned long long)ep_wait);
             atomicAdd(a.stats + 5, (unsigned long long)ep_busy);
+            atomicAdd(a.stats + 8, (unsigned long long)ep_xwait);
         }
     }
     __syncthreads();
@@ -1015,6 +1053,10 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
         attrs[na].val.clusterDim.z = 1;
         ++na;
     }
+    // profiling knob: ncu cannot replay cluster + cooperative launches; with one CTA per SM
+    // (225 KB smem) and grid <= SM count every CTA is resident anyway
+    if (const char* e = getenv("VXQ_DENSE_NOCOOP"))
+        if (atoi(e) == 1) cooperative = false;
     if (cooperative) {
         // all CTAs must be co-resident (they wait on each other's tiles): one per SM
         attrs[na].id = cudaLaunchAttributeCooperative;
@@ -1024,6 +1066,9 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
     cfg.attrs = attrs;
     cfg.numAttrs = na;
     VXQ_REQUIRE(!a.xm || (tmX && tmM), "x/m staging needs their tensor maps");
+    a.timeout_ns = 10ull * 1000 * 1000 * 1000;
+    if (const char* e = getenv("VXQ_WAIT_TIMEOUT_S"))
+        a.timeout_ns = (uint64_t)std::max(1, atoi(e)) * 1000ull * 1000 * 1000;
     VXQ_CUDA(cudaLaunchKernelEx(&cfg, kern, tmA, tmB0, tmB1, tmX ? *tmX : tmA, tmM ? *tmM : tmA,
                                 a));
     VXQ_CHECK_LAUNCH();
@@ -1139,8 +1184,8 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     const char* want = getenv("VXQ_DENSE_STATS");
     DevBuf<unsigned long long> stats;
     if (want && want[0] == '1') {
-        stats = DevBuf<unsigned long long>(8, s);
-        VXQ_CUDA(cudaMemsetAsync(stats.get(), 0, 8 * sizeof(unsigned long long), s));
+        stats = DevBuf<unsigned long long>(9, s);
+        VXQ_CUDA(cudaMemsetAsync(stats.get(), 0, 9 * sizeof(unsigned long long), s));
         a.stats = stats.get();
     }
     cudaEvent_t e0, e1;
@@ -1163,15 +1208,16 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (a.stats) {
-        unsigned long long h[8];
+        unsigned long long h[9];
         VXQ_CUDA(cudaMemcpy(h, a.stats, sizeof(h), cudaMemcpyDeviceToHost));
         const double ctas = (double)std::min<int64_t>((int64_t)a.m_tiles * a.n_tiles * a.T,
                                                       num_sms());
         fprintf(stderr,
                 "[vxq dense stats] kernel %.0f cyc | per CTA: prod<-empty %.0f, prod<-dep %.0f, "
-                "mma<-full %.0f, mma<-tempty %.0f, epi<-tfull %.0f, epi busy %.0f | tiles %llu\n",
+                "mma<-full %.0f, mma<-tempty %.0f, epi<-tfull %.0f, epi busy %.0f (of which "
+                "<-x/m %.0f) | tiles %llu\n",
                 (double)h[7], h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas,
-                h[5] / ctas, h[6]);
+                h[5] / ctas, h[8] / ctas, h[6]);
     }
     return ms;
 }
@@ -1206,6 +1252,8 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     if (mx) {  // fewest <= 240-wide replica blocks, rounded up to 16 (pair N % 16 == 0)
         const int64_t blocks = ceil_div(R, (int64_t)kAccMx);
         bn = (int)std::min<int64_t>(kAccMx, ceil_div(ceil_div(R, blocks), 16) * 16);
+        if (const char* e = getenv("VXQ_DENSE_BN"))
+            bn = std::max(16, std::min((int)kAccMx, atoi(e) / 16 * 16));
     }
     // VXQ_DENSE_CLUSTER=2: B multicast across 2-CTA clusters (fewer cycles, same wall time
     // under the 1 kW power cap; cluster + cooperative launches cannot be profiled by ncu)
@@ -1216,7 +1264,7 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     // traffic per MMA; cfg2 +9 %); VXQ_DENSE_2CTA=0 -> one CTA per 128-row tile
     bool pair = true;
     if (const char* e = getenv("VXQ_DENSE_2CTA")) pair = atoi(e) == 1;
-    if (ceil_div(n, DBM) < 2 || bn % 32 != 0) pair = false;
+    if (ceil_div(n, DBM) < 2 || bn % 16 != 0) pair = false;  // each CTA: bn/2 rows of B
     if (pair || mx) cl = 1;
     const int bbox = pair ? bn / 2 : bn / cl;  // B rows (replicas) per TMA box
     CUtensorMap tmB0, tmB1, tmAmx;

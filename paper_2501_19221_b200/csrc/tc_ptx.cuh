@@ -48,15 +48,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.  The bound
+// (default 10 s) is raised for instrumented runs (ncu source counters slow kernels down).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity,
+                                          uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000) {
     const uint32_t addr = smem_u32(bar);
     if (mbar_try_wait(addr, parity)) return;
     uint64_t t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (!mbar_try_wait(addr, parity)) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 10ull * 1000 * 1000 * 1000) __trap();  // 10 s: pipeline bug
+        if (t - t0 > timeout_ns) __trap();  // pipeline bug
     }
 }
 

@@ -31,7 +31,7 @@ fi
 cap() {  # cap <name> <kernel regex> <profile_run args...>
   local name=$1 kern=$2; shift 2
   if timeout 300 python tools/profile_run.py "$@" > "$OUT/plain_$name.log" 2>&1; then
-    timeout 900 $NCU --set full --clock-control none --import-source on \
+    VXQ_WAIT_TIMEOUT_S=600 VXQ_DENSE_NOCOOP=1 timeout 900 $NCU --set full --clock-control none --import-source on \
       -k "regex:$kern" -s 2 -c 1 -o "$OUT/$name" -f python tools/profile_run.py "$@" \
       > "$OUT/ncu_$name.log" 2>&1
     echo "ncu $name rc=$?" | tee -a "$OUT/status.txt"
