@@ -74,6 +74,17 @@ __global__ void k_sa_energy0(const double* __restrict__ e, int64_t R, int64_t R_
     if (r < R_pad) E0[r] = r < R ? __dsub_rn(e[r], offset) : 0.0;
 }
 
+// F_j += v without waiting for the old value: in HBM/L2 a reduction performed at L2
+// (one IEEE round-to-nearest add, identical to the separate load + add + store); only this
+// lane ever touches its replica's fields, and its later loads of F_j are ordered after it
+template <typename T>
+__device__ __forceinline__ void red_add_global(T* p, T v) {
+    if constexpr (sizeof(T) == 8)
+        asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+    else
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 struct SaArgs {
     int64_t n, W, R_pad, sweeps;
     const int64_t* indptr;
@@ -184,6 +195,14 @@ __global__ void __launch_bounds__(32) k_sa_run(SaArgs a) {
                     }
                 };
                 int64_t e = e0;
+                if constexpr (!SMEM) {  // fire-and-forget reductions at L2
+                    for (; e < e1; ++e) {
+                        const int j = indices[e];
+                        const T v = O::mul(d2, data[e]);
+                        red_add_global(Fb + (int64_t)j * fs, v);
+                        patch(j, v);
+                    }
+                }
                 for (; e + kB <= e1; e += kB) {
                     int j[kB];
                     T v[kB], fv[kB];

@@ -403,6 +403,9 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // flop); the scale factors are all 1 (UE8M0 0x7F), written once into TMEM columns
 // kSfCol..511, and the two accumulators sit at columns 0 / kAccMx (bn <= 240).
 constexpr uint32_t kAccMx = 240, kSfCol = 480;
+#ifndef VXQ_PAIR_STAGES
+#define VXQ_PAIR_STAGES 5  // 5 x 32 KB operand stages + 4 x/m slots in 224 KB
+#endif
 
 template <Kind KD, int CL, bool PAIR = false, bool MX = false>
 __global__ void __launch_bounds__(DTHREADS, 1)
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     static_assert(!MX || (KD == Kind::kFp8 && CL == 1), "mxf4: fp8-kind layout, no multicast");
     constexpr uint32_t ACC_COLS = MX ? kAccMx : 256;
     constexpr int NCTA = PAIR ? 2 : CL;
-    constexpr int STAGES = PAIR ? 5 : TR::kStages;
+    constexpr int STAGES = PAIR ? VXQ_PAIR_STAGES : TR::kStages;
     constexpr int SBYTES = PAIR ? DA_BYTES + TR::kBnMax / 2 * DROW : stage_bytes<KD>();
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
     static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
