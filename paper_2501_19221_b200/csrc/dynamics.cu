@@ -162,13 +162,13 @@ inline Dests<P> one_dest(P* ptr) {
 // Rows [row0, row0 + nrows): x/m are indexed locally (row - row0), the CSR, h and the
 // sign-bit buffers by global row (a row-partitioned rank reads every row's spins).
 #ifndef VXQ_PA_MINB
-#define VXQ_PA_MINB 4
+#define VXQ_PA_MINB 6  // cfg4 894 -> 757 us/step vs 4 (more loads in flight per SM)
 #endif
 #ifndef VXQ_PA_LATE_XM
 #define VXQ_PA_LATE_XM 1
 #endif
 template <typename T, int V, int CPW, bool MULTI = false>
-__global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int64_t nrows, int64_t R_pad,
+__global__ void __launch_bounds__(256, MULTI ? 4 : VXQ_PA_MINB) k_pa_step(int64_t row0, int64_t nrows, int64_t R_pad,
                                                  Operator<T> op, const T* __restrict__ h,
                                                  T lam, T eta, T alpha, T* __restrict__ x,
                                                  T* __restrict__ m,
@@ -288,8 +288,11 @@ __global__ void __launch_bounds__(256, VXQ_PA_MINB) k_pa_step(int64_t row0, int6
 // base + 32 + l), issues all their spin-word gathers at once, then every row walks its
 // entries in ascending order through warp shuffles -- 3 memory round trips per RPW rows
 // instead of ~2 per neighbour, same sequential per-row sum as k_pa_step (bit-identical).
+#ifndef VXQ_COOP_MINB
+#define VXQ_COOP_MINB 5
+#endif
 template <typename T, int RPW, bool MULTI = false>
-__global__ void __launch_bounds__(256) k_pa_step_coop(int64_t row0, int64_t nrows,
+__global__ void __launch_bounds__(256, MULTI ? 4 : VXQ_COOP_MINB) k_pa_step_coop(int64_t row0, int64_t nrows,
                                                       Operator<T> op, const T* __restrict__ h,
                                                       T lam, T eta, T alpha, T* __restrict__ x,
                                                       T* __restrict__ m,
