@@ -47,7 +47,7 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
@@ -109,7 +109,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -164,7 +164,7 @@ def make_params(vxq, solver, R, T, seed):
     return vxq.SbmParams(steps=T, dt=0.05, replicas=R, seed=seed)
 
 
-def cpu_sample_plan(nnz: int, n: int, R: int, T: int, target_ops: float = 3e9):
+def cpu_sample_plan(nnz: int, n: int, R: int, T: int, target_ops: float = 1.5e10):
     """Bounded sample: (replicas, steps) so the C port does ~target_ops field terms."""
     per = max(nnz + n, 1)
     budget = max(target_ops / per, 1.0)
@@ -403,19 +403,22 @@ def run_ours(args):
     mean_step_kernel_ms = float(np.mean(loop_ms)) / T
     dbar = 2.0 * model.num_couplings / n
     if info.get("path") == "dense" and args.solver == "sbm":
-        # SBM on the tensor cores: q is split into 3 exact bf16 planes (kind::f16), so the
-        # kernel issues 3 x 2N flops per update at the bf16 rate; useful work is 2N
-        flops = 3 * 2.0 * n * R * n
+        # SBM on the tensor cores: q enters as 2 fp16 terms (default) or 3 exact bf16 terms
+        # (VXQ_SBM_PLANES=3), kind::f16, so the kernel issues planes x 2N flops per update at
+        # the bf16 rate; useful work is 2N
+        planes = 3 if os.environ.get("VXQ_SBM_PLANES") == "3" else 2
+        flops = planes * 2.0 * n * R * n
         achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
         tr, tsrc = measured_traffic("k_dense_run_sbm", args.config)
         roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
                 "frac": achieved / bf16, "traffic": tr, "traffic_unit": "bytes/step",
                 "traffic_source": tsrc,
-                "kernel": "k_dense_run<bf16x3>: tcgen05.mma kind::f16 over 3 exact bf16 q "
-                          "planes + fused symplectic SBM epilogue (persistent)",
+                "kernel": (f"k_dense_run<{'bf16x3' if planes == 3 else 'f16x2'}>: "
+                           f"tcgen05.mma kind::f16 over {planes} q planes + fused symplectic "
+                           "SBM epilogue (persistent)"),
                 "peak_note": f"measured bf16 sustained ({bf16} TF/s, {src})",
-                "flops_per_update_issued": 6.0 * n, "flops_per_update_useful": 2.0 * n,
-                "useful_frac_of_fp8_peak": achieved / 3.0 / (2.0 * bf16),
+                "flops_per_update_issued": planes * 2.0 * n, "flops_per_update_useful": 2.0 * n,
+                "useful_frac_of_fp8_peak": achieved / planes / (2.0 * bf16),
                 "units_per_launch": R * n, "mean_launch_ms": mean_step_kernel_ms}
     elif info.get("path") == "dense":
         # The default dense kernel issues tcgen05.mma kind::mxf4 (block-scaled E2M1, unit
@@ -514,12 +517,59 @@ def run_ours(args):
                 dist.all_reduce(tt, op=dist.ReduceOp.MIN)
                 tr = tt.cpu().numpy()
             step_ms = tot_ms / args.steps / T
-            hit = np.nonzero(tr <= target)[0]
-            ttt = {"target": target, "rule": "SK energy density E/N <= -0.70 (best replica "
-                                              "of the whole job)",
-                   "step": int(hit[0]) if hit.size else None,
-                   "ms": float(step_ms * (hit[0] + 1)) if hit.size else None,
-                   "best_trace_energy": float(np.nanmin(tr))}
+            if np.all(np.isnan(tr)):
+                ttt = {"target": target, "note": "no per-step energy trace on this path"}
+            else:
+                hit = np.nonzero(tr <= target)[0]
+                ttt = {"target": target, "rule": "SK energy density E/N <= -0.70 (best "
+                                                  "replica of the whole job)",
+                       "step": int(hit[0]) if hit.size else None,
+                       "ms": float(step_ms * (hit[0] + 1)) if hit.size else None,
+                       "best_trace_energy": float(np.nanmin(tr))}
+                # shorter annealing schedules (the reference's defaults except `steps`): the
+                # first step of each traced run that reaches the target, timed at that
+                # schedule's own measured per-step cost (one untimed warm-up + one timed solve)
+                sweep = []
+                for Ts in (200, 500, 700, 850):
+                    if Ts >= T:
+                        continue
+                    ps = make_params(vxq, args.solver, R, Ts, seed=0)
+                    trs = fn(model, ps, path=args.path, device=local, trace=True,
+                             replica_begin=rbegin).info["energy_trace"]
+                    if world > 1:
+                        tt = torch.tensor(np.nan_to_num(trs, nan=np.inf),
+                                          dtype=torch.float64, device="cuda")
+                        dist.all_reduce(tt, op=dist.ReduceOp.MIN)
+                        trs = tt.cpu().numpy()
+                    hs = np.nonzero(trs <= target)[0]
+                    ent = {"steps": Ts, "step": int(hs[0]) if hs.size else None,
+                           "best_trace_energy": float(np.nanmin(trs))}
+                    if hs.size:
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        with torch.cuda.stream(stream):
+                            for w in range(2):
+                                flush.fill_(w)
+                                e0.record(stream)
+                                run_device(args.solver, model, ps, states.data_ptr(),
+                                           energies.data_ptr(), order_ptr=order.data_ptr(),
+                                           stream=stream.cuda_stream,
+                                           precision=args.precision, path=args.path,
+                                           device=local, replica_begin=rbegin)
+                                e1.record(stream)
+                            torch.cuda.synchronize()
+                        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
+                                          device="cuda")
+                        if world > 1:
+                            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+                        ent["ms"] = float(ms.item()) / Ts * (hs[0] + 1)
+                    sweep.append(ent)
+                ttt["schedule_sweep"] = sweep
+                cands = [(e["ms"], e["steps"]) for e in sweep if e.get("ms") is not None]
+                if ttt["ms"] is not None:
+                    cands.append((ttt["ms"], T))
+                if cands:
+                    ttt["best_ms"], ttt["best_schedule_steps"] = min(cands)
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu and hasattr(model, "rows"):

@@ -24,6 +24,7 @@
 // or wave quantisation.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -44,7 +45,7 @@ constexpr int XM_SLOT_BYTES = 2 * 16 * DBM * 4;  // x and m of 16 replicas x 128
 constexpr int DSMEM = RING_BYTES + 1024 + 256;
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
-enum class Kind : int { kFp8 = 0, kBf16x3 = 1 };
+enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2 };
 
 template <Kind K>
 struct KindTraits;
@@ -62,6 +63,15 @@ struct KindTraits<Kind::kBf16x3> {
     // D=F32, A=B=BF16, K-major
     static constexpr uint32_t kIdescBase = (1u << 4) | (1u << 7) | (1u << 10);
 };
+// SBM default: q = h1 + h2 as two fp16 terms (11 + 11 significant bits, |q - h1 - h2| <=
+// 2^-23 |q| + 2^-25): 2 MMAs per k-block instead of 3, 4 B of B operand per q instead of 6
+template <>
+struct KindTraits<Kind::kF16x2> {
+    static constexpr int kPlanes = 2, kStages = 4, kBnMax = 128, kElemBytes = 2;
+    static constexpr int kKPerMma = 16;  // f16: K = 16 per tcgen05.mma (32 B)
+    // D=F32, A=B=F16 (format 0), K-major
+    static constexpr uint32_t kIdescBase = (1u << 4);
+};
 
 template <Kind K>
 constexpr int stage_bytes() {
@@ -69,6 +79,7 @@ constexpr int stage_bytes() {
 }
 static_assert(4 * stage_bytes<Kind::kFp8>() <= 192 * 1024, "fp8 ring");
 static_assert(3 * stage_bytes<Kind::kBf16x3>() <= 192 * 1024, "bf16 ring");
+static_assert(4 * stage_bytes<Kind::kF16x2>() <= 192 * 1024, "f16 ring");
 
 struct DenseOperand {
     int64_t n = 0, ld = 0;      // ld = n_pad (multiple of 128)
@@ -76,11 +87,13 @@ struct DenseOperand {
     uint8_t* K8 = nullptr;      // [ld][ld] fp8 E4M3 in {-1, 0, +1}, or (fp4) packed E2M1
                                 //   nibbles [ld][ld/2] (element 2k in the low nibble)
     uint32_t afmt = 0;          // A format in the f8f6f4 instruction descriptor (0 E4M3, 5 E2M1)
-    __nv_bfloat16* K16 = nullptr;  // [ld][ld] bf16 in {-1, 0, +1} (SBM, built lazily)
-    CUtensorMap tmA8, tmA16;
+    __nv_bfloat16* K16 = nullptr;  // [ld][ld] bf16 in {-1, 0, +1} (SBM bf16x3, built lazily)
+    __half* K16h = nullptr;        // [ld][ld] fp16 in {-1, 0, +1} (SBM f16x2, built lazily)
+    CUtensorMap tmA8, tmA16, tmA16h;
     ~DenseOperand() {
         if (K8) cudaFree(K8);
         if (K16) cudaFree(K16);
+        if (K16h) cudaFree(K16h);
     }
 };
 
@@ -171,7 +184,8 @@ constexpr uint32_t FP4_P1 = 0x2, FP4_M1 = 0xA;  // E2M1 +1 / -1
 __global__ void k_build_sign_matrix(int64_t n, int64_t ld, const int64_t* __restrict__ indptr,
                                     const int32_t* __restrict__ indices,
                                     const double* __restrict__ data, uint8_t* __restrict__ K8,
-                                    __nv_bfloat16* __restrict__ K16, uint32_t* __restrict__ K4) {
+                                    __nv_bfloat16* __restrict__ K16, uint32_t* __restrict__ K4,
+                                    __half* __restrict__ K16h) {
     int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -179,6 +193,7 @@ __global__ void k_build_sign_matrix(int64_t n, int64_t ld, const int64_t* __rest
         const bool pos = data[k] > 0;
         if (K8) K8[row * ld + indices[k]] = pos ? FP8_P1 : FP8_M1;
         if (K16) K16[row * ld + indices[k]] = __float2bfloat16_rn(pos ? 1.f : -1.f);
+        if (K16h) K16h[row * ld + indices[k]] = __float2half_rn(pos ? 1.f : -1.f);
         if (K4) {  // neighbours share bytes: OR the nibble into its 32-bit word
             const int64_t e = row * ld + indices[k];
             atomicOr(K4 + (e >> 3), (pos ? FP4_P1 : FP4_M1) << (4 * (e & 7)));
@@ -200,6 +215,12 @@ __device__ __forceinline__ void split3(float v, __nv_bfloat16& q1, __nv_bfloat16
     q2 = __float2bfloat16_rn(r1);
     const float r2 = __fsub_rn(r1, __bfloat162float(q2));
     q3 = __float2bfloat16_rn(r2);
+}
+
+// 2-way fp16 split: v ~= h1 + h2 (h1 = fp16(v), h2 = fp16(v - h1); v - h1 is exact in fp32)
+__device__ __forceinline__ void split2(float v, __half& h1, __half& h2) {
+    h1 = __float2half_rn(v);
+    h2 = __float2half_rn(__fsub_rn(v, __half2float(h1)));
 }
 
 // x0 ~ uniform(-1, 1) from replica stream r (same draws as k_init_pa), row-major [R][ld]
@@ -233,7 +254,7 @@ __global__ void k_init_pa_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, in
 // q0, p0 (stream r: n q-draws then n p-draws, as k_init_sbm) + the bf16 q-splits
 __global__ void k_init_sbm_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, int64_t rbegin,
                               double amp, float* __restrict__ q, float* __restrict__ p,
-                              __nv_bfloat16* __restrict__ planes) {
+                              void* __restrict__ planes_raw, int nplanes) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nq = (2 * n + 3) / 4;
     if (idx >= nq * R) return;
@@ -247,11 +268,20 @@ __global__ void k_init_sbm_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, i
         float v = (float)uniform_from_raw(o.v[w], lo, range);
         if (k < n) {
             q[r * ld + k] = v;
-            __nv_bfloat16 a, b, c;
-            split3(v, a, b, c);
-            planes[r * ld + k] = a;
-            planes[plane + r * ld + k] = b;
-            planes[2 * plane + r * ld + k] = c;
+            if (nplanes == 3) {
+                __nv_bfloat16* planes = reinterpret_cast<__nv_bfloat16*>(planes_raw);
+                __nv_bfloat16 a, b, c;
+                split3(v, a, b, c);
+                planes[r * ld + k] = a;
+                planes[plane + r * ld + k] = b;
+                planes[2 * plane + r * ld + k] = c;
+            } else {
+                __half* planes = reinterpret_cast<__half*>(planes_raw);
+                __half a, b;
+                split2(v, a, b);
+                planes[r * ld + k] = a;
+                planes[plane + r * ld + k] = b;
+            }
         } else if (k < 2 * n) {
             p[r * ld + (k - n)] = v;
         }
@@ -830,12 +860,20 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             if (ok) {
                                 ptx::st_stream(xg + off, qn, stream);
                                 ptx::st_stream(mg + off, pn, stream);
-                                __nv_bfloat16 q1, q2, q3;
-                                split3(qn, q1, q2, q3);
-                                __nv_bfloat16* pl = reinterpret_cast<__nv_bfloat16*>(nxt);
-                                pl[off] = q1;
-                                pl[a.plane_elems + off] = q2;
-                                pl[2 * a.plane_elems + off] = q3;
+                                if constexpr (KD == Kind::kF16x2) {
+                                    __half q1, q2;
+                                    split2(qn, q1, q2);
+                                    __half* pl = reinterpret_cast<__half*>(nxt);
+                                    pl[off] = q1;
+                                    pl[a.plane_elems + off] = q2;
+                                } else {
+                                    __nv_bfloat16 q1, q2, q3;
+                                    split3(qn, q1, q2, q3);
+                                    __nv_bfloat16* pl = reinterpret_cast<__nv_bfloat16*>(nxt);
+                                    pl[off] = q1;
+                                    pl[a.plane_elems + off] = q2;
+                                    pl[2 * a.plane_elems + off] = q3;
+                                }
                             }
                         }
                     }
@@ -1086,7 +1124,8 @@ bool dense_eligible(const Problem* p, int64_t R) {
 }
 
 // Lazily build the sign matrix K (fp8 for PA/energies, bf16 for SBM) and its TMA maps.
-DenseOperand* dense_operand(Problem* p, cudaStream_t s, bool need_bf16) {
+// need16: 0 none, 1 bf16 K (SBM bf16x3), 2 fp16 K (SBM f16x2)
+DenseOperand* dense_operand(Problem* p, cudaStream_t s, int need16) {
     std::lock_guard<std::mutex> g(p->mu);
     if (!p->uniform_magnitude)
         throw Error(VXQ_ERR_UNSUPPORTED, "dense tensor-core path needs uniform |J_ij|");
@@ -1102,6 +1141,7 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, bool need_bf16) {
         const int64_t ld = d->ld;
         uint8_t* k8 = nullptr;
         __nv_bfloat16* k16 = nullptr;
+        __half* k16h = nullptr;
         uint32_t* k4 = nullptr;
         if (!d->K8) {
             // default: K as packed E2M1 (51 MB at n = 10^4: stays L2-resident, -60 % DRAM
@@ -1122,16 +1162,23 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, bool need_bf16) {
                                    1);
             }
         }
-        if (need_bf16 && !d->K16) {
+        if (need16 == 2 && !d->K16h) {
+            VXQ_CUDA(cudaMalloc(&d->K16h, ld * ld * 2));
+            VXQ_CUDA(cudaMemsetAsync(d->K16h, 0, ld * ld * 2, s));
+            k16h = d->K16h;
+            d->tmA16h = make_map(d->K16h, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ld, ld, 1,
+                                 DROW / 2, DBM, 1);
+        }
+        if (need16 == 1 && !d->K16) {
             VXQ_CUDA(cudaMalloc(&d->K16, ld * ld * 2));
             VXQ_CUDA(cudaMemsetAsync(d->K16, 0, ld * ld * 2, s));
             k16 = d->K16;
             d->tmA16 = make_map(d->K16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, ld, 1, DROW / 2,
                                 DBM, 1);
         }
-        if (k8 || k16 || k4) {
+        if (k8 || k16 || k4 || k16h) {
             k_build_sign_matrix<<<(unsigned)ceil_div(p->n * 32, TB), TB, 0, s>>>(
-                p->n, ld, p->indptr, p->indices, p->data64, k8, k16, k4);
+                p->n, ld, p->indptr, p->indices, p->data64, k8, k16, k4, k16h);
             VXQ_CHECK_LAUNCH();
             VXQ_CUDA(cudaStreamSynchronize(s));
         }
@@ -1181,7 +1228,7 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
 }
 
 static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap& tb0,
-                       const CUtensorMap& tb1, bool bf16, int cl, cudaStream_t s,
+                       const CUtensorMap& tb1, int planes16, int cl, cudaStream_t s,
                        bool pair = false, const CUtensorMap* tmX = nullptr,
                        const CUtensorMap* tmM = nullptr, bool mx = false) {
     const char* want = getenv("VXQ_DENSE_STATS");
@@ -1196,7 +1243,8 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     VXQ_CUDA(cudaEventCreate(&e1));
     VXQ_CUDA(cudaEventRecord(e0, s));
     if (a.T > 0) {
-        if (bf16) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        if (planes16 == 3) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (planes16 == 2) launch_run<Kind::kF16x2, 1>(tmA, tb0, tb1, a, a.T, s, true);
         else if (pair && mx)
             launch_run<Kind::kFp8, 1, true, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
         else if (mx) launch_run<Kind::kFp8, 1, false, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
@@ -1233,7 +1281,7 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                    int64_t rbegin, float* x_il, float* m_il, uint32_t* sb, long long* q2,
                    cudaStream_t s, double* loop_ms, int64_t* launches, double* trace_out,
                    bool trace_on_dev, uint32_t* sb_best) {
-    DenseOperand* d = dense_operand(p, s, false);
+    DenseOperand* d = dense_operand(p, s, 0);
     const int64_t n = p->n, ld = d->ld, T = (int64_t)sched.size();
     DevBuf<float> x(R * ld, s), m(R * ld, s);
     // spins (the B operand): packed E2M1 nibbles with a packed-fp4 K (VXQ_DENSE_FP4S=0: fp8)
@@ -1382,27 +1430,33 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     VXQ_CUDA(cudaStreamSynchronize(s));
 }
 
-// Run the T-step SBM loop (B = -A, g = -h) on the tensor cores with bf16x3 q-splits.
+// Run the T-step SBM loop (B = -A, g = -h) on the tensor cores.  q enters the MMA as two
+// fp16 terms (default) or three exact bf16 terms (VXQ_SBM_PLANES=3, and always when |q| may
+// leave the fp16 range).
 void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                     const std::vector<double>& a_sched, double dt, double a0, double c0,
                     double q_cap, double amp, uint64_t seed, int64_t rbegin, float* q_il,
                     float* p_il, uint32_t* sb, long long* q2, cudaStream_t s, double* loop_ms,
                     int64_t* launches) {
-    DenseOperand* d = dense_operand(p, s, true);
+    int planes = 2;
+    if (const char* e = getenv("VXQ_SBM_PLANES")) planes = atoi(e) == 3 ? 3 : 2;
+    if (!(std::max(q_cap, amp) <= 16384.0)) planes = 3;  // fp16 max is 65504
+    DenseOperand* d = dense_operand(p, s, planes == 3 ? 1 : 2);
     const int64_t n = p->n, ld = d->ld, T = (int64_t)a_sched.size();
     const int64_t plane = R * ld;
     DevBuf<float> q(R * ld, s), pm(R * ld, s);
-    DevBuf<__nv_bfloat16> b0(3 * plane, s), b1(3 * plane, s);
-    VXQ_CUDA(cudaMemsetAsync(b0.get(), 0, 3 * plane * 2, s));
-    VXQ_CUDA(cudaMemsetAsync(b1.get(), 0, 3 * plane * 2, s));
+    DevBuf<uint16_t> b0(planes * plane, s), b1(planes * plane, s);
+    VXQ_CUDA(cudaMemsetAsync(b0.get(), 0, planes * plane * 2, s));
+    VXQ_CUDA(cudaMemsetAsync(b1.get(), 0, planes * plane * 2, s));
     k_init_sbm_rm<<<nblk(((2 * n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, amp,
-                                                            q.get(), pm.get(), b0.get());
+                                                            q.get(), pm.get(), b0.get(), planes);
     VXQ_CHECK_LAUNCH();
-    const int bn = choose_bn(n, R, 3, KindTraits<Kind::kBf16x3>::kBnMax);
-    CUtensorMap tmB0 = make_map(b0.get(), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, R, 3,
-                                DROW / 2, bn, 3);
-    CUtensorMap tmB1 = make_map(b1.get(), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, R, 3,
-                                DROW / 2, bn, 3);
+    const int bn = planes == 3 ? choose_bn(n, R, 3, KindTraits<Kind::kBf16x3>::kBnMax)
+                               : choose_bn(n, R, 2, KindTraits<Kind::kF16x2>::kBnMax);
+    const CUtensorMapDataType bt =
+        planes == 3 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUtensorMap tmB0 = make_map(b0.get(), bt, 2, ld, R, planes, DROW / 2, bn, planes);
+    CUtensorMap tmB1 = make_map(b1.get(), bt, 2, ld, R, planes, DROW / 2, bn, planes);
     std::vector<float> s32(T);
     for (int64_t t = 0; t < T; ++t) s32[t] = (float)a_sched[t];
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
@@ -1436,7 +1490,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
-    *loop_ms = run_loop(a, d->tmA16, tmB0, tmB1, true, 1, s);
+    *loop_ms = run_loop(a, planes == 3 ? d->tmA16 : d->tmA16h, tmB0, tmB1, planes, 1, s);
     *launches += 2;
     if (q2) energy_pass(d, q.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(q.get(), n, R, ld, R_pad, V, q_il);

@@ -288,10 +288,13 @@ def test_dense_tensor_core_path_bitexact_with_emulation(n, R):
     assert np.array_equal(r.energies, O.energies_exact(m, r.states))
 
 
+@pytest.mark.parametrize("planes", ["2", "3"])
 @pytest.mark.parametrize("n,R", [(1000, 256), (700, 200)])
-def test_dense_sbm_tensor_core_short_horizon(n, R):
-    """SBM on the tensor cores (bf16x3 exact q-splits, f32 accumulation) tracks the fp64
-    restatement of the reference loop within the fp32 tolerance for t <= 30."""
+def test_dense_sbm_tensor_core_short_horizon(n, R, planes, monkeypatch):
+    """SBM on the tensor cores (q as two fp16 terms -- the default -- or three exact bf16
+    terms, f32 accumulation) tracks the fp64 restatement of the reference loop within the
+    fp32 tolerance for t <= 30."""
+    monkeypatch.setenv("VXQ_SBM_PLANES", planes)
     m = sk_model(n, 6)
     c0 = 0.02
     r = vxq.run_sbm(m, vxq.SbmParams(steps=30, dt=0.05, replicas=R, seed=2, c0=c0),
