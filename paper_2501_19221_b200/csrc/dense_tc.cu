@@ -445,12 +445,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ CUtensorMap tmM, DenseRunArgs a) {
     using TR = KindTraits<KD>;
-    static_assert(!PAIR || (KD == Kind::kFp8 && CL == 1), "pair MMA: f8f6f4, no B multicast");
+    static_assert(!PAIR || (KD != Kind::kBf16x3 && CL == 1), "pair MMA: f8f6f4 / f16x2, no B multicast");
     static_assert(!MX || (KD == Kind::kFp8 && CL == 1), "mxf4: fp8-kind layout, no multicast");
     constexpr uint32_t ACC_COLS = MX ? kAccMx : 256;
     constexpr int NCTA = PAIR ? 2 : CL;
-    constexpr int STAGES = PAIR ? VXQ_PAIR_STAGES : TR::kStages;
-    constexpr int SBYTES = PAIR ? DA_BYTES + TR::kBnMax / 2 * DROW : stage_bytes<KD>();
+    // pair: each CTA stages its 128 A rows and <= 128 B rows per plane
+    constexpr int STAGES = PAIR ? (TR::kPlanes == 1 ? VXQ_PAIR_STAGES : 4) : TR::kStages;
+    constexpr int SBYTES = PAIR ? DA_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
     static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
     static_assert(KD != Kind::kFp8 || XMS >= 2, "x/m staging slots");
@@ -572,7 +573,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                         if (a.stats) st_dep += clk() - c1;
                     }
-                    if constexpr (PAIR) {
+                    if constexpr (PAIR && TR::kPlanes > 1) {
+                        ptx::tma_load_3d_2sm(sa + DA_BYTES, tmB, full + stage, kcol,
+                                             nb * a.bn + crank * (a.bn / 2), 0, keep);
+                    } else if constexpr (PAIR) {
                         ptx::tma_load_2d_2sm(sa + DA_BYTES, tmB, full + stage, kcol,
                                              nb * a.bn + crank * (a.bn / 2), keep);
                     } else if constexpr (CL > 1) {
@@ -643,6 +647,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                                 ptx::mma_mxf4(d, da + 2 * k, db + 2 * k, idesc,
                                               tmem_base + kSfCol, tmem_base + kSfCol + 16,
                                               accum);
+                            else if constexpr (PAIR && KD == Kind::kF16x2)
+                                ptx::mma2_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
                             else if constexpr (PAIR)
                                 ptx::mma2_f8f6f4(d, da + 2 * k, db + 2 * k, idesc, accum);
                             else if constexpr (KD == Kind::kFp8)
@@ -1244,6 +1250,8 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     VXQ_CUDA(cudaEventRecord(e0, s));
     if (a.T > 0) {
         if (planes16 == 3) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (planes16 == 2 && pair)
+            launch_run<Kind::kF16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 2) launch_run<Kind::kF16x2, 1>(tmA, tb0, tb1, a, a.T, s, true);
         else if (pair && mx)
             launch_run<Kind::kFp8, 1, true, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
@@ -1451,19 +1459,30 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     k_init_sbm_rm<<<nblk(((2 * n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, amp,
                                                             q.get(), pm.get(), b0.get(), planes);
     VXQ_CHECK_LAUNCH();
-    const int bn = planes == 3 ? choose_bn(n, R, 3, KindTraits<Kind::kBf16x3>::kBnMax)
-                               : choose_bn(n, R, 2, KindTraits<Kind::kF16x2>::kBnMax);
+    // f16x2 on tcgen05 CTA pairs (M = 256, bn <= 256, each CTA stages its 128 K rows and
+    // bn/2 replicas of both planes): half the replica blocks -> half the K re-reads per step
+    bool pair = planes == 2 && ceil_div(n, DBM) >= 2;
+    if (const char* e = getenv("VXQ_DENSE_2CTA")) pair = pair && atoi(e) == 1;
+    int bn;
+    if (pair) {
+        const int64_t blocks = ceil_div(R, (int64_t)256);
+        bn = (int)std::min<int64_t>(256, ceil_div(ceil_div(R, blocks), 16) * 16);
+    } else {
+        bn = planes == 3 ? choose_bn(n, R, 3, KindTraits<Kind::kBf16x3>::kBnMax)
+                         : choose_bn(n, R, 2, KindTraits<Kind::kF16x2>::kBnMax);
+    }
+    const int bbox = pair ? bn / 2 : bn;
     const CUtensorMapDataType bt =
         planes == 3 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    CUtensorMap tmB0 = make_map(b0.get(), bt, 2, ld, R, planes, DROW / 2, bn, planes);
-    CUtensorMap tmB1 = make_map(b1.get(), bt, 2, ld, R, planes, DROW / 2, bn, planes);
+    CUtensorMap tmB0 = make_map(b0.get(), bt, 2, ld, R, planes, DROW / 2, bbox, planes);
+    CUtensorMap tmB1 = make_map(b1.get(), bt, 2, ld, R, planes, DROW / 2, bbox, planes);
     std::vector<float> s32(T);
     for (int64_t t = 0; t < T; ++t) s32[t] = (float)a_sched[t];
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
     VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
     DenseRunArgs a{};
-    a.a_tx_bytes = DA_BYTES;  // bf16 K planes: full boxes
-    a.b_tx_bytes = (uint32_t)bn * DROW;
+    a.a_tx_bytes = DA_BYTES;  // 16-bit K: full boxes
+    a.b_tx_bytes = (uint32_t)bbox * DROW;
     a.n = (int)n;
     a.R = (int)R;
     a.ld = (int)ld;
@@ -1490,7 +1509,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
-    *loop_ms = run_loop(a, planes == 3 ? d->tmA16 : d->tmA16h, tmB0, tmB1, planes, 1, s);
+    *loop_ms = run_loop(a, planes == 3 ? d->tmA16 : d->tmA16h, tmB0, tmB1, planes, 1, s, pair);
     *launches += 2;
     if (q2) energy_pass(d, q.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(q.get(), n, R, ld, R_pad, V, q_il);
