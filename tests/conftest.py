@@ -11,6 +11,7 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "reference_vectors.npz")
 GOLDEN_SA = os.path.join(ROOT, "tests", "golden", "reference_sa.npz")
+GOLDEN_ACC = os.path.join(ROOT, "tests", "golden", "reference_acceptance.npz")
 
 
 def pytest_configure(config):
@@ -25,6 +26,11 @@ def golden():
 @pytest.fixture(scope="session")
 def golden_sa():
     return dict(np.load(GOLDEN_SA))
+
+
+@pytest.fixture(scope="session")
+def golden_acc():
+    return dict(np.load(GOLDEN_ACC))
 
 
 def has_gpu() -> bool:
