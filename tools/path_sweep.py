@@ -1,11 +1,12 @@
-"""Small solves over every kernel path, for compute-sanitizer (memcheck / racecheck /
-synccheck / initcheck) on the B200:
+"""Small solves over every kernel path, one process per case if wanted (compute-sanitizer
+is closed on this GPU pool, so bad accesses are hunted with small cases, the kernels' own
+bounds checks and the CPU oracle):
 
-    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize.py --case pa_sparse
-    python tools/sanitize.py --list
+    python tools/path_sweep.py                 # all cases
+    python tools/path_sweep.py --case pa_dense
+    python tools/path_sweep.py --list
 
-Each case checks its result against the oracle where that is cheap, so a sanitizer run
-that perturbs timing still has to produce the right answer.
+Each case checks its energies against the oracle's exact sums.
 """
 
 import argparse
