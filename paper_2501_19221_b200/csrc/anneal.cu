@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(32) k_sa_run(SaArgs a) {
     const double inv53 = 1.0 / 9007199254740992.0;
     for (int64_t s = 0; s < a.sweeps; ++s) {
         const double Tt = a.temps[s];
+        const double invT = 1.0 / Tt;
         // pf[d] = field of spin i + d (prefetched kPf spins ahead; patched when a flip of
         // spin i updates one of them)
         T pf[kPf];
@@ -168,13 +169,28 @@ __global__ void __launch_bounds__(32) k_sa_run(SaArgs a) {
             ++k;
             const bool up = (word >> lane) & 1u;
             const double dE = up ? -2.0 * (double)f : 2.0 * (double)f;  // -2 s F (exact)
-            const double x = __ddiv_rn(-dE, Tt);
-            bool acc;
-            if (x >= 0.0) {
-                acc = true;  // exp(min(x, 0)) = 1 > U
-            } else {
+            bool acc = dE <= 0.0;  // x = -dE / T >= 0: exp(min(x, 0)) = 1 > U; NaN: never
+            if (dE > 0.0) {
+                // U < exp(x), x = RN(-dE / T).  Decided without the fp64 divide and exp
+                // unless U falls within 1e-4 (relative) of a fast estimate: |ef / exp(x) - 1|
+                // <= ~1.1e-5 for x >= -80 (fp32 cast of x 4.8e-6, __expf <= 94 ulp of fp32,
+                // x ~ -dE * (1/T) 3e-16); below -80, exp(x) < 2^-115 < every U > 0
                 const double u = __dmul_rn((double)(raw >> 11), inv53);
-                acc = u < exp(x);  // NaN x: never (numpy: U < NaN is False)
+                const double xa = -dE * invT;
+                int verdict = -1;  // 1 accept, 0 reject, -1 undecided
+                if (xa >= -80.0) {
+                    const float ef = __expf((float)xa);
+                    if (u < (double)(ef * 0.9999f)) verdict = 1;
+                    else if (u > (double)(ef * 1.0001f)) verdict = 0;
+                } else if (u > 0.0) {
+                    verdict = 0;
+                }
+                if (verdict < 0) {
+                    const double x = __ddiv_rn(-dE, Tt);
+                    acc = x >= 0.0 ? true : u < exp(x);
+                } else {
+                    acc = verdict == 1;
+                }
             }
             const uint32_t am = __ballot_sync(0xffffffffu, acc);
             if (am == 0u) continue;
