@@ -17,6 +17,8 @@ from .errors import QubokitError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libvxq.so")
+if os.environ.get("VXQ_LIB"):  # A/B experiments: a variant build (build.py --variant)
+    LIB_PATH = os.environ["VXQ_LIB"]
 
 VXQ_OK, VXQ_ERR_INVALID, VXQ_ERR_OOM, VXQ_ERR_CUDA, VXQ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 FP32, FP64 = 0, 1

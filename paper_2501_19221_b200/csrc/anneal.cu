@@ -32,7 +32,10 @@ namespace vxq {
 namespace {
 
 constexpr int kSaSmemMax = 200 * 1024;
-constexpr int kPf = 4;  // field prefetch depth (spins ahead)
+#ifndef VXQ_SA_PF
+#define VXQ_SA_PF 8
+#endif
+constexpr int kPf = VXQ_SA_PF;  // field / spin-word prefetch depth (spins ahead)
 constexpr int kB = 8;   // neighbour updates per batch
 
 __global__ void k_sa_init_spins(int64_t n, int64_t W, int64_t R_pad, uint64_t seed,
@@ -152,14 +155,20 @@ __global__ void __launch_bounds__(32) k_sa_run(SaArgs a) {
         T pf[kPf];
 #pragma unroll
         for (int d = 0; d < kPf; ++d) pf[d] = d < n ? Fb[d * fs] : (T)0;
-        uint32_t wn = sbw[0];
+        // wq[d] = spin word of spin i + d: a spin's word changes only when that spin is
+        // visited, so words ahead of i are final for this sweep
+        uint32_t wq[kPf];
+#pragma unroll
+        for (int d = 0; d < kPf; ++d) wq[d] = d < n ? sbw[d * ws] : 0u;
         for (int64_t i = 0; i < n; ++i) {
             const T f = pf[0];
 #pragma unroll
             for (int d = 0; d + 1 < kPf; ++d) pf[d] = pf[d + 1];
             pf[kPf - 1] = i + kPf < n ? Fb[(i + kPf) * fs] : (T)0;
-            const uint32_t word = wn;
-            if (i + 1 < n) wn = sbw[(i + 1) * ws];
+            const uint32_t word = wq[0];
+#pragma unroll
+            for (int d = 0; d + 1 < kPf; ++d) wq[d] = wq[d + 1];
+            wq[kPf - 1] = i + kPf < n ? sbw[(i + kPf) * ws] : 0u;
             const uint64_t q = k >> 2;
             if (q != kb) {
                 blk = philox4x64_10(q + 1, 0, rg, 0, a.seed, 0);
