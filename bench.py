@@ -498,6 +498,7 @@ def run_ours(args):
             dist.all_reduce(wt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * R * n * T * len(walls) / float(wt.item()),
                "unit": "rv-updates/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "walls_ms": [round(1e3 * w, 2) for w in walls],
                "best_energy": float(ss.best.energy)}
 
     # time-to-target (BASELINE metric): one traced solve outside the timed region; the
@@ -530,7 +531,7 @@ def run_ours(args):
                 # first step of each traced run that reaches the target, timed at that
                 # schedule's own measured per-step cost (one untimed warm-up + one timed solve)
                 sweep = []
-                for Ts in (200, 500, 700, 850):
+                for Ts in (500, 550, 600, 650, 700, 850):
                     if Ts >= T:
                         continue
                     ps = make_params(vxq, args.solver, R, Ts, seed=0)
