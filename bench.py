@@ -85,6 +85,15 @@ def measured_traffic(kernel: str, config: str):
     return None, None
 
 
+def _uniform(model, device) -> bool:
+    """All |J_ij| equal (the SK-family tensor path) -- else the general dense-J kernel."""
+    from paper_2501_19221_b200.device import get_problem
+    try:
+        return get_problem(model, device).info()["uniform_magnitude"]
+    except Exception:
+        return True
+
+
 def bytes_per_update(solver: str, dbar: float, R: int) -> float:
     """algorithmic bytes per replica-variable update (fp32 state, int32+fp32 CSR)."""
     amort = (8.0 * dbar + 4.0) / R
@@ -419,6 +428,20 @@ def run_ours(args):
                 "peak_note": f"measured bf16 sustained ({bf16} TF/s, {src})",
                 "flops_per_update_issued": planes * 2.0 * n, "flops_per_update_useful": 2.0 * n,
                 "useful_frac_of_fp8_peak": achieved / planes / (2.0 * bf16),
+                "units_per_launch": R * n, "mean_launch_ms": mean_step_kernel_ms}
+    elif info.get("path") == "dense" and not _uniform(model, local):
+        # general (non-uniform) dense J: J as two fp16 planes (kind::f16 on CTA pairs), so the
+        # kernel issues 2 x 2N flops per update at the bf16 rate; useful work is 2N
+        flops = 2 * 2.0 * n * R * n
+        achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
+        tr, tsrc = measured_traffic("k_dense_run_general", args.config)
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                "frac": achieved / bf16, "traffic": tr, "traffic_unit": "bytes/step",
+                "traffic_source": tsrc,
+                "kernel": "k_dense_run<J16x2>: tcgen05.mma.cta_group::2 kind::f16, J as two "
+                          "fp16 planes x fp16 +-1 spins + fused PA epilogue (persistent)",
+                "peak_note": f"measured bf16 sustained ({bf16} TF/s, {src})",
+                "flops_per_update_issued": 4.0 * n, "flops_per_update_useful": 2.0 * n,
                 "units_per_launch": R * n, "mean_launch_ms": mean_step_kernel_ms}
     elif info.get("path") == "dense":
         # The default dense kernel issues tcgen05.mma kind::mxf4 (block-scaled E2M1, unit

@@ -45,20 +45,20 @@ constexpr int XM_SLOT_BYTES = 2 * 16 * DBM * 4;  // x and m of 16 replicas x 128
 constexpr int DSMEM = RING_BYTES + 1024 + 256;
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
-enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2 };
+enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3 };
 
 template <Kind K>
 struct KindTraits;
 template <>
 struct KindTraits<Kind::kFp8> {
-    static constexpr int kPlanes = 1, kStages = 4, kBnMax = 256, kElemBytes = 1;
+    static constexpr int kPlanes = 1, kAPlanes = 1, kStages = 4, kBnMax = 256, kElemBytes = 1;
     static constexpr int kKPerMma = 32;  // fp8: K = 32 per tcgen05.mma (32 B)
     // D=F32, A=B=E4M3, K-major
     static constexpr uint32_t kIdescBase = (1u << 4);
 };
 template <>
 struct KindTraits<Kind::kBf16x3> {
-    static constexpr int kPlanes = 3, kStages = 3, kBnMax = 128, kElemBytes = 2;
+    static constexpr int kPlanes = 3, kAPlanes = 1, kStages = 3, kBnMax = 128, kElemBytes = 2;
     static constexpr int kKPerMma = 16;  // bf16: K = 16 per tcgen05.mma (32 B)
     // D=F32, A=B=BF16, K-major
     static constexpr uint32_t kIdescBase = (1u << 4) | (1u << 7) | (1u << 10);
@@ -67,15 +67,24 @@ struct KindTraits<Kind::kBf16x3> {
 // 2^-23 |q| + 2^-25): 2 MMAs per k-block instead of 3, 4 B of B operand per q instead of 6
 template <>
 struct KindTraits<Kind::kF16x2> {
-    static constexpr int kPlanes = 2, kStages = 4, kBnMax = 128, kElemBytes = 2;
+    static constexpr int kPlanes = 2, kAPlanes = 1, kStages = 4, kBnMax = 128, kElemBytes = 2;
     static constexpr int kKPerMma = 16;  // f16: K = 16 per tcgen05.mma (32 B)
     // D=F32, A=B=F16 (format 0), K-major
+    static constexpr uint32_t kIdescBase = (1u << 4);
+};
+// PA with general (non-uniform) dense J: J (scaled by 2^k) as two fp16 A planes
+// J1 = fp16(J), J2 = fp16(J - J1) against the spins as fp16 +-1 (products exact, fp32
+// accumulation): 2 MMAs per k-block, CTA pairs only
+template <>
+struct KindTraits<Kind::kJ16x2> {
+    static constexpr int kPlanes = 1, kAPlanes = 2, kStages = 3, kBnMax = 128, kElemBytes = 2;
+    static constexpr int kKPerMma = 16;
     static constexpr uint32_t kIdescBase = (1u << 4);
 };
 
 template <Kind K>
 constexpr int stage_bytes() {
-    return DA_BYTES + KindTraits<K>::kPlanes * KindTraits<K>::kBnMax * DROW;
+    return DA_BYTES * KindTraits<K>::kAPlanes + KindTraits<K>::kPlanes * KindTraits<K>::kBnMax * DROW;
 }
 static_assert(4 * stage_bytes<Kind::kFp8>() <= 192 * 1024, "fp8 ring");
 static_assert(3 * stage_bytes<Kind::kBf16x3>() <= 192 * 1024, "bf16 ring");
@@ -89,11 +98,15 @@ struct DenseOperand {
     uint32_t afmt = 0;          // A format in the f8f6f4 instruction descriptor (0 E4M3, 5 E2M1)
     __nv_bfloat16* K16 = nullptr;  // [ld][ld] bf16 in {-1, 0, +1} (SBM bf16x3, built lazily)
     __half* K16h = nullptr;        // [ld][ld] fp16 in {-1, 0, +1} (SBM f16x2, built lazily)
+    __half* J16 = nullptr;         // [2][ld][ld] fp16 planes of 2^e J (general dense J)
+    float jscale_inv = 0.f;        // 2^-e
+    CUtensorMap tmJ;
     CUtensorMap tmA8, tmA16, tmA16h;
     ~DenseOperand() {
         if (K8) cudaFree(K8);
         if (K16) cudaFree(K16);
         if (K16h) cudaFree(K16h);
+        if (J16) cudaFree(J16);
     }
 };
 
@@ -201,6 +214,23 @@ __global__ void k_build_sign_matrix(int64_t n, int64_t ld, const int64_t* __rest
     }
 }
 
+// general dense J: 2^e J split into two fp16 planes (P[0] = fp16(v), P[1] = fp16(v - P[0]))
+__global__ void k_build_j_planes(int64_t n, int64_t ld, const int64_t* __restrict__ indptr,
+                                 const int32_t* __restrict__ indices,
+                                 const float* __restrict__ data32, float scale,
+                                 __half* __restrict__ P) {
+    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32) {
+        const float v = data32[k] * scale;  // power of two: exact
+        const __half h1 = __float2half_rn(v);
+        const __half h2 = __float2half_rn(__fsub_rn(v, __half2float(h1)));
+        P[row * ld + indices[k]] = h1;
+        P[ld * ld + row * ld + indices[k]] = h2;
+    }
+}
+
 __device__ __forceinline__ int64_t pos_interleaved(int64_t r, int V) {
     int64_t ch = 32 * V;
     int64_t c = r / ch, rem = r % ch;
@@ -226,7 +256,8 @@ __device__ __forceinline__ void split2(float v, __half& h1, __half& h2) {
 // x0 ~ uniform(-1, 1) from replica stream r (same draws as k_init_pa), row-major [R][ld]
 __global__ void k_init_pa_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, int64_t rbegin,
                              float* __restrict__ x, float* __restrict__ m,
-                             uint8_t* __restrict__ s, bool s_fp4) {
+                             uint8_t* __restrict__ s, int s_fmt) {  // 0 fp8, 1 fp4, 2 fp16
+    const bool s_fp4 = s_fmt == 1;
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nq = (n + 3) / 4;
     if (idx >= nq * R) return;
@@ -241,6 +272,8 @@ __global__ void k_init_pa_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, in
             x[r * ld + i] = v;
             m[r * ld + i] = 0.f;
             if (s_fp4) code[w] = v >= 0.f ? FP4_P1 : FP4_M1;
+            else if (s_fmt == 2)
+                reinterpret_cast<uint16_t*>(s)[r * ld + i] = v >= 0.f ? 0x3C00 : 0xBC00;
             else s[r * ld + i] = v >= 0.f ? FP8_P1 : FP8_M1;
         }
     }
@@ -446,15 +479,19 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const __grid_constant__ CUtensorMap tmM, DenseRunArgs a) {
     using TR = KindTraits<KD>;
     static_assert(!PAIR || (KD != Kind::kBf16x3 && CL == 1), "pair MMA: f8f6f4 / f16x2, no B multicast");
+    static_assert(KD != Kind::kJ16x2 || PAIR, "general-J planes: CTA pairs only");
+    constexpr int A_BYTES = DA_BYTES * TR::kAPlanes;  // A planes of one stage, back to back
     static_assert(!MX || (KD == Kind::kFp8 && CL == 1), "mxf4: fp8-kind layout, no multicast");
     constexpr uint32_t ACC_COLS = MX ? kAccMx : 256;
     constexpr int NCTA = PAIR ? 2 : CL;
     // pair: each CTA stages its 128 A rows and <= 128 B rows per plane
-    constexpr int STAGES = PAIR ? (TR::kPlanes == 1 ? VXQ_PAIR_STAGES : 4) : TR::kStages;
-    constexpr int SBYTES = PAIR ? DA_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
+    constexpr int STAGES =
+        PAIR ? ((TR::kPlanes == 1 && TR::kAPlanes == 1) ? VXQ_PAIR_STAGES : 4) : TR::kStages;
+    constexpr int SBYTES = PAIR ? A_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
     static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
-    static_assert(KD != Kind::kFp8 || XMS >= 2, "x/m staging slots");
+    static_assert((KD != Kind::kFp8 && KD != Kind::kJ16x2) || XMS >= 2, "x/m staging slots");
+    constexpr bool PA_KIND = KD == Kind::kFp8 || KD == Kind::kJ16x2;
     extern __shared__ uint8_t smem_raw[];
     __shared__ int s_last;  // fused tracking: this tile completed its step's decisions
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -535,12 +572,21 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 // A (the coupling panel) never depends on the dynamics: keep kPrefetch
                 // k-blocks of it on their way into L2 ahead of the smem loads
                 constexpr int kPrefetch = 8;
-                for (int kb = 0; kb < kPrefetch && kb < a.kblocks; ++kb)
-                    ptx::tma_prefetch_2d(&tmA, kb * (DROW / TR::kElemBytes), mb * DBM);
+                for (int kb = 0; kb < kPrefetch && kb < a.kblocks; ++kb) {
+                    if constexpr (TR::kAPlanes > 1)
+                        ptx::tma_prefetch_3d(&tmA, kb * (DROW / TR::kElemBytes), mb * DBM, 0);
+                    else
+                        ptx::tma_prefetch_2d(&tmA, kb * (DROW / TR::kElemBytes), mb * DBM);
+                }
                 for (int kb = 0; kb < a.kblocks; ++kb) {
-                    if (kb + kPrefetch < a.kblocks)
-                        ptx::tma_prefetch_2d(&tmA, (kb + kPrefetch) * (DROW / TR::kElemBytes),
-                                             mb * DBM);
+                    if (kb + kPrefetch < a.kblocks) {
+                        if constexpr (TR::kAPlanes > 1)
+                            ptx::tma_prefetch_3d(&tmA, (kb + kPrefetch) * (DROW / TR::kElemBytes),
+                                                 mb * DBM, 0);
+                        else
+                            ptx::tma_prefetch_2d(&tmA, (kb + kPrefetch) * (DROW / TR::kElemBytes),
+                                                 mb * DBM);
+                    }
                     long long c0 = a.stats ? clk() : 0;
                     ptx::mbar_wait(empty + stage, ph ^ 1, a.timeout_ns);
                     if (a.stats) st_empty += clk() - c0;
@@ -551,7 +597,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         // the leader's barrier counts both CTAs' bytes; each CTA's loads land
                         // in its own smem and complete on the leader's barrier
                         if (crank == 0) ptx::mbar_arrive_expect_tx(full + stage, 2 * tx);
-                        ptx::tma_load_2d_2sm(sa, &tmA, full + stage, kcol, mb * DBM, keep);
+                        if constexpr (TR::kAPlanes > 1)
+                            ptx::tma_load_3d_2sm(sa, &tmA, full + stage, kcol, mb * DBM, 0, keep);
+                        else
+                            ptx::tma_load_2d_2sm(sa, &tmA, full + stage, kcol, mb * DBM, keep);
                     } else {
                         ptx::mbar_arrive_expect_tx(full + stage, tx);
                         ptx::tma_load_2d_hint(sa, &tmA, full + stage, kcol, mb * DBM, keep);
@@ -577,7 +626,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         ptx::tma_load_3d_2sm(sa + DA_BYTES, tmB, full + stage, kcol,
                                              nb * a.bn + crank * (a.bn / 2), 0, keep);
                     } else if constexpr (PAIR) {
-                        ptx::tma_load_2d_2sm(sa + DA_BYTES, tmB, full + stage, kcol,
+                        ptx::tma_load_2d_2sm(sa + A_BYTES, tmB, full + stage, kcol,
                                              nb * a.bn + crank * (a.bn / 2), keep);
                     } else if constexpr (CL > 1) {
                         static_assert(TR::kPlanes == 1, "B multicast: single-plane B only");
@@ -635,7 +684,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 #pragma unroll
                     for (int pl = 0; pl < TR::kPlanes; ++pl) {
                         const uint64_t db =
-                            ptx::sw128_kmajor_desc(sa + DA_BYTES + pl * b_plane_bytes);
+                            ptx::sw128_kmajor_desc(sa + A_BYTES + pl * b_plane_bytes);
 #pragma unroll
                         for (int k = 0; k < DROW / 32; ++k) {  // 32 B of K per MMA
                             const uint32_t accum = (kb | pl | k) != 0;
@@ -649,6 +698,12 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                                               accum);
                             else if constexpr (PAIR && KD == Kind::kF16x2)
                                 ptx::mma2_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
+                            else if constexpr (PAIR && KD == Kind::kJ16x2) {
+                                // J1.s then J2.s (the A planes sit DA_BYTES apart)
+                                ptx::mma2_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
+                                ptx::mma2_f16(d, da + (DA_BYTES >> 4) + 2 * k, db + 2 * k, idesc,
+                                              1u);
+                            }
                             else if constexpr (PAIR)
                                 ptx::mma2_f8f6f4(d, da + 2 * k, db + 2 * k, idesc, accum);
                             else if constexpr (KD == Kind::kFp8)
@@ -825,8 +880,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         const bool ok = row_ok && (r0 + jj) < a.R;
                         const int64_t off = base + (int64_t)jj * a.ld;
                         const float f = O::mul(a.scale, __uint_as_float(v[jj]));
-                        if constexpr (KD == Kind::kFp8) {
-                            if (a.qtrace) {  // exact per-step energy of s_t = sign(x_t)
+                        if constexpr (PA_KIND) {
+                            if (KD == Kind::kFp8 && a.qtrace) {  // exact energy of s_t
                                 const int kk = (int)__uint_as_float(v[jj]);
                                 const int term = ok ? (xo[jj] >= 0.f ? kk : -kk) : 0;
                                 const int sum = __reduce_add_sync(0xffffffffu, term);
@@ -840,12 +895,19 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             const float mn = O::sub(O::mul(a.alpha, mo[jj]), O::mul(a.eta, grad));
                             float xn = O::add(xo[jj], mn);
                             xn = xn < -1.f ? -1.f : (xn > 1.f ? 1.f : xn);
-                            if (ok) {
+                            if constexpr (KD == Kind::kJ16x2) {
+                                if (ok) {
+                                    ptx::st_stream(xg + off, xn, stream);
+                                    ptx::st_stream(mg + off, mn, stream);
+                                    reinterpret_cast<uint16_t*>(nxt)[off] =
+                                        xn >= 0.f ? (uint16_t)0x3C00 : (uint16_t)0xBC00;  // +-1
+                                }
+                            } else if (ok) {
                                 ptx::st_stream(xg + off, xn, stream);
                                 ptx::st_stream(mg + off, mn, stream);
                                 if (!a.b_fp4) nxt[off] = xn >= 0.f ? FP8_P1 : FP8_M1;
                             }
-                            if (a.b_fp4) {  // lanes 2k, 2k+1 = rows i, i+1: one packed byte
+                            if (KD == Kind::kFp8 && a.b_fp4) {  // lanes 2k, 2k+1 = rows i, i+1: one packed byte
                                 const uint32_t code = ok ? (xn >= 0.f ? FP4_P1 : FP4_M1) : 0u;
                                 const uint32_t hi4 = __shfl_xor_sync(0xffffffffu, code, 1);
                                 if (!(lane & 1) && (code | hi4))
@@ -1129,6 +1191,51 @@ bool dense_eligible(const Problem* p, int64_t R) {
     return density >= 0.25;
 }
 
+// general (non-uniform) dense J on the tensor cores: PA only, no in-kernel energies
+bool dense_general_eligible(const Problem* p, int64_t R) {
+    if (p->uniform_magnitude || p->n < 512 || R < 128 || !(p->magnitude > 0)) return false;
+    if (const char* e = getenv("VXQ_DENSE_GENERAL"))
+        if (atoi(e) == 0) return false;
+    double density = (double)p->nnz / ((double)p->n * (double)p->n);
+    return density >= 0.25;
+}
+
+// Lazily build the fp16 planes of 2^e J (e: the largest scaled |J| stays below 2^15).
+static DenseOperand* dense_jplanes(Problem* p, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(p->mu);
+    DenseOperand* d = p->dense;
+    const bool fresh = d == nullptr;
+    if (fresh) {
+        d = new DenseOperand();
+        d->n = p->n;
+        d->ld = ceil_div(p->n, 128) * 128;
+    }
+    try {
+        if (!d->J16) {
+            const int64_t ld = d->ld;
+            int ex = 0;
+            std::frexp((double)(float)p->magnitude, &ex);  // |J| < 2^ex
+            const int e = 15 - ex;
+            VXQ_REQUIRE(e > -100 && e < 100, "coupling magnitudes out of the fp16-plane range");
+            const float scale = std::ldexp(1.0f, e);
+            d->jscale_inv = std::ldexp(1.0f, -e);
+            VXQ_CUDA(cudaMalloc(&d->J16, 2 * ld * ld * sizeof(__half)));
+            VXQ_CUDA(cudaMemsetAsync(d->J16, 0, 2 * ld * ld * sizeof(__half), s));
+            k_build_j_planes<<<(unsigned)ceil_div(p->n * 32, TB), TB, 0, s>>>(
+                p->n, ld, p->indptr, p->indices, p->data32, scale, d->J16);
+            VXQ_CHECK_LAUNCH();
+            d->tmJ = make_map(d->J16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ld, ld, 2, DROW / 2,
+                              DBM, 2);
+            VXQ_CUDA(cudaStreamSynchronize(s));
+        }
+    } catch (...) {
+        if (fresh) delete d;
+        throw;
+    }
+    p->dense = d;
+    return d;
+}
+
 // Lazily build the sign matrix K (fp8 for PA/energies, bf16 for SBM) and its TMA maps.
 // need16: 0 none, 1 bf16 K (SBM bf16x3), 2 fp16 K (SBM f16x2)
 DenseOperand* dense_operand(Problem* p, cudaStream_t s, int need16) {
@@ -1236,7 +1343,8 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
 static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap& tb0,
                        const CUtensorMap& tb1, int planes16, int cl, cudaStream_t s,
                        bool pair = false, const CUtensorMap* tmX = nullptr,
-                       const CUtensorMap* tmM = nullptr, bool mx = false) {
+                       const CUtensorMap* tmM = nullptr, bool mx = false,
+                       bool jplanes = false) {
     const char* want = getenv("VXQ_DENSE_STATS");
     DevBuf<unsigned long long> stats;
     if (want && want[0] == '1') {
@@ -1249,7 +1357,9 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     VXQ_CUDA(cudaEventCreate(&e1));
     VXQ_CUDA(cudaEventRecord(e0, s));
     if (a.T > 0) {
-        if (planes16 == 3) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        if (jplanes)
+            launch_run<Kind::kJ16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
+        else if (planes16 == 3) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 2 && pair)
             launch_run<Kind::kF16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 2) launch_run<Kind::kF16x2, 1>(tmA, tb0, tb1, a, a.T, s, true);
@@ -1300,7 +1410,7 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     VXQ_CUDA(cudaMemsetAsync(s0.get(), 0, sbytes, s));
     VXQ_CUDA(cudaMemsetAsync(s1.get(), 0, sbytes, s));
     k_init_pa_rm<<<nblk(((n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, x.get(), m.get(),
-                                                       s0.get(), s_fp4);
+                                                       s0.get(), s_fp4 ? 1 : 0);
     VXQ_CHECK_LAUNCH();
     // kind::mxf4 (VXQ_DENSE_MXF4=1): packed E2M1 operands in smem at twice the f8f6f4 MMA
     // rate; needs the packed K and spins, and bn <= 240 (TMEM holds the scale factors too)
@@ -1430,6 +1540,77 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
         VXQ_CHECK_LAUNCH();
         *launches += 2;
     }
+    k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(x.get(), n, R, ld, R_pad, V, x_il);
+    k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(m.get(), n, R, ld, R_pad, V, m_il);
+    k_pack_bits_rm<<<(unsigned)ceil_div(n * W * 32, TB), TB, 0, s>>>(x.get(), n, R, ld, W, sb);
+    VXQ_CHECK_LAUNCH();
+    *launches += 3;
+    VXQ_CUDA(cudaStreamSynchronize(s));
+}
+
+// Run the T-step PA loop for a general (non-uniform) dense J on the tensor cores: J as two
+// fp16 A planes, spins as fp16 +-1, tcgen05 CTA pairs, the fused PA epilogue.  Outputs as
+// dense_pa_loop (no in-kernel energies: the caller's exact energy kernel runs on sb).
+void dense_pa_general_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
+                           const std::vector<double>& sched, float eta, float alpha,
+                           uint64_t seed, int64_t rbegin, float* x_il, float* m_il, uint32_t* sb,
+                           cudaStream_t s, double* loop_ms, int64_t* launches) {
+    DenseOperand* d = dense_jplanes(p, s);
+    const int64_t n = p->n, ld = d->ld, T = (int64_t)sched.size();
+    VXQ_REQUIRE(ceil_div(n, DBM) >= 2, "general dense path needs n > 128");
+    DevBuf<float> x(R * ld, s), m(R * ld, s);
+    DevBuf<uint16_t> s0(R * ld, s), s1(R * ld, s);
+    VXQ_CUDA(cudaMemsetAsync(s0.get(), 0, R * ld * 2, s));
+    VXQ_CUDA(cudaMemsetAsync(s1.get(), 0, R * ld * 2, s));
+    k_init_pa_rm<<<nblk(((n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, x.get(), m.get(),
+                                                       reinterpret_cast<uint8_t*>(s0.get()), 2);
+    VXQ_CHECK_LAUNCH();
+    const int64_t blocks = ceil_div(R, (int64_t)256);
+    int bn = (int)std::min<int64_t>(256, ceil_div(ceil_div(R, blocks), 16) * 16);
+    if (const char* e = getenv("VXQ_DENSE_BN")) bn = std::max(16, std::min(256, atoi(e) / 16 * 16));
+    const int bbox = bn / 2;
+    CUtensorMap tmB0 = make_map(s0.get(), CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ld, R, 1, DROW / 2,
+                                bbox, 1);
+    CUtensorMap tmB1 = make_map(s1.get(), CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ld, R, 1, DROW / 2,
+                                bbox, 1);
+    std::vector<float> s32(T);
+    for (int64_t t = 0; t < T; ++t) s32[t] = (float)sched[t];
+    DevBuf<float> sc(std::max<int64_t>(T, 1), s);
+    VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
+    DenseRunArgs a{};
+    a.idesc_extra = 0;
+    a.a_tx_bytes = 2 * DA_BYTES;  // both J planes
+    a.b_tx_bytes = (uint32_t)bbox * DROW;
+    a.b_fp4 = 0;
+    a.n = (int)n;
+    a.R = (int)R;
+    a.ld = (int)ld;
+    a.kblocks = (int)(ld / (DROW / 2));
+    a.m_tiles = (int)ceil_div(n, DBM);
+    a.n_tiles = (int)ceil_div(R, bn);
+    a.bn = bn;
+    a.T = (int)T;
+    a.scale = d->jscale_inv;
+    a.eta = eta;
+    a.alpha = alpha;
+    a.sched = sc.get();
+    a.h = p->h32;
+    a.x = x.get();
+    a.m = m.get();
+    a.b_buf[0] = reinterpret_cast<uint8_t*>(s0.get());
+    a.b_buf[1] = reinterpret_cast<uint8_t*>(s1.get());
+    a.group = pick_group(a.n_tiles);
+    a.mode = 0;
+    DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
+    VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
+    a.done = done.get();
+    CUtensorMap tmX = make_map(x.get(), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ld, R, 1, DBM, 16, 1,
+                               CU_TENSOR_MAP_SWIZZLE_NONE);
+    CUtensorMap tmM = make_map(m.get(), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ld, R, 1, DBM, 16, 1,
+                               CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.xm = 1;
+    *loop_ms = run_loop(a, d->tmJ, tmB0, tmB1, 0, 1, s, true, &tmX, &tmM, false, true);
+    *launches += 2;
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(x.get(), n, R, ld, R_pad, V, x_il);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(m.get(), n, R, ld, R_pad, V, m_il);
     k_pack_bits_rm<<<(unsigned)ceil_div(n * W * 32, TB), TB, 0, s>>>(x.get(), n, R, ld, W, sb);

@@ -980,20 +980,29 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     // fused best tracking on the dense path uses the in-kernel exact coupling energies,
     // which are the whole energy only when h == 0 (else: the sparse path's exact tracker)
     const bool dense_cand =
-        sizeof(T) == 4 && (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+        sizeof(T) == 4 && p->uniform_magnitude &&
+        (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+    // general (non-uniform) dense J: fp16 J planes on the tensor cores, PA without tracking
+    const bool gen_cand =
+        sizeof(T) == 4 && !p->uniform_magnitude &&
+        (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && dense_general_eligible(p, R)));
+    if (gen_cand && req == VXQ_PATH_DENSE && (want_best || want_trace))
+        throw Error(VXQ_ERR_UNSUPPORTED,
+                    "trace / track_best on the dense path need uniform |J_ij| (e.g. SK)");
+    const bool dense_gen = gen_cand && !want_best && !want_trace;
     const bool h0 = want_best && dense_cand ? problem_h_zero(p, s) : true;
     if (want_best && req == VXQ_PATH_DENSE && !h0)
         throw Error(VXQ_ERR_UNSUPPORTED, "track_best on the dense path needs h = 0");
     const bool dense = dense_cand && (!want_best || h0);
-    if (!dense) path = choose_path(req, L, smem, p->nnz);
+    if (!dense && !dense_gen) path = choose_path(req, L, smem, p->nnz);
     // the resident kernel keeps spins in shared memory: tracking needs per-step spins
-    if (!dense && path == VXQ_PATH_RESIDENT && (want_best || want_trace)) {
+    if (!dense && !dense_gen && path == VXQ_PATH_RESIDENT && (want_best || want_trace)) {
         if (req == VXQ_PATH_RESIDENT)
             throw Error(VXQ_ERR_UNSUPPORTED, "tracking needs the sparse or dense path");
         path = VXQ_PATH_SPARSE;
     }
     Tracker trk;
-    if (!dense) trk.init(p, L, T_, want_trace, want_best, s);
+    if (!dense && !dense_gen) trk.init(p, L, T_, want_trace, want_best, s);
     EventTimer tm(s);
     const uint32_t* sb_final = nullptr;
     DevBuf<long long> q2;
@@ -1007,6 +1016,12 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
                           out->energy_trace, opts && opts->outputs_on_device, sb_best.get());
         }
         sb_final = want_best ? sb_best.get() : sbA.get();
+    } else if (dense_gen) {
+        if constexpr (sizeof(T) == 4) {
+            dense_pa_general_loop(p, R, L.R_pad, L.V, L.W, sched, eta, alpha, prm->seed, rbegin,
+                                  x.get(), m.get(), sbA.get(), s, &out->loop_ms, &launches);
+        }
+        sb_final = sbA.get();
     } else if (path == VXQ_PATH_RESIDENT) {
         DevBuf<T> ds(std::max<int64_t>(T_, 1), s);
         std::vector<T> st(T_);
@@ -1045,7 +1060,7 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         trk.export_trace(out, T_, opts && opts->outputs_on_device, s);
         if (trk.best) sb_final = trk.best_sb.get();
     }
-    out->path_used = dense ? VXQ_PATH_DENSE : path;
+    out->path_used = (dense || dense_gen) ? VXQ_PATH_DENSE : path;
     // q2 (coupling energy counts of the final spins) only describes sb_final without tracking
     finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s,
                       dense && !want_best ? q2.get() : nullptr);

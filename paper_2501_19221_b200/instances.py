@@ -232,8 +232,8 @@ CONFIGS = {
 
 
 def build(name: str, n: int | None = None) -> IsingModel:
-    if name == "cfg1":
-        return cfg1_qubo()[1]
+    if name == "cfg1":  # --n scales the same dense random QUBO family (general dense J)
+        return cfg1_qubo(n=n or 100)[1]
     if name == "cfg2":
         return sk(n or 10_000)
     if name == "cfg3":
