@@ -416,15 +416,17 @@ def run_ours(args):
         # (VXQ_SBM_PLANES=3), kind::f16, so the kernel issues planes x 2N flops per update at
         # the bf16 rate; useful work is 2N
         planes = 3 if os.environ.get("VXQ_SBM_PLANES") == "3" else 2
+        if not _uniform(model, local):
+            planes = 4  # general dense J: 2 fp16 J planes x 2 fp16 q planes
         flops = planes * 2.0 * n * R * n
         achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
         tr, tsrc = measured_traffic("k_dense_run_sbm", args.config)
         roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
                 "frac": achieved / bf16, "traffic": tr, "traffic_unit": "bytes/step",
                 "traffic_source": tsrc,
-                "kernel": (f"k_dense_run<{'bf16x3' if planes == 3 else 'f16x2'}>: "
-                           f"tcgen05.mma kind::f16 over {planes} q planes + fused symplectic "
-                           "SBM epilogue (persistent)"),
+                "kernel": (f"k_dense_run<{ {3: 'bf16x3', 2: 'f16x2', 4: 'JQ16'}[planes] }>: "
+                           f"tcgen05.mma kind::f16, {planes} plane products per k-block + "
+                           "fused symplectic SBM epilogue (persistent)"),
                 "peak_note": f"measured bf16 sustained ({bf16} TF/s, {src})",
                 "flops_per_update_issued": planes * 2.0 * n, "flops_per_update_useful": 2.0 * n,
                 "useful_frac_of_fp8_peak": achieved / planes / (2.0 * bf16),

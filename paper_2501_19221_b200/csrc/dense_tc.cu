@@ -45,7 +45,7 @@ constexpr int XM_SLOT_BYTES = 2 * 16 * DBM * 4;  // x and m of 16 replicas x 128
 constexpr int DSMEM = RING_BYTES + 1024 + 256;
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
-enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3 };
+enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3, kJQ16 = 4 };
 
 template <Kind K>
 struct KindTraits;
@@ -78,6 +78,13 @@ struct KindTraits<Kind::kF16x2> {
 template <>
 struct KindTraits<Kind::kJ16x2> {
     static constexpr int kPlanes = 1, kAPlanes = 2, kStages = 3, kBnMax = 128, kElemBytes = 2;
+    static constexpr int kKPerMma = 16;
+    static constexpr uint32_t kIdescBase = (1u << 4);
+};
+// SBM with general dense J: two fp16 J planes (A) x two fp16 q planes (B), 4 MMAs per k-block
+template <>
+struct KindTraits<Kind::kJQ16> {
+    static constexpr int kPlanes = 2, kAPlanes = 2, kStages = 2, kBnMax = 128, kElemBytes = 2;
     static constexpr int kKPerMma = 16;
     static constexpr uint32_t kIdescBase = (1u << 4);
 };
@@ -479,14 +486,17 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const __grid_constant__ CUtensorMap tmM, DenseRunArgs a) {
     using TR = KindTraits<KD>;
     static_assert(!PAIR || (KD != Kind::kBf16x3 && CL == 1), "pair MMA: f8f6f4 / f16x2, no B multicast");
-    static_assert(KD != Kind::kJ16x2 || PAIR, "general-J planes: CTA pairs only");
+    static_assert((KD != Kind::kJ16x2 && KD != Kind::kJQ16) || PAIR,
+                  "general-J planes: CTA pairs only");
     constexpr int A_BYTES = DA_BYTES * TR::kAPlanes;  // A planes of one stage, back to back
     static_assert(!MX || (KD == Kind::kFp8 && CL == 1), "mxf4: fp8-kind layout, no multicast");
     constexpr uint32_t ACC_COLS = MX ? kAccMx : 256;
     constexpr int NCTA = PAIR ? 2 : CL;
     // pair: each CTA stages its 128 A rows and <= 128 B rows per plane
     constexpr int STAGES =
-        PAIR ? ((TR::kPlanes == 1 && TR::kAPlanes == 1) ? VXQ_PAIR_STAGES : 4) : TR::kStages;
+        PAIR ? ((TR::kPlanes == 1 && TR::kAPlanes == 1) ? VXQ_PAIR_STAGES
+                                                        : (TR::kPlanes * TR::kAPlanes > 2 ? 3 : 4))
+             : TR::kStages;
     constexpr int SBYTES = PAIR ? A_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
     static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
@@ -623,7 +633,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         if (a.stats) st_dep += clk() - c1;
                     }
                     if constexpr (PAIR && TR::kPlanes > 1) {
-                        ptx::tma_load_3d_2sm(sa + DA_BYTES, tmB, full + stage, kcol,
+                        ptx::tma_load_3d_2sm(sa + A_BYTES, tmB, full + stage, kcol,
                                              nb * a.bn + crank * (a.bn / 2), 0, keep);
                     } else if constexpr (PAIR) {
                         ptx::tma_load_2d_2sm(sa + A_BYTES, tmB, full + stage, kcol,
@@ -638,7 +648,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         ptx::tma_load_2d_hint(sa + DA_BYTES, tmB, full + stage, kcol,
                                               nb * a.bn, keep);
                     } else {
-                        ptx::tma_load_3d_hint(sa + DA_BYTES, tmB, full + stage, kcol,
+                        ptx::tma_load_3d_hint(sa + A_BYTES, tmB, full + stage, kcol,
                                               nb * a.bn, 0, keep);
                     }
                     if (++stage == STAGES) {
@@ -698,7 +708,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                                               accum);
                             else if constexpr (PAIR && KD == Kind::kF16x2)
                                 ptx::mma2_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
-                            else if constexpr (PAIR && KD == Kind::kJ16x2) {
+                            else if constexpr (PAIR && (KD == Kind::kJ16x2 || KD == Kind::kJQ16)) {
                                 // J1.s then J2.s (the A planes sit DA_BYTES apart)
                                 ptx::mma2_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
                                 ptx::mma2_f16(d, da + (DA_BYTES >> 4) + 2 * k, db + 2 * k, idesc,
@@ -928,7 +938,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             if (ok) {
                                 ptx::st_stream(xg + off, qn, stream);
                                 ptx::st_stream(mg + off, pn, stream);
-                                if constexpr (KD == Kind::kF16x2) {
+                                if constexpr (KD == Kind::kF16x2 || KD == Kind::kJQ16) {
                                     __half q1, q2;
                                     split2(qn, q1, q2);
                                     __half* pl = reinterpret_cast<__half*>(nxt);
@@ -1191,7 +1201,9 @@ bool dense_eligible(const Problem* p, int64_t R) {
     return density >= 0.25;
 }
 
-// general (non-uniform) dense J on the tensor cores: PA only, no in-kernel energies
+bool dense_sbm_fp16_ok(double q_cap, double amp) { return std::max(q_cap, amp) <= 16384.0; }
+
+// general (non-uniform) dense J on the tensor cores: no in-kernel energies
 bool dense_general_eligible(const Problem* p, int64_t R) {
     if (p->uniform_magnitude || p->n < 512 || R < 128 || !(p->magnitude > 0)) return false;
     if (const char* e = getenv("VXQ_DENSE_GENERAL"))
@@ -1344,7 +1356,7 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
                        const CUtensorMap& tb1, int planes16, int cl, cudaStream_t s,
                        bool pair = false, const CUtensorMap* tmX = nullptr,
                        const CUtensorMap* tmM = nullptr, bool mx = false,
-                       bool jplanes = false) {
+                       bool jplanes = false, bool jq = false) {
     const char* want = getenv("VXQ_DENSE_STATS");
     DevBuf<unsigned long long> stats;
     if (want && want[0] == '1') {
@@ -1359,6 +1371,7 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     if (a.T > 0) {
         if (jplanes)
             launch_run<Kind::kJ16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
+        else if (jq) launch_run<Kind::kJQ16, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 3) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 2 && pair)
             launch_run<Kind::kF16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
@@ -1627,10 +1640,13 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                     double q_cap, double amp, uint64_t seed, int64_t rbegin, float* q_il,
                     float* p_il, uint32_t* sb, long long* q2, cudaStream_t s, double* loop_ms,
                     int64_t* launches) {
+    // general (non-uniform) J: J as two fp16 planes too (kJQ16, the caller checked the range)
+    const bool general = !p->uniform_magnitude;
     int planes = 2;
     if (const char* e = getenv("VXQ_SBM_PLANES")) planes = atoi(e) == 3 ? 3 : 2;
-    if (!(std::max(q_cap, amp) <= 16384.0)) planes = 3;  // fp16 max is 65504
-    DenseOperand* d = dense_operand(p, s, planes == 3 ? 1 : 2);
+    if (!dense_sbm_fp16_ok(q_cap, amp)) planes = 3;  // fp16 max is 65504
+    VXQ_REQUIRE(!general || planes == 2, "general dense J on the tensor cores needs fp16 q");
+    DenseOperand* d = general ? dense_jplanes(p, s) : dense_operand(p, s, planes == 3 ? 1 : 2);
     const int64_t n = p->n, ld = d->ld, T = (int64_t)a_sched.size();
     const int64_t plane = R * ld;
     DevBuf<float> q(R * ld, s), pm(R * ld, s);
@@ -1644,6 +1660,10 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     // bn/2 replicas of both planes): half the replica blocks -> half the K re-reads per step
     bool pair = planes == 2 && ceil_div(n, DBM) >= 2;
     if (const char* e = getenv("VXQ_DENSE_2CTA")) pair = pair && atoi(e) == 1;
+    if (general) {
+        VXQ_REQUIRE(ceil_div(n, DBM) >= 2, "general dense path needs n > 128");
+        pair = true;
+    }
     int bn;
     if (pair) {
         const int64_t blocks = ceil_div(R, (int64_t)256);
@@ -1662,7 +1682,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
     VXQ_CUDA(cudaMemcpyAsync(sc.get(), s32.data(), T * sizeof(float), cudaMemcpyHostToDevice, s));
     DenseRunArgs a{};
-    a.a_tx_bytes = DA_BYTES;  // 16-bit K: full boxes
+    a.a_tx_bytes = general ? 2 * DA_BYTES : DA_BYTES;  // 16-bit K (or both J planes): full boxes
     a.b_tx_bytes = (uint32_t)bbox * DROW;
     a.n = (int)n;
     a.R = (int)R;
@@ -1672,7 +1692,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     a.n_tiles = (int)ceil_div(R, bn);
     a.bn = bn;
     a.T = (int)T;
-    a.scale = d->scale;
+    a.scale = general ? d->jscale_inv : d->scale;
     a.dt = (float)dt;
     a.a0 = (float)a0;
     a.c0 = (float)c0;
@@ -1690,9 +1710,10 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
-    *loop_ms = run_loop(a, planes == 3 ? d->tmA16 : d->tmA16h, tmB0, tmB1, planes, 1, s, pair);
+    *loop_ms = run_loop(a, general ? d->tmJ : (planes == 3 ? d->tmA16 : d->tmA16h), tmB0, tmB1,
+                        planes, 1, s, pair, nullptr, nullptr, false, false, general);
     *launches += 2;
-    if (q2) energy_pass(d, q.get(), n, R, q2, s, launches);
+    if (q2 && !general) energy_pass(d, q.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(q.get(), n, R, ld, R_pad, V, q_il);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(pm.get(), n, R, ld, R_pad, V, p_il);
     k_pack_bits_rm<<<(unsigned)ceil_div(n * W * 32, TB), TB, 0, s>>>(q.get(), n, R, ld, W, sb);

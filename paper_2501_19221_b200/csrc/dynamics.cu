@@ -1154,8 +1154,13 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
     const bool want_trace = out->energy_trace != nullptr;
     if (want_best && req == VXQ_PATH_DENSE)
         throw Error(VXQ_ERR_UNSUPPORTED, "track_best is not available on the dense path yet");
+    // uniform |J| (SK family): sign matrix K; general dense J: fp16 J planes (needs fp16 q)
+    const bool elig = p->uniform_magnitude
+                          ? dense_eligible(p, R)
+                          : dense_general_eligible(p, R) && dense_sbm_fp16_ok(prm->q_cap,
+                                                                              prm->init_noise);
     const bool dense = sizeof(T) == 4 && !want_best &&
-                       (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && dense_eligible(p, R)));
+                       (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && elig));
     if (dense) {
         if (want_trace) {  // no per-step energies on the dense SBM path (round 1): NaN
             DevBuf<double> nan_tr(std::max<int64_t>(T_, 1), s);
@@ -1168,10 +1173,12 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
         if constexpr (sizeof(T) == 4) {
             dense_sbm_loop(p, R, L.R_pad, L.V, L.W, sched, prm->dt, prm->a0, c0, prm->q_cap,
                            prm->init_noise, prm->seed, rbegin, q.get(), pm.get(), sb.get(),
-                           qq.get(), s, &out->loop_ms, &launches);
+                           p->uniform_magnitude ? qq.get() : nullptr, s, &out->loop_ms,
+                           &launches);
         }
         out->path_used = VXQ_PATH_DENSE;
-        finish_outputs<T>(p, L, sb.get(), q.get(), pm.get(), opts, out, s, qq.get());
+        finish_outputs<T>(p, L, sb.get(), q.get(), pm.get(), opts, out, s,
+                          p->uniform_magnitude ? qq.get() : nullptr);
         out->launches = launches + 4;
         return;
     }

@@ -201,6 +201,7 @@ void session_set_own_stream(Session* S, bool own);
 // ---- dense_tc.cu (tcgen05 path)
 bool dense_eligible(const Problem* p, int64_t R);
 bool dense_general_eligible(const Problem* p, int64_t R);
+bool dense_sbm_fp16_ok(double q_cap, double amp);  // |q| stays in the fp16 q-plane range
 void dense_pa_general_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                            const std::vector<double>& sched, float eta, float alpha,
                            uint64_t seed, int64_t rbegin, float* x_il, float* m_il, uint32_t* sb,

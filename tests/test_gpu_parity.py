@@ -500,3 +500,28 @@ def test_dense_general_j_quality_and_fallbacks():
     assert t.info["path"] == "sparse"
     with pytest.raises(vxq.QubokitError):
         vxq.run_pa(m, vxq.PaParams(steps=20, replicas=128, seed=1), path="dense", trace=True)
+
+
+@pytest.mark.parametrize("n,R", [(1000, 256), (700, 200)])
+def test_dense_general_j_sbm_short_horizon(n, R):
+    """SBM with a general dense J on the tensor cores (two fp16 J planes x two fp16 q planes,
+    fp32 accumulation): one step within 2e-5 of the fp64 reference loop, ten steps as close
+    to it as the fp32 CSR restatement (99th percentile); energies exact."""
+    m = gen_complete(23, n)
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    c0 = vxq.resolve_c0(m)
+    for T in (1, 10):
+        prm = vxq.SbmParams(steps=T, dt=0.05, replicas=R, seed=7, c0=c0)
+        r = vxq.run_sbm(m, prm, want_state=True)
+        assert r.info["path"] == "dense"
+        assert np.array_equal(r.energies, O.energies_exact(m, r.states))
+        Q, P = O.sbm_init(7, 8, m.n, 1.0)
+        Q, P = O.sbm_run(ip, ix, -dv, -m.h, O.sbm_schedule(1.0, T), 0.05, 1.0, c0, 1.0, Q, P)
+        dq = np.abs(r.x[:8] - Q)
+        if T == 1:
+            assert dq.max() <= 2e-5 and np.abs(r.m[:8] - P).max() <= 2e-5
+            continue
+        s = vxq.run_sbm(m, prm, path="sparse", want_state=True)
+        ds = np.abs(s.x[:8] - Q)
+        assert np.quantile(dq, 0.99) <= 3 * np.quantile(ds, 0.99) + 1e-5
+        assert np.mean(r.states == s.states) >= 0.999
