@@ -306,9 +306,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only knob: VXQ_BENCH_BACKEND=gloo runs the multi-rank control flow with several
+    # ranks sharing the visible GPU(s) (replica shards never wait on each other); the
+    # driver's runs use NCCL with one GPU per rank
+    backend = os.environ.get("VXQ_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2501_19221_b200 as vxq
     from paper_2501_19221_b200 import instances
