@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--solver", default="pa", choices=["pa", "sbm"])
     ap.add_argument("--T", type=int, default=None)
     ap.add_argument("--replicas", type=int, default=None)
-    ap.add_argument("--n", type=int, default=None, help="override instance size")
+    ap.add_argument("--n", "--nvars", dest="n", type=int, default=None,
+                    help="override instance size (--nvars under torchrun)")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-e2e", action="store_true")
