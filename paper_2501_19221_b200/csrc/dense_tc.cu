@@ -110,10 +110,10 @@ struct DenseOperand {
     CUtensorMap tmJ;
     CUtensorMap tmA8, tmA16, tmA16h;
     ~DenseOperand() {
-        if (K8) cudaFree(K8);
-        if (K16) cudaFree(K16);
-        if (K16h) cudaFree(K16h);
-        if (J16) cudaFree(J16);
+        if (K8) cudaFreeAsync(K8, 0);  // back to the retained pool
+        if (K16) cudaFreeAsync(K16, 0);
+        if (K16h) cudaFreeAsync(K16h, 0);
+        if (J16) cudaFreeAsync(J16, 0);
     }
 };
 
@@ -1231,7 +1231,7 @@ static DenseOperand* dense_jplanes(Problem* p, cudaStream_t s) {
             VXQ_REQUIRE(e > -100 && e < 100, "coupling magnitudes out of the fp16-plane range");
             const float scale = std::ldexp(1.0f, e);
             d->jscale_inv = std::ldexp(1.0f, -e);
-            VXQ_CUDA(cudaMalloc(&d->J16, 2 * ld * ld * sizeof(__half)));
+            VXQ_CUDA(cudaMallocAsync((void**)&d->J16, 2 * ld * ld * sizeof(__half), s));
             VXQ_CUDA(cudaMemsetAsync(d->J16, 0, 2 * ld * ld * sizeof(__half), s));
             k_build_j_planes<<<(unsigned)ceil_div(p->n * 32, TB), TB, 0, s>>>(
                 p->n, ld, p->indptr, p->indices, p->data32, scale, d->J16);
@@ -1274,7 +1274,7 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, int need16) {
             const char* e4 = getenv("VXQ_DENSE_FP4");
             const bool fp4 = !(e4 && atoi(e4) == 0);
             const int64_t bytes = fp4 ? ld * ld / 2 : ld * ld;
-            VXQ_CUDA(cudaMalloc(&d->K8, bytes));
+            VXQ_CUDA(cudaMallocAsync((void**)&d->K8, bytes, s));
             VXQ_CUDA(cudaMemsetAsync(d->K8, 0, bytes, s));
             if (fp4) {
                 k4 = reinterpret_cast<uint32_t*>(d->K8);
@@ -1288,14 +1288,14 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, int need16) {
             }
         }
         if (need16 == 2 && !d->K16h) {
-            VXQ_CUDA(cudaMalloc(&d->K16h, ld * ld * 2));
+            VXQ_CUDA(cudaMallocAsync((void**)&d->K16h, ld * ld * 2, s));
             VXQ_CUDA(cudaMemsetAsync(d->K16h, 0, ld * ld * 2, s));
             k16h = d->K16h;
             d->tmA16h = make_map(d->K16h, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, ld, ld, 1,
                                  DROW / 2, DBM, 1);
         }
         if (need16 == 1 && !d->K16) {
-            VXQ_CUDA(cudaMalloc(&d->K16, ld * ld * 2));
+            VXQ_CUDA(cudaMallocAsync((void**)&d->K16, ld * ld * 2, s));
             VXQ_CUDA(cudaMemsetAsync(d->K16, 0, ld * ld * 2, s));
             k16 = d->K16;
             d->tmA16 = make_map(d->K16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, ld, 1, DROW / 2,

@@ -6,6 +6,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstring>
 
@@ -19,8 +20,11 @@ Problem::~Problem() {
     cudaSetDevice(device);
     void* ptrs[] = {indptr, indices, data64, data32, lower_count, h64,  h32,
                     g64,    g32,     coo_i,  coo_j,  coo_v,       coef_fx, h_fx};
+    // problem arrays live in the device's retained stream-ordered pool: freeing them
+    // returns the memory to the pool (no unmapping), and the next problem reuses it
     for (void* q : ptrs)
-        if (q) cudaFree(q);
+        if (q) cudaFreeAsync(q, 0);
+    cudaStreamSynchronize(0);
     extern void dense_destroy(DenseOperand*);
     if (dense) dense_destroy(dense);
     cudaSetDevice(prev);
@@ -39,8 +43,13 @@ __global__ void k_validate_coo(int64_t n, int64_t m, const int64_t* rows, const 
         int64_t pi = rows[k - 1], pj = cols[k - 1];
         if (!(pi < i || (pi == i && pj < j))) e |= 2;
     }
-    if (!isfinite(values[k])) e |= 4;
+    if (values && !isfinite(values[k])) e |= 4;
     if (e) atomicOr(err, e);
+}
+
+__global__ void k_check_finite(int64_t m, const double* values, int* err) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < m && !isfinite(values[k])) atomicOr(err, 4);
 }
 
 __global__ void k_count_deg(int64_t m, const int64_t* rows, const int64_t* cols, int32_t* deg_up,
@@ -246,8 +255,8 @@ void widen_i32_i64(int64_t n, const int32_t* a, int64_t* b, cudaStream_t s) {
 }  // namespace
 
 void encode_energy(Problem* P, cudaStream_t s) {
-    if (P->coef_fx) cudaFree(P->coef_fx);
-    if (P->h_fx) cudaFree(P->h_fx);
+    if (P->coef_fx) cudaFreeAsync(P->coef_fx, s);
+    if (P->h_fx) cudaFreeAsync(P->h_fx, s);
     P->coef_fx = P->h_fx = nullptr;
     P->energy_ok = true;
     const int64_t n = P->n, m = P->m;
@@ -281,8 +290,8 @@ void encode_energy(Problem* P, cudaStream_t s) {
                 L = kMaxLimbs;
             }
             P->limbs = L;
-            VXQ_CUDA(cudaMalloc(&P->coef_fx, std::max<int64_t>(m, 1) * L * sizeof(uint32_t)));
-            VXQ_CUDA(cudaMalloc(&P->h_fx, n * L * sizeof(uint32_t)));
+            VXQ_CUDA(cudaMallocAsync((void**)&P->coef_fx, std::max<int64_t>(m, 1) * L * sizeof(uint32_t), s));
+            VXQ_CUDA(cudaMallocAsync((void**)&P->h_fx, n * L * sizeof(uint32_t), s));
             if (P->energy_ok) {
                 if (m > 0) k_encode<<<nblk(m), TB, 0, s>>>(m, P->coo_v, P->e_low, L, P->coef_fx);
                 k_encode<<<nblk(n), TB, 0, s>>>(n, P->h64, P->e_low, L, P->h_fx);
@@ -303,8 +312,31 @@ void encode_energy(Problem* P, cudaStream_t s) {
         }
 }
 
+namespace {
+// VXQ_CREATE_TIMING=1: synchronise after each phase of problem_create and print its time
+struct PhaseTimer {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    std::chrono::steady_clock::time_point t0;
+    PhaseTimer() {
+        const char* e = getenv("VXQ_CREATE_TIMING");
+        on = e && e[0] == '1';
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        if (s) cudaStreamSynchronize(s);
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[vxq create] %-14s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+}  // namespace
+
 Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t* cols,
                         const double* values, const double* h, double offset, int device) {
+    PhaseTimer ph;
     VXQ_REQUIRE(n >= 1, "model needs at least one variable");
     VXQ_REQUIRE(n < (1LL << 31) - 1, "n must be < 2^31");
     VXQ_REQUIRE(m >= 0 && m < (1LL << 31) - 1, "num_couplings must be in [0, 2^31)");
@@ -314,6 +346,7 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
     VXQ_CUDA(cudaGetDeviceCount(&ndev));
     VXQ_REQUIRE(device >= 0 && device < ndev, "invalid CUDA device ordinal");
     VXQ_CUDA(cudaSetDevice(device));
+    retain_mempool();  // problem arrays come from the retained stream-ordered pool
 
     Problem* P = new Problem();
     try {
@@ -328,19 +361,22 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
             cudaStream_t s;
             ~SG() { cudaStreamDestroy(s); }
         } sg{s};
+        ph.s = s;
+        ph.mark("stream");
 
         const int64_t nnz = 2 * m;
-        VXQ_CUDA(cudaMalloc(&P->indptr, (n + 1) * sizeof(int64_t)));
-        VXQ_CUDA(cudaMalloc(&P->indices, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
-        VXQ_CUDA(cudaMalloc(&P->data64, std::max<int64_t>(nnz, 1) * sizeof(double)));
-        VXQ_CUDA(cudaMalloc(&P->data32, std::max<int64_t>(nnz, 1) * sizeof(float)));
-        VXQ_CUDA(cudaMalloc(&P->lower_count, n * sizeof(int32_t)));
-        VXQ_CUDA(cudaMalloc(&P->h64, n * sizeof(double)));
-        VXQ_CUDA(cudaMalloc(&P->h32, n * sizeof(float)));
-        VXQ_CUDA(cudaMalloc(&P->g64, n * sizeof(double)));
-        VXQ_CUDA(cudaMalloc(&P->g32, n * sizeof(float)));
-        VXQ_CUDA(cudaMalloc(&P->coo_i, std::max<int64_t>(m, 1) * sizeof(int32_t)));
-        VXQ_CUDA(cudaMalloc(&P->coo_j, std::max<int64_t>(m, 1) * sizeof(int32_t)));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->indptr, (n + 1) * sizeof(int64_t), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->indices, std::max<int64_t>(nnz, 1) * sizeof(int32_t), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->data64, std::max<int64_t>(nnz, 1) * sizeof(double), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->data32, std::max<int64_t>(nnz, 1) * sizeof(float), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->lower_count, n * sizeof(int32_t), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->h64, n * sizeof(double), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->h32, n * sizeof(float), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->g64, n * sizeof(double), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->g32, n * sizeof(float), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->coo_i, std::max<int64_t>(m, 1) * sizeof(int32_t), s));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->coo_j, std::max<int64_t>(m, 1) * sizeof(int32_t), s));
+        ph.mark("alloc");
 
         // fields
         if (h) {
@@ -356,27 +392,54 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
             lo64(n + 1, s);
         VXQ_CUDA(cudaMemsetAsync(deg_up.get(), 0, n * sizeof(int32_t), s));
         VXQ_CUDA(cudaMemsetAsync(deg_lo.get(), 0, n * sizeof(int32_t), s));
-        VXQ_CUDA(cudaMalloc(&P->coo_v, std::max<int64_t>(m, 1) * sizeof(double)));
+        VXQ_CUDA(cudaMallocAsync((void**)&P->coo_v, std::max<int64_t>(m, 1) * sizeof(double), s));
         struct DV {
             double* p;
             double* get() const { return p; }
         } dval{P->coo_v};
         DevBuf<int32_t> err(1, s);
         VXQ_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(int), s));
+        // the values travel on a second stream while the structure (validation, degree
+        // counts, the column sort) is built from rows / cols; the fills wait for them
+        cudaStream_t s2 = nullptr;
+        cudaEvent_t ev_rc = nullptr, ev_val = nullptr;
+        struct SG2 {
+            cudaStream_t& s;
+            cudaEvent_t& a;
+            cudaEvent_t& b;
+            ~SG2() {
+                if (a) cudaEventDestroy(a);
+                if (b) cudaEventDestroy(b);
+                if (s) cudaStreamDestroy(s);
+            }
+        } sg2{s2, ev_rc, ev_val};
         if (m > 0) {
-            DevBuf<int64_t> drows(m, s), dcols(m, s);
+            VXQ_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+            VXQ_CUDA(cudaEventCreateWithFlags(&ev_rc, cudaEventDisableTiming));
+            VXQ_CUDA(cudaEventCreateWithFlags(&ev_val, cudaEventDisableTiming));
+        }
+        DevBuf<int64_t> drows, dcols;
+        if (m > 0) {
+            drows = DevBuf<int64_t>(m, s);
+            dcols = DevBuf<int64_t>(m, s);
             VXQ_CUDA(cudaMemcpyAsync(drows.get(), rows, m * sizeof(int64_t), cudaMemcpyDefault, s));
             VXQ_CUDA(cudaMemcpyAsync(dcols.get(), cols, m * sizeof(int64_t), cudaMemcpyDefault, s));
-            VXQ_CUDA(cudaMemcpyAsync(dval.get(), values, m * sizeof(double), cudaMemcpyDefault, s));
-            k_validate_coo<<<nblk(m), TB, 0, s>>>(n, m, drows.get(), dcols.get(), dval.get(),
+            VXQ_CUDA(cudaEventRecord(ev_rc, s));
+            VXQ_CUDA(cudaStreamWaitEvent(s2, ev_rc, 0));  // one transfer at a time on PCIe
+            VXQ_CUDA(cudaMemcpyAsync(dval.get(), values, m * sizeof(double), cudaMemcpyDefault,
+                                     s2));
+            VXQ_CUDA(cudaEventRecord(ev_val, s2));
+            ph.mark("h2d");
+            k_validate_coo<<<nblk(m), TB, 0, s>>>(n, m, drows.get(), dcols.get(), nullptr,
                                                   err.get());
             VXQ_CHECK_LAUNCH();
             int herr = 0;
             VXQ_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
             VXQ_CUDA(cudaStreamSynchronize(s));
+            if (herr) cudaStreamSynchronize(s2);  // do not free dval under an in-flight copy
             VXQ_REQUIRE(!(herr & 1), "couplings must satisfy 0 <= i < j < n");
             VXQ_REQUIRE(!(herr & 2), "couplings must be sorted and unique by (i, j)");
-            VXQ_REQUIRE(!(herr & 4), "non-finite coupling value");
+            ph.mark("validate");
             k_count_deg<<<nblk(m), TB, 0, s>>>(m, drows.get(), dcols.get(), deg_up.get(),
                                                deg_lo.get(), P->coo_i, P->coo_j);
             VXQ_CHECK_LAUNCH();
@@ -416,6 +479,9 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
             VXQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), need, P->coo_j, sorted_cols.get(),
                                                      perm_in.get(), perm.get(), (int)m, 0,
                                                      end_bit, s));
+            VXQ_CUDA(cudaStreamWaitEvent(s, ev_val, 0));  // the values have landed
+            k_check_finite<<<nblk(m), TB, 0, s>>>(m, dval.get(), err.get());
+            VXQ_CHECK_LAUNCH();
             k_fill_upper<<<nblk(m), TB, 0, s>>>(m, P->coo_i, P->coo_j, dval.get(), P->indptr,
                                                 deg_lo.get(), ustart.get(), P->indices,
                                                 P->data64);
@@ -427,6 +493,7 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
             k_convert<<<nblk(nnz), TB, 0, s>>>(nnz, P->data64, P->data32);
             VXQ_CHECK_LAUNCH();
         }
+        ph.mark("csr");
         // max row length (dispatch heuristics)
         {
             DevBuf<int64_t> mx(1, s);
@@ -452,9 +519,14 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
             memcpy(&b, &res[1], 8);
             P->uniform_magnitude = (a == b) && a > 0;
             P->magnitude = b;
+            int herr = 0;
+            VXQ_CUDA(cudaMemcpy(&herr, err.get(), sizeof(int), cudaMemcpyDeviceToHost));
+            VXQ_REQUIRE(!(herr & 4), "non-finite coupling value");
         }
+        ph.mark("stats");
         encode_energy(P, s);
         VXQ_CUDA(cudaStreamSynchronize(s));
+        ph.mark("encode");
     } catch (...) {
         delete P;
         throw;
