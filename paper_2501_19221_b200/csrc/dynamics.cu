@@ -1367,10 +1367,11 @@ struct Session {
     int* status = nullptr;        // device: 1 = peer wait timed out
     uint64_t epoch = 0;           // flag values are (epoch << 32) + state + 1
     int64_t row_bytes = 0;
-    ~Session() {
-        if (x) cudaFree(x);
-        if (m) cudaFree(m);
-        if (status) cudaFree(status);
+    ~Session() {  // state from the retained stream-ordered pool (no unmapping)
+        if (x) cudaFreeAsync(x, s);
+        if (m) cudaFreeAsync(m, s);
+        if (status) cudaFreeAsync(status, s);
+        if (s) cudaStreamSynchronize(s);
         if (own_stream && s) cudaStreamDestroy(s);
     }
 };
@@ -1386,9 +1387,9 @@ template <typename T>
 void session_init_t(Session* S) {
     const Layout& L = S->L;
     const int64_t n = S->p->n;
-    VXQ_CUDA(cudaMalloc(&S->x, std::max<int64_t>(L.nrows, 1) * L.R_pad * sizeof(T)));
+    VXQ_CUDA(cudaMallocAsync(&S->x, std::max<int64_t>(L.nrows, 1) * L.R_pad * sizeof(T), S->s));
     if (S->solver == 0) {
-        VXQ_CUDA(cudaMalloc(&S->m, std::max<int64_t>(L.nrows, 1) * L.R_pad * sizeof(T)));
+        VXQ_CUDA(cudaMallocAsync(&S->m, std::max<int64_t>(L.nrows, 1) * L.R_pad * sizeof(T), S->s));
         k_init_pa<T><<<nblk(((L.nrows + 3) / 4 + 1) * L.R_pad), TB, 0, S->s>>>(
             L.row0, L.nrows, L.R_pad, L.V, S->seed, S->rbegin, (T*)S->x, (T*)S->m);
         VXQ_CHECK_LAUNCH();
@@ -1556,7 +1557,7 @@ void session_set_peers(Session* S, int world, int rank, uint32_t epoch, void* co
         S->pflags.p[k] = flags[k];
     }
     S->pxb[0].n = S->pxb[1].n = S->pflags.n = world;
-    VXQ_CUDA(cudaMalloc(&S->status, sizeof(int)));
+    VXQ_CUDA(cudaMallocAsync((void**)&S->status, sizeof(int), S->s));
     VXQ_CUDA(cudaMemsetAsync(S->status, 0, sizeof(int), S->s));
     // state 0 (written to the local rows by create) -> every peer, then publish it
     const int64_t off = S->L.row0 * S->row_bytes, bytes = S->L.nrows * S->row_bytes;
