@@ -476,6 +476,9 @@ constexpr uint32_t kAccMx = 240, kSfCol = 480;
 #ifndef VXQ_PAIR_STAGES
 #define VXQ_PAIR_STAGES 5  // 5 x 32 KB operand stages + 4 x/m slots in 224 KB
 #endif
+#if VXQ_PAIR_STAGES > 5
+#error "VXQ_PAIR_STAGES > 5 leaves 2 x/m slots: the loader/epilogue slot protocol needs 3+"
+#endif
 
 template <Kind KD, int CL, bool PAIR = false, bool MX = false>
 __global__ void __launch_bounds__(DTHREADS, 1)
