@@ -477,7 +477,7 @@ constexpr uint32_t kAccMx = 240, kSfCol = 480;
 #define VXQ_PAIR_STAGES 5  // 5 x 32 KB operand stages + 4 x/m slots in 224 KB
 #endif
 #if VXQ_PAIR_STAGES > 5
-#error "VXQ_PAIR_STAGES > 5 leaves 2 x/m slots: the loader/epilogue slot protocol needs 3+"
+#error "VXQ_PAIR_STAGES > 5: the mxf4 pair kernel faulted at 6 stages (not investigated); 5 is the measured best"
 #endif
 
 template <Kind KD, int CL, bool PAIR = false, bool MX = false>
