@@ -109,7 +109,8 @@ typedef struct {
     int32_t track_best;        /* 1: states/energies = best state seen per replica
                                   (over s_0..s_T; sparse/resident paths; opt-in)   */
     int64_t replica_begin;     /* global index of local replica 0 (sharding)     */
-    void* stream;              /* cudaStream_t; NULL => library stream           */
+    void* stream;              /* cudaStream_t; NULL => library stream (pass
+                                  cudaStreamLegacy, (void*)1, for the legacy default) */
 } vxq_run_opts;
 
 typedef struct {

@@ -178,6 +178,11 @@ def _opts(precision: str, path: str, replica_begin: int, stream=None,
     o.outputs_on_device = 1 if on_device else 0
     o.track_best = 1 if track_best else 0
     o.replica_begin = int(replica_begin)
+    # a NULL stream means "the library's own stream for this call"; a caller that hands in
+    # the legacy default stream (handle 0, e.g. torch's default current stream) wants work
+    # ordered on it, so pass the explicit cudaStreamLegacy handle instead
+    if stream is not None and int(stream) == 0:
+        stream = 0x1  # cudaStreamLegacy
     o.stream = stream
     return o
 
