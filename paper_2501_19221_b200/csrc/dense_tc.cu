@@ -1198,21 +1198,26 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
 
 }  // namespace
 
+// Crossovers (measured at n = 10^4, R = 1024): the mxf4 path is ~350x the CSR step on a
+// dense SK instance and the general fp16-plane path ~42x, while their cost does not depend
+// on the density -- so they stay ahead down to a few percent density.  The n caps bound the
+// dense operands (packed fp4: n^2/2 bytes; two fp16 planes: 4 n^2 bytes).
 bool dense_eligible(const Problem* p, int64_t R) {
-    if (!p->uniform_magnitude || p->n < 256 || R < 128) return false;
+    if (!p->uniform_magnitude || p->n < 256 || p->n > 65536 || R < 128) return false;
     double density = (double)p->nnz / ((double)p->n * (double)p->n);
-    return density >= 0.25;
+    return density >= 0.02;
 }
 
 bool dense_sbm_fp16_ok(double q_cap, double amp) { return std::max(q_cap, amp) <= 16384.0; }
 
 // general (non-uniform) dense J on the tensor cores: no in-kernel energies
 bool dense_general_eligible(const Problem* p, int64_t R) {
-    if (p->uniform_magnitude || p->n < 512 || R < 128 || !(p->magnitude > 0)) return false;
+    if (p->uniform_magnitude || p->n < 512 || p->n > 32768 || R < 128 || !(p->magnitude > 0))
+        return false;
     if (const char* e = getenv("VXQ_DENSE_GENERAL"))
         if (atoi(e) == 0) return false;
     double density = (double)p->nnz / ((double)p->n * (double)p->n);
-    return density >= 0.25;
+    return density >= 0.05;
 }
 
 // Lazily build the fp16 planes of 2^e J (e: the largest scaled |J| stays below 2^15).

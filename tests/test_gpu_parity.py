@@ -525,3 +525,36 @@ def test_dense_general_j_sbm_short_horizon(n, R):
         ds = np.abs(s.x[:8] - Q)
         assert np.quantile(dq, 0.99) <= 3 * np.quantile(ds, 0.99) + 1e-5
         assert np.mean(r.states == s.states) >= 0.999
+
+
+def _random_pairs(n, density, seed):
+    rng = np.random.default_rng(seed)
+    iu, ju = np.triu_indices(n, 1)
+    keep = rng.random(len(iu)) < density
+    return rng, iu[keep], ju[keep]
+
+
+def test_dense_paths_selected_at_moderate_density():
+    """The tensor paths win far below full density (their cost does not depend on it), so
+    auto selects them down to a few percent: a 3 % uniform-|J| instance runs the mxf4 path
+    bit-exact with its fp32 emulation; a 10 % general-J instance runs the fp16-plane path
+    (one step within 2e-5 of the fp64 reference loop)."""
+    rng, iu, ju = _random_pairs(2048, 0.03, 31)
+    J = np.where(rng.random(len(iu)) < 0.5, -0.25, 0.25)
+    m = vxq.IsingModel.from_arrays(2048, iu, ju, J, h=rng.uniform(-1, 1, 2048), canonical=True)
+    r = vxq.run_pa(m, vxq.PaParams(steps=25, replicas=256, seed=4), want_state=True)
+    assert r.info["path"] == "dense"
+    X, M = _dense_pa_emulation(m, 256, 25, 4)
+    assert np.array_equal(r.x, X.astype(np.float64)) and np.array_equal(r.m, M.astype(np.float64))
+    assert np.array_equal(r.energies, O.energies_exact(m, r.states))
+
+    rng, iu, ju = _random_pairs(1024, 0.10, 32)
+    g = vxq.IsingModel.from_arrays(1024, iu, ju, rng.standard_normal(len(iu)),
+                                   h=rng.standard_normal(1024), canonical=True)
+    rg = vxq.run_pa(g, vxq.PaParams(steps=1, replicas=128, seed=6), want_state=True)
+    assert rg.info["path"] == "dense"
+    ip, ix, dv = O.symmetric_csr(g.n, g.rows, g.cols, g.values)
+    Xg, Mg = O.pa_run(ip, ix, dv, g.h, O.pa_schedule(O.resolve_lambda0(g), 1), 0.05, 0.9,
+                      O.pa_init(6, 8, g.n), np.zeros((8, g.n)))
+    assert np.abs(rg.x[:8] - Xg).max() <= 2e-5
+    assert np.array_equal(rg.energies, O.energies_exact(g, rg.states))
