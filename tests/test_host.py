@@ -99,3 +99,13 @@ def test_use_in_reference_patches_every_lookup(monkeypatch):
     harness.use_in_reference(pkg, restore=True)
     for m in [pkg, *subs.values()]:
         assert m.solve_pa == "solve_pa" and m.solve_sbm == "solve_sbm"
+
+
+def test_run_opts_stream_mapping():
+    """NULL = the library's own stream per call; a caller's legacy default stream (handle
+    0, e.g. torch's default current stream) becomes cudaStreamLegacy so work is ordered on
+    it (three row-partition sessions on one stream must not race)."""
+    from paper_2501_19221_b200.solvers import _opts
+    assert _opts("fp32", "auto", 0).stream is None
+    assert _opts("fp32", "auto", 0, stream=0).stream == 0x1
+    assert _opts("fp32", "auto", 0, stream=0x7f00).stream == 0x7f00
