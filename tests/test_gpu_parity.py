@@ -558,3 +558,22 @@ def test_dense_paths_selected_at_moderate_density():
                       O.pa_init(6, 8, g.n), np.zeros((8, g.n)))
     assert np.abs(rg.x[:8] - Xg).max() <= 2e-5
     assert np.array_equal(rg.energies, O.energies_exact(g, rg.states))
+
+
+def test_dense_sbm_fp16_range_fallbacks():
+    """|q| may leave the fp16 range (q_cap or init_noise beyond 2^14): the SK tensor path
+    then splits q into three exact bf16 planes, and general dense J (fp16 J and q planes
+    only) falls back to the CSR path -- both still track the fp64 restatement."""
+    m = sk_model(700, 6)
+    prm = vxq.SbmParams(steps=5, dt=0.05, replicas=200, seed=2, c0=0.02, q_cap=1e5)
+    r = vxq.run_sbm(m, prm, want_state=True)
+    assert r.info["path"] == "dense"
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    Q, P = O.sbm_init(2, 8, m.n, 1.0)
+    Q, P = O.sbm_run(ip, ix, -dv, -m.h, O.sbm_schedule(1.0, 5), 0.05, 1.0, 0.02, 1e5, Q, P)
+    assert np.abs(r.x[:8] - Q).max() <= 1e-4
+    g = gen_complete(24, 600)
+    rg = vxq.run_sbm(g, vxq.SbmParams(steps=5, dt=0.05, replicas=128, seed=3, c0=0.01,
+                                      init_noise=3e4), want_state=True)
+    assert rg.info["path"] == "sparse"
+    assert np.array_equal(rg.energies, O.energies_exact(g, rg.states))
