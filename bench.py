@@ -19,6 +19,9 @@ the job value is N * R * n * T / max-over-ranks time.
           bytes * units per launch / mean launch time (library CUDA events).
   cpu_baseline  the oracle's C port (1 thread) timed on a bounded sample (fewer
           replicas / steps of the same instance) on this host, rank 0 at N=1.
+  time_to_target  (cfg2) first step whose best replica (min over all ranks) reaches
+          E/N <= -0.70 in a traced solve, at the measured per-step cost; the same for
+          shorter annealing schedules (reference defaults otherwise), best_ms = fastest.
 
 --impl reference runs the unmodified reference (baseline/_ref/qubokit) on a bounded
 sample of the same workload: its own IsingModel, coupling_operator() and sign_pm,
