@@ -406,19 +406,16 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         for (int u = 0; u < 4; ++u)
             qv[u] = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j[u] * R_pad + off);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            T c[V];
-            scale_into(c, a[u], qv[u].v);
-            acc_add(f, c);
-        }
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a[u], qv[u].v[b]));
     }
     for (; k < k1; ++k) {
         int j = __ldg(op.indices + k);
         T a = O::mul(op.sign, __ldg(op.data + k));
         Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j * R_pad + off);
-        T c[V];
-        scale_into(c, a, qv.v);
-        acc_add(f, c);
+#pragma unroll
+        for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a, qv.v[b]));
     }
     Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(q_in + base);
     Vec<T, V> pv = ld_cs<T, V>(p + pbase);

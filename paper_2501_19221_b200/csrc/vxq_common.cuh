@@ -96,58 +96,6 @@ struct Ops<double> {
     static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 };
 
-// f[b] += c[b] for b < N, each a round-to-nearest fp32/fp64 add (bit-identical to
-// Ops<T>::add).  fp32 pairs issue as one sm_100 packed FADD2 (add.rn.f32x2: each half is
-// the IEEE result of the scalar add).  Used by the SBM step (FMUL2 + FADD2 per replica
-// pair: cfg3 146.7 -> 143.1 us/step, cfg4 1212 -> 1207); the PA step keeps scalar adds
-// (its select-per-value inner loop measured 0.7 % slower with FADD2 on cfg4).
-#ifndef VXQ_F32X2
-#define VXQ_F32X2 1
-#endif
-template <typename T, int N>
-__device__ __forceinline__ void acc_add(T (&f)[N], const T (&c)[N]) {
-#pragma unroll
-    for (int b = 0; b < N; ++b) f[b] = Ops<T>::add(f[b], c[b]);
-}
-#if VXQ_F32X2
-__device__ __forceinline__ void add2_rn(float& x0, float& x1, float y0, float y1) {
-    asm("{\n\t.reg .b64 ra, rb;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rb, {%2, %3};\n\t"
-        "add.rn.f32x2 ra, ra, rb;\n\tmov.b64 {%0, %1}, ra;\n\t}"
-        : "+f"(x0), "+f"(x1)
-        : "f"(y0), "f"(y1));
-}
-__device__ __forceinline__ void mul2_rn(float& d0, float& d1, float a0, float a1, float b0,
-                                        float b1) {
-    asm("{\n\t.reg .b64 ra, rb;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "mul.rn.f32x2 ra, ra, rb;\n\tmov.b64 {%0, %1}, ra;\n\t}"
-        : "=f"(d0), "=f"(d1)
-        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-template <int N>
-__device__ __forceinline__ void acc_add(float (&f)[N], const float (&c)[N]) {
-    if constexpr (N % 2 == 0) {
-#pragma unroll
-        for (int b = 0; b < N; b += 2) add2_rn(f[b], f[b + 1], c[b], c[b + 1]);
-    } else {
-#pragma unroll
-        for (int b = 0; b < N; ++b) f[b] = __fadd_rn(f[b], c[b]);
-    }
-}
-#endif
-// c[b] = a * q[b] (round-to-nearest; FMUL2 pairs for fp32)
-template <typename T, int N>
-__device__ __forceinline__ void scale_into(T (&c)[N], T a, const T (&q)[N]) {
-#if VXQ_F32X2
-    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
-#pragma unroll
-        for (int b = 0; b < N; b += 2) mul2_rn(c[b], c[b + 1], a, a, q[b], q[b + 1]);
-        return;
-    }
-#endif
-#pragma unroll
-    for (int b = 0; b < N; ++b) c[b] = Ops<T>::mul(a, q[b]);
-}
-
 // vector of V scalars (16-byte max)
 template <typename T, int V>
 struct alignas(sizeof(T) * V) Vec {

@@ -15,7 +15,8 @@ import pytest
 
 import oracle as O
 import paper_2501_19221_b200 as vxq
-from helpers import brute_force_min, gen_complete, maxcut_model, model_from_golden, sk_model
+from helpers import (brute_force_min, gen_complete, maxcut_model, model_from_golden,
+                     random_regular_edges, sk_model)
 
 pytestmark = pytest.mark.gpu
 
@@ -240,6 +241,26 @@ def test_maxcut_scaled_cfg4_matches_oracle_subset():
     cut = (m.num_couplings - r.energies) / 2
     assert np.all(cut == np.round(cut))
     assert np.array_equal(r.energies, O.energies_exact(m, r.states))
+
+
+@pytest.mark.parametrize("R", [64, 256])
+def test_sparse_sbm_wide_replicas_match_oracle_subset(R):
+    """Sparse SBM step with several replicas per lane (R >= 64: the vector widths cfg 3/4
+    run) equals the oracle's fp32 restatement bit for bit -- guards against any change
+    that lets the compiler contract the in-order a*q products and sums into FMAs."""
+    r_, c_ = random_regular_edges(20_000, 6, 7)
+    rng = np.random.default_rng(11)
+    m = vxq.IsingModel.from_arrays(20_000, r_, c_, rng.uniform(-1, 1, len(r_)),
+                                   h=rng.uniform(-1, 1, 20_000), canonical=True)  # inexact a*q
+    c0 = 0.3
+    s = vxq.run_sbm(m, vxq.SbmParams(steps=40, dt=0.05, replicas=R, seed=4, c0=c0),
+                    path="sparse", want_state=True)
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    Q, P = O.sbm_init(4, 8, m.n, 1.0)
+    Q, P = O.sbm_run(ip, ix, -dv, -m.h, O.sbm_schedule(1.0, 40), 0.05, 1.0, c0, 1.0, Q, P,
+                     np.float32)
+    assert np.array_equal(s.x[:8], Q.astype(np.float64))
+    assert np.array_equal(s.m[:8], P.astype(np.float64))
 
 
 def test_sk_dense_family_matches_oracle_subset():
