@@ -167,6 +167,9 @@ inline Dests<P> one_dest(P* ptr) {
 #ifndef VXQ_PA_LATE_XM
 #define VXQ_PA_LATE_XM 1
 #endif
+#ifndef VXQ_SBM_PTAIL
+#define VXQ_SBM_PTAIL 1  // cfg3 146 -> 141, cfg4 1208 -> 1185, cfg5 86.6 -> 82.6 ms (profiles/r01/ab_sbm_tail)
+#endif
 template <typename T, int V, int CPW, bool MULTI = false>
 __global__ void __launch_bounds__(256, MULTI ? 4 : VXQ_PA_MINB) k_pa_step(int64_t row0, int64_t nrows, int64_t R_pad,
                                                  Operator<T> op, const T* __restrict__ h,
@@ -410,6 +413,29 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
 #pragma unroll
             for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a[u], qv[u].v[b]));
     }
+#if VXQ_SBM_PTAIL
+    // the 1-3 remaining entries: one round of index loads, one of gathers (predicated)
+    if (k < k1) {
+        const int rem = (int)(k1 - k);
+        int j[3];
+        T a[3];
+        Vec<T, V> qv[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) {
+                j[u] = __ldg(op.indices + k + u);
+                a[u] = O::mul(op.sign, __ldg(op.data + k + u));
+            }
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) qv[u] = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j[u] * R_pad + off);
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem)
+#pragma unroll
+                for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a[u], qv[u].v[b]));
+    }
+#else
     for (; k < k1; ++k) {
         int j = __ldg(op.indices + k);
         T a = O::mul(op.sign, __ldg(op.data + k));
@@ -417,6 +443,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
 #pragma unroll
         for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a, qv.v[b]));
     }
+#endif
     Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(q_in + base);
     Vec<T, V> pv = ld_cs<T, V>(p + pbase);
     const T gi = __ldg(g + i);
