@@ -140,8 +140,9 @@ VXQ_API int vxq_problem_create(int64_t n, int64_t num_couplings, const int64_t* 
                        double offset, int device, vxq_problem** out);
 VXQ_API int vxq_problem_destroy(vxq_problem* p);
 /* Generate an instance directly on the device (no host arrays).
- * family 0 = "qubo_deg6": random QUBO with mean degree ~6 (three seeded circulant offsets
- * per variable, duplicates merged), Q ~ U[-1,1), converted like qubo_to_ising
+ * family 0 = "qubo_deg6": random QUBO with mean degree ~6 -- a random graph: for each
+ * variable i and c in {0,1,2} an independent Philox draw picks a partner j != i uniformly
+ * (duplicates merged), Q ~ U[-1,1), converted like qubo_to_ising
  * (transforms.py:36-56) -- BASELINE config 5 at n = 2e8.  Definition: csrc/generate.cu. */
 VXQ_API int vxq_problem_generate(int32_t family, int64_t n, uint64_t seed, int device,
                                  vxq_problem** out);
@@ -149,11 +150,24 @@ VXQ_API int vxq_problem_generate(int32_t family, int64_t n, uint64_t seed, int d
  * rows/cols/values [num_couplings] (i<j, sorted), h [n], offset. */
 VXQ_API int vxq_problem_export(const vxq_problem* p, int64_t* rows, int64_t* cols,
                                double* values, double* h, double* offset);
-/* info: [n, num_couplings, nnz_sym, dense_eligible, uniform_magnitude] */
+/* info: [n, num_couplings, nnz_sym, max_row_nnz, uniform_magnitude] */
 VXQ_API int vxq_problem_info(const vxq_problem* p, int64_t* info5);
+/* *out = 1 if VXQ_PATH_AUTO would run an fp32 solve of `replicas` replicas on the tensor-core
+ * path (solver 0 = PA, 1 = SBM; q_cap / init_noise matter for SBM on general J only).
+ * Replica shards use it to choose the path once from the GLOBAL replica count, so every
+ * shard computes exactly the rows the single-GPU solve would. */
+VXQ_API int vxq_dense_eligible(const vxq_problem* p, int32_t solver, int64_t replicas,
+                               double q_cap, double init_noise, int32_t* out);
 
 VXQ_API int vxq_problem_lambda0(vxq_problem* p, double* out); /* max(field_scale, 1e-12) */
 VXQ_API int vxq_problem_c0(vxq_problem* p, double* out);      /* 1/lambda_max(-A) or 1.0 */
+/* How the automatic c0 was obtained (computes it if needed), eig_extreme(-A, "max")
+ * (solvers/eigen.py:35-56): info6 = [lambda_max returned, largest Ritz value theta,
+ * explicit residual ||B y - theta y|| / ||y||, Lanczos steps, method, c0]; method 0 = n <= 512
+ * exact (full-dimension Lanczos with full reorthogonalisation, as eigvalsh), 1 = Lanczos to
+ * ARPACK's tol 1e-8 and theta + residual, 2 = no convergence: Gershgorin bound.  Entries
+ * 0-4 are NaN / -1 for a coupling-free problem (c0 = 1). */
+VXQ_API int vxq_problem_eig_info(vxq_problem* p, double* info6);
 
 VXQ_API int vxq_pa_solve(vxq_problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts,
                  vxq_outputs* out);
@@ -183,8 +197,11 @@ VXQ_API int vxq_sbm_integrate(int64_t n, const int64_t* bt_indptr, const int32_t
  * globally row-indexed: PA = sign bits, SBM = q) that the caller all-gathers between steps
  * (e.g. NCCL all_gather over NVLink).  Buffer k & 1 holds state k: create() writes the
  * local rows of state 0; step(t) reads buffer t & 1 and writes the local rows of buffer
- * (t+1) & 1 on opts->stream.  finish() needs the final buffer complete on every row and
- * returns states/energies of all replicas (x/m outputs must be NULL).
+ * (t+1) & 1 on opts->stream; steps run in order.  finish() needs the buffer of the last
+ * state complete on every row and returns states/energies of all replicas after the steps
+ * taken (normally all T; after k < T steps: a snapshot of the T-step schedule, e.g. for
+ * short-horizon trajectory checks).  x/m outputs (PA X/M, SBM Q/P) only from a session
+ * over all rows [0, n).
  * solver: 0 = PA (pa params), 1 = SBM (sbm params).                                  */
 typedef struct vxq_session vxq_session;
 VXQ_API int vxq_exchange_row_bytes(int32_t solver, int64_t replicas, int32_t precision,

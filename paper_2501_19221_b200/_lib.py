@@ -37,6 +37,7 @@ EXPORTS = (
     "vxq_session_finish", "vxq_session_destroy", "vxq_problem_generate", "vxq_problem_export",
     "vxq_sa_solve", "vxq_sa_schedule", "vxq_session_set_peers", "vxq_exchange_alloc",
     "vxq_exchange_free", "vxq_ipc_handle", "vxq_ipc_open", "vxq_ipc_close",
+    "vxq_dense_eligible", "vxq_problem_eig_info",
 )
 IPC_HANDLE_BYTES = 64
 
@@ -92,8 +93,10 @@ def load():
         L.vxq_problem_generate.argtypes = [i32, i64, u64, ctypes.c_int, ctypes.POINTER(P)]
         L.vxq_problem_export.argtypes = [P, P, P, P, P, ctypes.POINTER(f64)]
         L.vxq_problem_info.argtypes = [P, P]
+        L.vxq_dense_eligible.argtypes = [P, i32, i64, f64, f64, ctypes.POINTER(i32)]
         L.vxq_problem_lambda0.argtypes = [P, ctypes.POINTER(f64)]
         L.vxq_problem_c0.argtypes = [P, ctypes.POINTER(f64)]
+        L.vxq_problem_eig_info.argtypes = [P, P]
         L.vxq_pa_solve.argtypes = [P, ctypes.POINTER(PaParamsC), ctypes.POINTER(RunOptsC),
                                    ctypes.POINTER(OutputsC)]
         L.vxq_sbm_solve.argtypes = [P, ctypes.POINTER(SbmParamsC), ctypes.POINTER(RunOptsC),

@@ -163,6 +163,37 @@ int vxq_problem_c0(vxq_problem* p, double* out) {
     });
 }
 
+int vxq_problem_eig_info(vxq_problem* p, double* info6) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && info6, "null argument");
+        DeviceGuard dg(p->p->device);
+        vxq::StreamScope ss(nullptr);
+        const double c0 = vxq::problem_c0(p->p, ss.s);
+        const vxq::EigInfo& e = p->p->eig;
+        info6[0] = e.value;
+        info6[1] = e.theta;
+        info6[2] = e.residual;
+        info6[3] = (double)e.iterations;
+        info6[4] = (double)e.method;
+        info6[5] = c0;
+    });
+}
+
+int vxq_dense_eligible(const vxq_problem* p, int32_t solver, int64_t replicas, double q_cap,
+                       double init_noise, int32_t* out) {
+    return guarded([&] {
+        VXQ_REQUIRE(p && out, "null argument");
+        VXQ_REQUIRE(solver == 0 || solver == 1, "solver must be 0 (PA) or 1 (SBM)");
+        VXQ_REQUIRE(replicas > 0, "replicas must be positive");
+        const vxq::Problem* P = p->p;
+        bool e;
+        if (P->uniform_magnitude) e = vxq::dense_eligible(P, replicas);
+        else e = vxq::dense_general_eligible(P, replicas) &&
+                 (solver == 0 || vxq::dense_sbm_fp16_ok(q_cap, init_noise));
+        *out = e ? 1 : 0;
+    });
+}
+
 int vxq_pa_solve(vxq_problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts,
                  vxq_outputs* out) {
     return guarded([&] {
@@ -331,7 +362,10 @@ int vxq_exchange_alloc(int device, int64_t bytes, void** out) {
         DeviceGuard dg(device);
         void* p = nullptr;
         VXQ_CUDA(cudaMalloc(&p, (size_t)bytes));  // plain cudaMalloc: IPC-shareable
+        // zeroing must be complete before the IPC handle reaches another process (peers
+        // write into this memory with no ordering against our stream)
         cudaError_t e = cudaMemset(p, 0, (size_t)bytes);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
             cudaFree(p);
             VXQ_CUDA(e);

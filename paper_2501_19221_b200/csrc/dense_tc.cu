@@ -42,7 +42,8 @@ constexpr int DA_BYTES = DBM * DROW;
 constexpr int DTHREADS = 352;  // TMA warp, MMA warp, 8 epilogue warps, x/m loader warp
 constexpr int RING_BYTES = 224 * 1024;  // operand stages + x/m staging slots
 constexpr int XM_SLOT_BYTES = 2 * 16 * DBM * 4;  // x and m of 16 replicas x 128 rows (fp32)
-constexpr int DSMEM = RING_BYTES + 1024 + 256;
+constexpr int DSMEM = RING_BYTES + 1024 + 512;
+constexpr int QN = 8;  // tile-ticket ring depth (dynamic tile queue, see k_dense_run)
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
 enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3, kJQ16 = 4 };
@@ -425,6 +426,7 @@ struct DenseRunArgs {
     long long* bestq;        // [R] lowest 2 sum K s s of s_0..s_{t-2} (LLONG_MAX initially)
     int8_t* best_s;          // [R][ld] best spins so far
     unsigned* decided;       // [T][n_tiles] tiles that made their step-(t-1) decisions
+    unsigned* ticket;        // [1] next tile of the dynamic queue (zeroed per launch)
 };
 
 // stats slots: 0 producer<-empty, 1 producer<-dependency, 2 mma<-full, 3 mma<-tempty,
@@ -515,7 +517,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     uint64_t* tempty = tfull + 2;
     uint64_t* xfull = tempty + 2;                                    // [XMS]
     uint64_t* xempty = xfull + (XMS > 0 ? XMS : 1);                  // [XMS]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + (XMS > 0 ? XMS : 1));
+    uint64_t* qfull = xempty + (XMS > 0 ? XMS : 1);                  // [QN] ticket ring
+    uint64_t* qempty = qfull + QN;                                   // [QN] (leader's used)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qempty + QN);
+    int* tq = reinterpret_cast<int*>(tmem_slot + 1);                 // [QN] tile tickets
     uint8_t* xm_smem = smem + STAGES * SBYTES;                       // XMS x XM_SLOT_BYTES
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -533,6 +538,15 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         for (int s = 0; s < XMS; ++s) {
             ptx::mbar_init(xfull + s, 1);
             ptx::mbar_init(xempty + s, 4);  // the 4 epilogue warps of one half
+        }
+        // ticket consumers (all arrive on the leader's qempty): per CTA 8 epilogue warps
+        // and the x/m loader (PA with staging), the MMA issuer(s) (pair: the leader's
+        // only), and every non-leader producer
+        const uint32_t xmc = (a.xm && a.mode == 0) ? 1u : 0u;
+        const uint32_t qcons = NCTA * (8u + xmc) + (PAIR ? 1u : (uint32_t)NCTA) + (NCTA - 1u);
+        for (int s = 0; s < QN; ++s) {
+            ptx::mbar_init(qfull + s, 1);
+            ptx::mbar_init(qempty + s, qcons);
         }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tmA);
@@ -562,7 +576,20 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         ptx::tc_fence_after();
     }
     const int crank = NCTA > 1 ? (int)ptx::cluster_ctarank() : 0;
-    const int wid0 = blockIdx.x / NCTA, wstride = gridDim.x / NCTA;  // cluster work index
+    // Dynamic tile queue: the leader CTA's TMA thread takes tile tickets in increasing
+    // order (atomicAdd on a.ticket) and hands each to every role of every CTA of its
+    // cluster through a QN-deep smem ring.  A tile only ever waits on tiles of the previous
+    // step -- lower tickets, already taken by running clusters -- so the schedule makes
+    // progress however many clusters are resident: no cooperative launch is needed.
+    auto next_ticket = [&](int k) -> int {  // consumers: ticket k (all lanes may call)
+        if constexpr (NCTA > 1) ptx::mbar_wait_cluster(qfull + (k % QN), (k / QN) & 1, a.timeout_ns);
+        else ptx::mbar_wait(qfull + (k % QN), (uint32_t)(k / QN) & 1u, a.timeout_ns);
+        return *reinterpret_cast<volatile int*>(tq + (k % QN));
+    };
+    auto release_ticket = [&](int k) {  // one arrival per consumer unit
+        if constexpr (NCTA > 1) ptx::mbar_arrive_cluster(ptx::cluster_addr(qempty + (k % QN), 0));
+        else ptx::mbar_arrive(qempty + (k % QN));
+    };
     const int mrows = (a.m_tiles + NCTA - 1) / NCTA;                 // row-block groups per step
     const int tps = mrows * a.n_tiles;                               // work items per step
     const int num_tiles = tps * a.T;
@@ -577,7 +604,27 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             long long st_empty = 0, st_dep = 0;
             int stage = 0;
             uint32_t ph = 0;
-            for (int g = wid0; g < num_tiles; g += wstride) {
+            for (int k = 0;; ++k) {
+                int g;
+                if (crank == 0) {  // take the next tile and hand it to the cluster
+                    g = (int)atomicAdd(a.ticket, 1u);
+                    if (g >= num_tiles) g = -1;
+                    const int qs = k % QN;
+                    ptx::mbar_wait(qempty + qs, ((uint32_t)(k / QN) & 1u) ^ 1u, a.timeout_ns);
+                    if constexpr (NCTA > 1) {
+                        for (int r = 0; r < NCTA; ++r) {
+                            ptx::st_cluster_s32(ptx::cluster_addr(tq + qs, (uint32_t)r), g);
+                            ptx::mbar_arrive_cluster(ptx::cluster_addr(qfull + qs, (uint32_t)r));
+                        }
+                    } else {
+                        tq[qs] = g;
+                        ptx::mbar_arrive(qfull + qs);
+                    }
+                } else {
+                    g = next_ticket(k);
+                    release_ticket(k);
+                }
+                if (g < 0) break;
                 int t, nb, mb;
                 decode_tile(a, g, tps, mrows, t, nb, mb);
                 mb = mb * NCTA + crank;
@@ -678,7 +725,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         uint32_t ph = 0;
         int lt = 0;
         long long mm_full = 0, mm_tempty = 0;
-        for (int g = wid0; g < num_tiles; g += wstride, ++lt) {
+        for (int k = 0;; ++k, ++lt) {
+            const int g = next_ticket(k);
+            __syncwarp();
+            if (lane == 0) release_ticket(k);
+            if (g < 0) break;
             const int acc = lt & 1;
             const uint32_t acc_ph = (lt >> 1) & 1;
             long long c0 = a.stats ? clk() : 0;
@@ -755,7 +806,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             const int nch = a.bn / 16;
             int slot = 0;
             uint32_t ph = 0;
-            for (int g = wid0; g < num_tiles; g += wstride) {
+            for (int k = 0;; ++k) {
+                const int g = next_ticket(k);
+                release_ticket(k);
+                if (g < 0) break;
                 int t, nb, mb;
                 decode_tile(a, g, tps, mrows, t, nb, mb);
                 mb = mb * NCTA + crank;
@@ -805,7 +859,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         float* __restrict__ mg = a.m;
         int lt = 0, xm_tiles = 0;
         long long ep_wait = 0, ep_busy = 0, ep_xwait = 0;
-        for (int g = wid0; g < num_tiles; g += wstride, ++lt) {
+        for (int k = 0;; ++k, ++lt) {
+            const int g = next_ticket(k);
+            __syncwarp();
+            if (lane == 0) release_ticket(k);
+            if (g < 0) break;
             int t, nb, mb;
             decode_tile(a, g, tps, mrows, t, nb, mb);
             mb = mb * NCTA + crank;
@@ -1175,12 +1233,13 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
         attrs[na].val.clusterDim.z = 1;
         ++na;
     }
-    // profiling knob: ncu cannot replay cluster + cooperative launches; with one CTA per SM
-    // (225 KB smem) and grid <= SM count every CTA is resident anyway
-    if (const char* e = getenv("VXQ_DENSE_NOCOOP"))
-        if (atoi(e) == 1) cooperative = false;
+    // The dynamic tile queue needs no co-residency, so the kernel launches as a plain
+    // (cluster) grid -- profilers can replay it.  VXQ_DENSE_COOP=1 adds the cooperative
+    // attribute anyway (A/B only).
+    cooperative = false;
+    if (const char* e = getenv("VXQ_DENSE_COOP"))
+        if (atoi(e) == 1) cooperative = true;
     if (cooperative) {
-        // all CTAs must be co-resident (they wait on each other's tiles): one per SM
         attrs[na].id = cudaLaunchAttributeCooperative;
         attrs[na].val.cooperative = 1;
         ++na;
@@ -1188,6 +1247,9 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
     cfg.attrs = attrs;
     cfg.numAttrs = na;
     VXQ_REQUIRE(!a.xm || (tmX && tmM), "x/m staging needs their tensor maps");
+    DevBuf<unsigned> ticket(1, s);
+    VXQ_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), s));
+    a.ticket = ticket.get();
     a.timeout_ns = 10ull * 1000 * 1000 * 1000;
     if (const char* e = getenv("VXQ_WAIT_TIMEOUT_S"))
         a.timeout_ns = (uint64_t)std::max(1, atoi(e)) * 1000ull * 1000 * 1000;

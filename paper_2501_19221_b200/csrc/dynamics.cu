@@ -1357,14 +1357,19 @@ __global__ void k_signal(const Dests<uint64_t> flags, int rank, uint64_t v) {
 }
 
 // wait until every source rank has published >= need; bounded (30 s), then reports
-// through *status instead of hanging the GPU
-__global__ void k_wait(const uint64_t* flags, int n, uint64_t need, int* status) {
+// through *status instead of hanging the GPU.  Once any wait has failed (status != 0) every
+// later wait returns at once: the host sees the status after at most one step
+// (session_step) instead of spinning 30 s per remaining step.
+__global__ void k_wait(const uint64_t* flags, int n, uint64_t need, volatile int* status) {
     if ((int)threadIdx.x >= n) return;
+    if (*status) return;
     const uint64_t t0 = global_ns();
     while (ld_acquire_sys(flags + threadIdx.x) < need) {
         __nanosleep(200);
+        if (*status) return;
         if (global_ns() - t0 > 30ull * 1000000000ull) {
-            atomicExch(status, 1);
+            *status = 1;
+            __threadfence_system();
             return;
         }
     }
@@ -1391,14 +1396,16 @@ struct Session {
     bool peers = false;
     Dests<void> pxb[2] = {};      // every rank's exchange buffers (own at [rank])
     Dests<uint64_t> pflags = {};  // every rank's flag array (own at [rank])
-    int* status = nullptr;        // device: 1 = peer wait timed out
+    int* status = nullptr;        // mapped pinned host word: 1 = a peer wait timed out
+    int* status_dev = nullptr;    // its device alias (written by k_wait)
     uint64_t epoch = 0;           // flag values are (epoch << 32) + state + 1
     int64_t row_bytes = 0;
+    int64_t done = 0;             // steps taken (step t must follow step t - 1)
     ~Session() {  // state from the retained stream-ordered pool (no unmapping)
         if (x) cudaFreeAsync(x, s);
         if (m) cudaFreeAsync(m, s);
-        if (status) cudaFreeAsync(status, s);
         if (s) cudaStreamSynchronize(s);
+        if (status) cudaFreeHost(status);
         if (own_stream && s) cudaStreamDestroy(s);
     }
 };
@@ -1442,8 +1449,13 @@ void session_step_t(Session* S, int64_t t) {
     const Layout& L = S->L;
     const int nb = (t + 1) & 1;
     if (S->peers) {  // state t complete on every rank
+        // a wait of an earlier step timed out (the host-mapped status word): fail now rather
+        // than launching the remaining steps on incomplete state
+        if (*(volatile int*)S->status)
+            throw Error(VXQ_ERR_CUDA, "row-partition exchange: a peer did not publish its "
+                                      "rows within 30 s");
         k_wait<<<1, 32, 0, S->s>>>(S->pflags.p[S->rank], S->world, S->epoch + (uint64_t)t + 1,
-                                   S->status);
+                                   S->status_dev);
         VXQ_CHECK_LAUNCH();
     }
     if (S->solver == 0) {
@@ -1478,30 +1490,35 @@ void session_finish_t(Session* S, int64_t T_, vxq_outputs* out, const vxq_run_op
     // full final state: PA sign bits / SBM q in buffer T & 1 (all rows, after the gather)
     if (S->peers) {
         k_wait<<<1, 32, 0, S->s>>>(S->pflags.p[S->rank], S->world, S->epoch + (uint64_t)T_ + 1,
-                                   S->status);
+                                   S->status_dev);
         VXQ_CHECK_LAUNCH();
-        int st = 0;
-        VXQ_CUDA(cudaMemcpyAsync(&st, S->status, sizeof(int), cudaMemcpyDeviceToHost, S->s));
         VXQ_CUDA(cudaStreamSynchronize(S->s));
-        if (st) throw Error(VXQ_ERR_CUDA, "row-partition exchange: a peer did not publish its "
+        if (*(volatile int*)S->status) throw Error(VXQ_ERR_CUDA, "row-partition exchange: a peer did not publish its "
                                           "rows within 30 s");
     }
     Layout F = S->L;
     F.row0 = 0;
     F.nrows = S->p->n;
+    // x/m (PA: X, M; SBM: Q, P) only from a session that owns every row
+    const bool all_rows = S->L.row0 == 0 && S->L.nrows == S->p->n;
+    VXQ_REQUIRE(all_rows || (!out->x && !out->m),
+                "x/m outputs need a session over all rows [0, n)");
     const uint32_t* sb = nullptr;
     DevBuf<uint32_t> tmp;
+    const T* xa = nullptr;
+    const T* ma = nullptr;
     if (S->solver == 0) {
         sb = (const uint32_t*)S->xb[T_ & 1];
+        xa = (const T*)S->x;
+        ma = (const T*)S->m;
     } else {
         tmp = DevBuf<uint32_t>(S->p->n * F.W, S->s);
         launch_pack<T>(F, (const T*)S->xb[T_ & 1], tmp.get(), S->s);
         sb = tmp.get();
+        xa = (const T*)S->xb[T_ & 1];
+        ma = (const T*)S->x;
     }
-    vxq_outputs o = *out;
-    o.x = nullptr;
-    o.m = nullptr;
-    finish_outputs<T>(S->p, F, sb, (const T*)nullptr, (const T*)nullptr, opts, &o, S->s);
+    finish_outputs<T>(S->p, F, sb, xa, ma, opts, out, S->s);
     out->loop_ms = 0;
     out->path_used = VXQ_PATH_SPARSE;
 }
@@ -1553,12 +1570,16 @@ Session* session_create(Problem* p, int solver, const vxq_pa_params* pa,
 
 void session_step(Session* S, int64_t t) {
     VXQ_REQUIRE(t >= 0 && t < (int64_t)S->sched.size(), "step index out of range");
+    VXQ_REQUIRE(t == S->done, "session steps must run in order 0, 1, ..., T-1");
     if (S->prec == VXQ_FP64) session_step_t<double>(S, t);
     else session_step_t<float>(S, t);
+    S->done = t + 1;
 }
 
 void session_finish(Session* S, vxq_outputs* out, const vxq_run_opts* opts) {
-    const int64_t T_ = (int64_t)S->sched.size();
+    // the state after the steps taken (normally all T; fewer = a snapshot of the T-step
+    // schedule after `done` steps)
+    const int64_t T_ = S->done;
     if (S->prec == VXQ_FP64) session_finish_t<double>(S, T_, out, opts);
     else session_finish_t<float>(S, T_, out, opts);
     out->lambda0_used = S->lam0;
@@ -1584,8 +1605,9 @@ void session_set_peers(Session* S, int world, int rank, uint32_t epoch, void* co
         S->pflags.p[k] = flags[k];
     }
     S->pxb[0].n = S->pxb[1].n = S->pflags.n = world;
-    VXQ_CUDA(cudaMallocAsync((void**)&S->status, sizeof(int), S->s));
-    VXQ_CUDA(cudaMemsetAsync(S->status, 0, sizeof(int), S->s));
+    VXQ_CUDA(cudaHostAlloc((void**)&S->status, sizeof(int), cudaHostAllocMapped));
+    *(volatile int*)S->status = 0;
+    VXQ_CUDA(cudaHostGetDevicePointer((void**)&S->status_dev, S->status, 0));
     // state 0 (written to the local rows by create) -> every peer, then publish it
     const int64_t off = S->L.row0 * S->row_bytes, bytes = S->L.nrows * S->row_bytes;
     for (int k = 0; k < world; ++k)

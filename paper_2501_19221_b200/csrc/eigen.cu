@@ -1,0 +1,480 @@
+// eigen.cu -- lambda_max of the SBM dynamics coupling matrix B = -A for the automatic c0.
+//
+// Restates eig_extreme(mat, "max") (solvers/eigen.py:35-56) as called by resolve_c0
+// (solvers/bifurcation.py:25-34), on the device:
+//   n <= 512 (DENSE_LIMIT, eigen.py:16,45-48): the reference takes the exact dense
+//       eigenvalue (np.linalg.eigvalsh).  Here: Lanczos with full reorthogonalisation
+//       (two classical Gram-Schmidt passes per step) run to the full dimension in one CTA,
+//       so the tridiagonal is orthogonally similar to B up to rounding, and its largest
+//       eigenvalue by Sturm bisection -- the exact value to a few ulps of ||B||.
+//   n > 512 (eigen.py:50-56): the reference runs ARPACK (k=1, 'LA', tol 1e-8) and returns
+//       theta + ||B v - theta v||, the Ritz value pushed outward by its residual.  Here:
+//       Lanczos without reorthogonalisation; every check computes the largest Ritz value
+//       theta of T_k and, by inverse iteration on T_k, the residual estimate
+//       |beta_k u_k| of its Ritz vector; converged when that is <= tol |theta| (ARPACK's
+//       criterion, tol 1e-8).  Then the recurrence is replayed from the same start vector
+//       (identical kernels => identical v_j) to assemble y = sum_j u_j v_j, and the
+//       returned value is theta + ||B y - theta y|| / ||y|| -- the explicit residual, as
+//       the reference computes it.
+//   No convergence within the iteration cap (eigen.py:49-52: ArpackNoConvergence): the
+//       Gershgorin bound max_i (B_ii + sum_{j!=i} |B_ij|) = max_i sum_j |A_ij|
+//       (eigen.py:21-32).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "vxq_internal.h"
+
+namespace vxq {
+
+namespace {
+
+constexpr int TB = 256;
+inline unsigned nblk(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, TB)); }
+
+constexpr int kDenseLimit = 512;       // eigen.py:16
+constexpr double kTol = 1e-8;          // eigen.py:17 (ARPACK tol)
+constexpr int64_t kMaxIter = 20000;    // Lanczos steps before the Gershgorin fallback
+
+__device__ __forceinline__ double start_entry(int64_t i) {
+    U64x4 o = philox4x64_10((uint64_t)i + 1, 0, 0x5eed, 0, 0x1a2b3c4dULL, 0);
+    return uniform_from_raw(o.v[0], -1.0, 2.0);
+}
+
+// ---------------------------------------------------------------- n <= 512: one CTA
+template <int NT>
+__device__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int k = 0; k < NT / 32; ++k) s += red[k];  // fixed order: deterministic
+    return s;
+}
+
+// Lanczos with full reorthogonalisation to dimension n: alpha[0..k), beta[0..k-1)
+// describe T_k; *kout = k.  V: [n][n] scratch (the Lanczos basis).
+__global__ void __launch_bounds__(kDenseLimit) k_lanczos_full(
+    int n, const int64_t* indptr, const int32_t* indices, const double* data, double sign,
+    double* V, double* alpha, double* beta, int* kout) {
+    __shared__ double v[kDenseLimit], w[kDenseLimit], c[kDenseLimit], red[kDenseLimit / 32];
+    const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+    constexpr int NW = kDenseLimit / 32;
+    double vi = i < n ? start_entry(i) : 0.0;
+    const double nrm = sqrt(block_sum<kDenseLimit>(vi * vi, red));
+    vi /= nrm;
+    v[i] = vi;
+    double vprev = 0.0, bprev = 0.0, scale = 0.0;
+    int k = 0;
+    while (k < n) {
+        if (i < n) V[(int64_t)k * n + i] = vi;
+        __syncthreads();
+        double wi = 0.0;
+        if (i < n) {
+            for (int64_t q = indptr[i]; q < indptr[i + 1]; ++q) wi += data[q] * v[indices[q]];
+            wi *= sign;
+        }
+        const double a = block_sum<kDenseLimit>(vi * wi, red);
+        wi = wi - a * vi - bprev * vprev;
+        for (int pass = 0; pass < 2; ++pass) {  // CGS2 against v_0..v_k
+            w[i] = wi;
+            __syncthreads();
+            for (int j = warp; j <= k; j += NW) {
+                double s = 0.0;
+                for (int l = lane; l < n; l += 32) s += V[(int64_t)j * n + l] * w[l];
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) c[j] = s;
+            }
+            __syncthreads();
+            if (i < n) {
+                double corr = 0.0;
+                for (int j = 0; j <= k; ++j) corr += c[j] * V[(int64_t)j * n + i];
+                wi -= corr;
+            }
+            __syncthreads();
+        }
+        const double b = sqrt(block_sum<kDenseLimit>(wi * wi, red));
+        if (i == 0) {
+            alpha[k] = a;
+            beta[k] = b;
+        }
+        ++k;
+        scale = fmax(scale, fabs(a) + b + bprev);
+        if (!(b > 1e-13 * scale)) break;  // invariant subspace: T_k is exact
+        vprev = vi;
+        vi = i < n ? wi / b : 0.0;
+        bprev = b;
+        v[i] = vi;
+    }
+    if (i == 0) *kout = k;
+}
+
+// ---------------------------------------------------------------- n > 512: kernels
+// y = sign * A x (warp per row)
+__global__ void k_spmv(int64_t n, const int64_t* indptr, const int32_t* indices,
+                       const double* data, double sign, const double* x, double* y) {
+    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    double acc = 0.0;
+    for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32)
+        acc += data[k] * x[indices[k]];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[row] = sign * acc;
+}
+
+constexpr int RB = 512;  // reduction blocks (fixed => deterministic)
+
+// part[b] = sum over this block's strided range of a[i]*b[i]  (b == nullptr: a[i]^2)
+// or, with theta given, of (a[i] - theta*b[i])^2
+__global__ void k_dot_partial(int64_t n, const double* a, const double* b, double* part,
+                              const double* theta) {
+    __shared__ double sh[TB];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)TB + threadIdx.x; i < n; i += (int64_t)TB * gridDim.x) {
+        if (theta) {
+            const double r = a[i] - (*theta) * b[i];
+            acc += r * r;
+        } else {
+            acc += a[i] * b[i];
+        }
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = TB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void k_sum_partials(int nb, const double* part, double* out, int root) {
+    __shared__ double sh[TB];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nb; i += TB) acc += part[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = TB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = root ? sqrt(sh[0]) : sh[0];
+}
+
+// w = w - alpha v - beta vprev  (alpha, beta device scalars)
+__global__ void k_axpy2(int64_t n, double* w, const double* v, const double* vp,
+                        const double* alpha, const double* beta) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) w[i] = w[i] - (*alpha) * v[i] - (*beta) * vp[i];
+}
+
+// y += u * v  (u device scalar)
+__global__ void k_axpy(int64_t n, double* y, const double* v, const double* u) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) y[i] += (*u) * v[i];
+}
+
+__global__ void k_scale_into(int64_t n, const double* w, const double* nrm, double* v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = w[i] / (*nrm);
+}
+
+__global__ void k_start_vec(int64_t n, double* v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = start_entry(i);
+}
+
+// eigenvalues of T_k below x (Sturm count)
+__device__ int sturm_count(int64_t k, const double* a, const double* b, double x) {
+    int c = 0;
+    double q = a[0] - x;
+    if (q < 0) ++c;
+    for (int64_t i = 1; i < k; ++i) {
+        double d = (q == 0.0) ? 1e-300 : q;
+        q = a[i] - x - b[i - 1] * b[i - 1] / d;
+        if (q < 0) ++c;
+    }
+    return c;
+}
+
+// largest eigenvalue of T_k: Gershgorin bracket, 256-way multisection, final bisection
+constexpr int kMS = 256;
+__global__ void __launch_bounds__(kMS) k_tridiag_max(int64_t k, const double* a, const double* b,
+                                                     double* out) {
+    __shared__ double s_lo, s_hi;
+    __shared__ int s_first;
+    if (threadIdx.x == 0) {
+        double lo = 1e300, hi = -1e300;
+        for (int64_t i = 0; i < k; ++i) {
+            double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < k - 1 ? fabs(b[i]) : 0.0);
+            lo = fmin(lo, a[i] - r);
+            hi = fmax(hi, a[i] + r);
+        }
+        s_lo = lo;
+        s_hi = hi;
+    }
+    __syncthreads();
+    for (int round = 0; round < 64; ++round) {
+        const double lo = s_lo, hi = s_hi;
+        const double x = lo + (hi - lo) * ((double)(threadIdx.x + 1) / (double)(kMS + 1));
+        if (threadIdx.x == 0) s_first = kMS;
+        __syncthreads();
+        const bool ok = x > lo && x < hi;
+        if (ok && sturm_count(k, a, b, x) >= k) atomicMin(&s_first, (int)threadIdx.x);
+        __syncthreads();
+        const int f = s_first;
+        const double xf = lo + (hi - lo) * ((double)(f + 1) / (double)(kMS + 1));
+        const double xp = lo + (hi - lo) * ((double)f / (double)(kMS + 1));
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const double nhi = f < kMS ? xf : hi;
+            const double nlo = f > 0 ? xp : lo;
+            s_lo = nlo > lo ? nlo : lo;
+            s_hi = nhi < hi ? nhi : hi;
+        }
+        __syncthreads();
+        if (!(s_hi - s_lo < hi - lo)) break;  // no progress: down to a few ulps
+    }
+    if (threadIdx.x == 0) {
+        double lo = s_lo, hi = s_hi;
+        for (int it = 0; it < 200; ++it) {
+            double mid = 0.5 * (lo + hi);
+            if (mid <= lo || mid >= hi) break;
+            if (sturm_count(k, a, b, mid) >= k) hi = mid;
+            else lo = mid;
+        }
+        *out = hi;
+    }
+}
+
+// Ritz vector of theta = lambda_max(T_k): two steps of inverse iteration with
+// M = (theta + delta) I - T_k, which is positive definite, so its LDL^T needs no pivoting
+// (delta grows tenfold if rounding leaves a non-positive pivot).  u[0..k) normalised;
+// out[0] = |beta_{k-1} u_{k-1}|, the residual norm ||B y - theta y|| of y = V_k u in exact
+// arithmetic (ARPACK's convergence estimate).  l, d: [k] scratch.
+__global__ void k_ritz_vector(int64_t k, const double* a, const double* b, const double* theta,
+                              double* u, double* l, double* d, double* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double tn = 0.0;
+    for (int64_t i = 0; i < k; ++i)
+        tn = fmax(tn, fabs(a[i]) + (i > 0 ? fabs(b[i - 1]) : 0.0) + (i + 1 < k ? fabs(b[i]) : 0.0));
+    double delta = 1e-11 * fmax(tn, 1e-300);
+    for (int attempt = 0; attempt < 8; ++attempt, delta *= 10.0) {
+        const double mu = *theta + delta;
+        bool ok = true;
+        d[0] = mu - a[0];
+        if (!(d[0] > 0)) ok = false;
+        for (int64_t i = 1; ok && i < k; ++i) {
+            l[i] = -b[i - 1] / d[i - 1];
+            d[i] = (mu - a[i]) - b[i - 1] * b[i - 1] / d[i - 1];
+            if (!(d[i] > 0)) ok = false;
+        }
+        if (!ok) continue;
+        for (int64_t i = 0; i < k; ++i) u[i] = 1.0;
+        for (int it = 0; it < 2; ++it) {
+            for (int64_t i = 1; i < k; ++i) u[i] -= l[i] * u[i - 1];  // L y = u
+            for (int64_t i = 0; i < k; ++i) u[i] /= d[i];             // D z = y
+            for (int64_t i = k - 2; i >= 0; --i) u[i] -= l[i + 1] * u[i + 1];  // L^T x = z
+            double s = 0.0;
+            for (int64_t i = 0; i < k; ++i) s += u[i] * u[i];
+            s = 1.0 / sqrt(s);
+            for (int64_t i = 0; i < k; ++i) u[i] *= s;
+        }
+        out[0] = fabs(b[k - 1] * u[k - 1]);
+        return;
+    }
+    out[0] = INFINITY;  // no usable factorisation: report "not converged"
+}
+
+// Gershgorin bound of B = -A (zero diagonal): max_i sum_j |A_ij|
+__global__ void k_row_abs_max(int64_t n, const int64_t* indptr, const double* data,
+                              unsigned long long* maxbits) {
+    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    double acc = 0.0;
+    for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32) acc += fabs(data[k]);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(acc));
+}
+
+template <typename T>
+T to_host(const T* dev, cudaStream_t s) {
+    T h;
+    VXQ_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+    VXQ_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+EigInfo eig_max_small(const Problem* p, double sign, cudaStream_t s) {
+    const int n = (int)p->n;
+    DevBuf<double> V((size_t)n * n, s), alpha(n, s), beta(n, s), theta(1, s);
+    DevBuf<int> kout(1, s);
+    k_lanczos_full<<<1, kDenseLimit, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, V.get(),
+                                            alpha.get(), beta.get(), kout.get());
+    VXQ_CHECK_LAUNCH();
+    const int k = to_host(kout.get(), s);
+    k_tridiag_max<<<1, kMS, 0, s>>>(k, alpha.get(), beta.get(), theta.get());
+    VXQ_CHECK_LAUNCH();
+    EigInfo r;
+    r.theta = r.value = to_host(theta.get(), s);
+    r.residual = 0.0;
+    r.iterations = k;
+    r.method = kEigDense;
+    return r;
+}
+
+struct Lanczos {
+    int64_t n;
+    const Problem* p;
+    double sign;
+    cudaStream_t s;
+    DevBuf<double> v0, v1, w, part, zero;
+    double* vp;
+    double* v;
+    unsigned spmv_blocks;
+
+    Lanczos(const Problem* p_, double sign_, cudaStream_t s_)
+        : n(p_->n), p(p_), sign(sign_), s(s_), v0(n, s_), v1(n, s_), w(n, s_), part(RB, s_),
+          zero(1, s_) {
+        spmv_blocks = (unsigned)ceil_div(n * 32, TB);
+        VXQ_CUDA(cudaMemsetAsync(zero.get(), 0, sizeof(double), s));
+    }
+
+    // v_0 = start / ||start||, vprev = 0
+    void start(double* nrm) {
+        vp = v0.get();
+        v = v1.get();
+        VXQ_CUDA(cudaMemsetAsync(vp, 0, n * sizeof(double), s));
+        k_start_vec<<<nblk(n), TB, 0, s>>>(n, w.get());
+        k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get(), nullptr);
+        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), nrm, 1);
+        k_scale_into<<<nblk(n), TB, 0, s>>>(n, w.get(), nrm, v);
+        VXQ_CHECK_LAUNCH();
+    }
+
+    // step k: w = B v_k - alpha_k v_k - beta_{k-1} v_{k-1}; beta_k = ||w||
+    void step(int64_t k, double* alpha, double* beta) {
+        k_spmv<<<spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, v, w.get());
+        k_dot_partial<<<RB, TB, 0, s>>>(n, v, w.get(), part.get(), nullptr);
+        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), alpha + k, 0);
+        k_axpy2<<<nblk(n), TB, 0, s>>>(n, w.get(), v, vp, alpha + k,
+                                       k > 0 ? beta + k - 1 : zero.get());
+        k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get(), nullptr);
+        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), beta + k, 1);
+        VXQ_CHECK_LAUNCH();
+    }
+
+    // v_{k+1} = w / beta_k
+    void advance(int64_t k, const double* beta) {
+        std::swap(vp, v);
+        k_scale_into<<<nblk(n), TB, 0, s>>>(n, w.get(), beta + k, v);
+        VXQ_CHECK_LAUNCH();
+    }
+};
+
+EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
+    const int64_t n = p->n;
+    int64_t cap = kMaxIter;
+    if (const char* e = getenv("VXQ_LANCZOS_MAXITER"))  // tests: force the fallback
+        cap = std::max<int64_t>(1, atoll(e));
+    const int64_t kmax = std::min<int64_t>(n, cap);
+    DevBuf<double> alpha(kmax + 1, s), beta(kmax + 1, s), nrm(1, s), theta(1, s), rho(1, s),
+        u(kmax + 1, s), l(kmax + 1, s), d(kmax + 1, s);
+    Lanczos lz(p, sign, s);
+    lz.start(nrm.get());
+    EigInfo r;
+    int64_t kk = -1;  // T_{kk} converged (size kk)
+    double th = 0.0;
+    int64_t next_check = 10, last_check = 0;
+    std::vector<double> hb;
+    for (int64_t k = 0; k < kmax; ++k) {
+        lz.step(k, alpha.get(), beta.get());
+        const bool last = k + 1 == kmax;
+        if (last || k + 1 == next_check) {
+            // an (almost) invariant subspace ends the recurrence at the first tiny beta
+            hb.resize(k + 1 - last_check);
+            VXQ_CUDA(cudaMemcpyAsync(hb.data(), beta.get() + last_check,
+                                     hb.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            VXQ_CUDA(cudaStreamSynchronize(s));
+            int64_t size = k + 1;
+            bool breakdown = false;
+            for (int64_t j = last_check; j <= k; ++j)
+                if (!(hb[j - last_check] > 1e-12)) {
+                    size = j + 1;
+                    breakdown = true;
+                    break;
+                }
+            k_tridiag_max<<<1, kMS, 0, s>>>(size, alpha.get(), beta.get(), theta.get());
+            k_ritz_vector<<<1, 32, 0, s>>>(size, alpha.get(), beta.get(), theta.get(), u.get(),
+                                           l.get(), d.get(), rho.get());
+            VXQ_CHECK_LAUNCH();
+            th = to_host(theta.get(), s);
+            const double res_est = breakdown ? 0.0 : to_host(rho.get(), s);
+            last_check = k + 1;
+            // check interval grows with k (at most ~6 % extra steps past convergence)
+            next_check = k + 1 + std::max<int64_t>(10, ((k + 1) / 16) / 10 * 10);
+            if (breakdown || res_est <= kTol * std::fabs(th)) {
+                kk = size;
+                break;
+            }
+        }
+        if (!last) lz.advance(k, beta.get());
+    }
+    if (kk < 0) {  // ArpackNoConvergence -> Gershgorin (eigen.py:49-52)
+        DevBuf<unsigned long long> mx(1, s);
+        VXQ_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned long long), s));
+        k_row_abs_max<<<(unsigned)ceil_div(n * 32, TB), TB, 0, s>>>(n, p->indptr, p->data64,
+                                                                     mx.get());
+        VXQ_CHECK_LAUNCH();
+        const unsigned long long bits = to_host(mx.get(), s);
+        double g;
+        memcpy(&g, &bits, 8);
+        r.value = g;
+        r.theta = th;
+        r.residual = NAN;
+        r.iterations = kmax;
+        r.method = kEigGershgorin;
+        return r;
+    }
+    // replay the recurrence (same kernels, same start => the same v_j) and assemble the
+    // Ritz vector y = sum_j u_j v_j, then the explicit residual ||B y - theta y|| / ||y||
+    DevBuf<double> y(n, s), by(n, s), ynrm(1, s), rnrm(1, s);
+    VXQ_CUDA(cudaMemsetAsync(y.get(), 0, n * sizeof(double), s));
+    DevBuf<double> alpha2(kk, s), beta2(kk, s);
+    lz.start(nrm.get());
+    for (int64_t j = 0; j < kk; ++j) {
+        k_axpy<<<nblk(n), TB, 0, s>>>(n, y.get(), lz.v, u.get() + j);
+        VXQ_CHECK_LAUNCH();
+        if (j + 1 == kk) break;
+        lz.step(j, alpha2.get(), beta2.get());
+        lz.advance(j, beta2.get());
+    }
+    k_spmv<<<lz.spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, y.get(),
+                                         by.get());
+    k_dot_partial<<<RB, TB, 0, s>>>(n, y.get(), y.get(), lz.part.get(), nullptr);
+    k_sum_partials<<<1, TB, 0, s>>>(RB, lz.part.get(), ynrm.get(), 1);
+    k_dot_partial<<<RB, TB, 0, s>>>(n, by.get(), y.get(), lz.part.get(), theta.get());
+    k_sum_partials<<<1, TB, 0, s>>>(RB, lz.part.get(), rnrm.get(), 1);
+    VXQ_CHECK_LAUNCH();
+    const double yn = to_host(ynrm.get(), s), rn = to_host(rnrm.get(), s);
+    r.theta = th;
+    r.residual = rn / yn;
+    r.value = th + r.residual;  // eigen.py:56: theta + residual for "max"
+    r.iterations = kk;
+    r.method = kEigLanczos;
+    return r;
+}
+
+}  // namespace
+
+EigInfo eig_max(const Problem* p, double sign, cudaStream_t s) {
+    if (p->n <= kDenseLimit) return eig_max_small(p, sign, s);
+    return eig_max_lanczos(p, sign, s);
+}
+
+}  // namespace vxq

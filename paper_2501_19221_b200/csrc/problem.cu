@@ -570,225 +570,12 @@ double problem_c0(Problem* p, cudaStream_t s) {
     if (!std::isnan(p->c0)) return p->c0;
     double c0 = 1.0;  // bifurcation.py:31-34
     if (p->m > 0) {
-        double lam = lanczos_lambda_max(p->n, p->indptr, p->indices, p->data64, -1.0, s);
+        p->eig = eig_max(p, -1.0, s);  // lambda_max(-A), eig_extreme(..., "max")
+        const double lam = p->eig.value;
         c0 = lam > 1e-12 ? 1.0 / lam : 1.0;
     }
     p->c0 = c0;
     return c0;
-}
-
-// ------------------------------------------------------------------ Lanczos
-namespace {
-
-// y = sign * A x (warp per row)
-__global__ void k_spmv(int64_t n, const int64_t* indptr, const int32_t* indices,
-                       const double* data, double sign, const double* x, double* y) {
-    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (row >= n) return;
-    double acc = 0.0;
-    for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32)
-        acc += data[k] * x[indices[k]];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) y[row] = sign * acc;
-}
-
-constexpr int RB = 512;  // reduction blocks (fixed => deterministic)
-
-__global__ void k_dot_partial(int64_t n, const double* a, const double* b, double* part) {
-    __shared__ double sh[TB];
-    double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)TB + threadIdx.x; i < n; i += (int64_t)TB * gridDim.x)
-        acc += a[i] * b[i];
-    sh[threadIdx.x] = acc;
-    __syncthreads();
-    for (int o = TB / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
-}
-
-__global__ void k_sum_partials(int nb, const double* part, double* out) {
-    __shared__ double sh[TB];
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < nb; i += TB) acc += part[i];
-    sh[threadIdx.x] = acc;
-    __syncthreads();
-    for (int o = TB / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *out = sh[0];
-}
-
-// w = w - alpha v - beta vprev  (alpha, beta device scalars)
-__global__ void k_axpy2(int64_t n, double* w, const double* v, const double* vp,
-                        const double* alpha, const double* beta) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) w[i] = w[i] - (*alpha) * v[i] - (*beta) * vp[i];
-}
-
-__global__ void k_scale_into(int64_t n, const double* w, const double* nrm2, double* v) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) v[i] = w[i] / sqrt(*nrm2);
-}
-
-__global__ void k_start_vec(int64_t n, double* v) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    U64x4 o = philox4x64_10((uint64_t)i + 1, 0, 0x5eed, 0, 0x1a2b3c4dULL, 0);
-    v[i] = uniform_from_raw(o.v[0], -1.0, 2.0);
-}
-
-// largest eigenvalue of the k x k symmetric tridiagonal (alpha, beta) by bisection
-__device__ int sturm_count(int k, const double* a, const double* b, double x) {
-    int c = 0;
-    double q = a[0] - x;
-    if (q < 0) ++c;
-    for (int i = 1; i < k; ++i) {
-        double d = (q == 0.0) ? 1e-300 : q;
-        q = a[i] - x - b[i - 1] * b[i - 1] / d;
-        if (q < 0) ++c;
-    }
-    return c;  // eigenvalues < x
-}
-
-__global__ void k_tridiag_max(int k, const double* a, const double* b, double* out) {
-    double lo = 1e300, hi = -1e300;
-    for (int i = 0; i < k; ++i) {
-        double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < k - 1 ? fabs(b[i]) : 0.0);
-        lo = fmin(lo, a[i] - r);
-        hi = fmax(hi, a[i] + r);
-    }
-    for (int it = 0; it < 200; ++it) {
-        double mid = 0.5 * (lo + hi);
-        if (mid <= lo || mid >= hi) break;
-        if (sturm_count(k, a, b, mid) >= k) hi = mid;  // all eigenvalues < mid
-        else lo = mid;
-    }
-    *out = hi;
-}
-
-// Same bracket, located by 256-way multisection (one Sturm count per thread and round)
-// before the final bisection steps: ~8 rounds instead of ~60 sequential bisections.
-constexpr int kMS = 256;
-__global__ void __launch_bounds__(kMS) k_tridiag_max_par(int k, const double* a, const double* b,
-                                                         double* out) {
-    __shared__ double s_lo, s_hi;
-    __shared__ int s_first;
-    if (threadIdx.x == 0) {
-        double lo = 1e300, hi = -1e300;
-        for (int i = 0; i < k; ++i) {
-            double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < k - 1 ? fabs(b[i]) : 0.0);
-            lo = fmin(lo, a[i] - r);
-            hi = fmax(hi, a[i] + r);
-        }
-        s_lo = lo;
-        s_hi = hi;
-    }
-    __syncthreads();
-    for (int round = 0; round < 64; ++round) {
-        const double lo = s_lo, hi = s_hi;
-        const double x = lo + (hi - lo) * ((double)(threadIdx.x + 1) / (double)(kMS + 1));
-        if (threadIdx.x == 0) s_first = kMS;
-        __syncthreads();
-        const bool ok = x > lo && x < hi;
-        if (ok && sturm_count(k, a, b, x) >= k) atomicMin(&s_first, (int)threadIdx.x);
-        __syncthreads();
-        const int f = s_first;
-        const double xf = lo + (hi - lo) * ((double)(f + 1) / (double)(kMS + 1));
-        const double xp = lo + (hi - lo) * ((double)f / (double)(kMS + 1));
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const double nhi = f < kMS ? xf : hi;
-            const double nlo = f > 0 ? xp : lo;
-            s_lo = nlo > lo ? nlo : lo;
-            s_hi = nhi < hi ? nhi : hi;
-        }
-        __syncthreads();
-        if (!(s_hi - s_lo < hi - lo)) break;  // no progress: down to a few ulps
-    }
-    if (threadIdx.x == 0) {
-        double lo = s_lo, hi = s_hi;
-        for (int it = 0; it < 200; ++it) {
-            double mid = 0.5 * (lo + hi);
-            if (mid <= lo || mid >= hi) break;
-            if (sturm_count(k, a, b, mid) >= k) hi = mid;
-            else lo = mid;
-        }
-        *out = hi;
-    }
-}
-
-__global__ void k_beta_sqrt(const double* nrm2, double* beta) { *beta = sqrt(*nrm2); }
-
-}  // namespace
-
-double lanczos_lambda_max(int64_t n, const int64_t* indptr, const int32_t* indices,
-                          const double* data, double sign, cudaStream_t s) {
-    const int kmax = (int)std::min<int64_t>(n, 600);
-    DevBuf<double> v0(n, s), v1(n, s), w(n, s), part(RB, s), alpha(kmax + 1, s),
-        beta(kmax + 1, s), nrm(1, s), theta(1, s);
-    double* vp = v0.get();
-    double* v = v1.get();
-    VXQ_CUDA(cudaMemsetAsync(vp, 0, n * sizeof(double), s));
-    VXQ_CUDA(cudaMemsetAsync(beta.get(), 0, (kmax + 1) * sizeof(double), s));
-    k_start_vec<<<nblk(n), TB, 0, s>>>(n, w.get());
-    k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get());
-    k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), nrm.get());
-    k_scale_into<<<nblk(n), TB, 0, s>>>(n, w.get(), nrm.get(), v);
-    VXQ_CHECK_LAUNCH();
-    DevBuf<double> zero(1, s);
-    VXQ_CUDA(cudaMemsetAsync(zero.get(), 0, sizeof(double), s));
-    double prev_theta = NAN, th = 0.0;
-    int k = 0;
-    const unsigned spmv_blocks = (unsigned)ceil_div(n * 32, TB);
-    for (k = 0; k < kmax; ++k) {
-        k_spmv<<<spmv_blocks, TB, 0, s>>>(n, indptr, indices, data, sign, v, w.get());
-        k_dot_partial<<<RB, TB, 0, s>>>(n, v, w.get(), part.get());
-        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), alpha.get() + k);
-        k_axpy2<<<nblk(n), TB, 0, s>>>(n, w.get(), v, vp, alpha.get() + k,
-                                       k > 0 ? beta.get() + k - 1 : zero.get());
-        k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get());
-        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), nrm.get());
-        // beta_k = sqrt(|w|^2) on the device (IEEE sqrt, as the host's): no per-iteration
-        // round trip; the betas are read back at the convergence checks (every 10)
-        k_beta_sqrt<<<1, 1, 0, s>>>(nrm.get(), beta.get() + k);
-        VXQ_CHECK_LAUNCH();
-        bool last = k + 1 == kmax;
-        if (last || (k + 1) % 10 == 0) {
-            // an (almost) invariant subspace inside this block ends the recurrence there:
-            // the steps after it are discarded
-            const int k0 = k - (k % 10);
-            double hb[10];
-            VXQ_CUDA(cudaMemcpyAsync(hb, beta.get() + k0, (k - k0 + 1) * sizeof(double),
-                                     cudaMemcpyDeviceToHost, s));
-            VXQ_CUDA(cudaStreamSynchronize(s));
-            int kk = k;
-            for (int j = k0; j <= k; ++j)
-                if (!(hb[j - k0] > 1e-12)) {
-                    kk = j;
-                    last = true;
-                    break;
-                }
-            k_tridiag_max_par<<<1, kMS, 0, s>>>(kk + 1, alpha.get(), beta.get(), theta.get());
-            VXQ_CHECK_LAUNCH();
-            VXQ_CUDA(cudaMemcpyAsync(&th, theta.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
-            VXQ_CUDA(cudaStreamSynchronize(s));
-            if (last) break;
-            if (!std::isnan(prev_theta) &&
-                std::fabs(th - prev_theta) <= 1e-13 * std::max(1.0, std::fabs(th)))
-                break;
-            prev_theta = th;
-        }
-        // v_{k+1} = w / beta_k ; rotate
-        std::swap(vp, v);  // vp <- v_k
-        k_scale_into<<<nblk(n), TB, 0, s>>>(n, w.get(), nrm.get(), v);
-        VXQ_CHECK_LAUNCH();
-    }
-    VXQ_CUDA(cudaStreamSynchronize(s));
-    return th;
 }
 
 }  // namespace vxq

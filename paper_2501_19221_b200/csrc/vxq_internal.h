@@ -17,6 +17,18 @@ constexpr int kMaxLimbs = 8;
 
 struct DenseOperand;  // dense tcgen05 path (dense_tc.cu)
 
+// lambda_max of the SBM coupling matrix (eigen.cu, eig_extreme "max")
+constexpr int kEigDense = 0;       // n <= 512: full-dimension Lanczos, full reorthogonalisation
+constexpr int kEigLanczos = 1;     // Lanczos to ARPACK's tol, theta + explicit residual
+constexpr int kEigGershgorin = 2;  // no convergence: Gershgorin bound
+struct EigInfo {
+    double value = NAN;     // what eig_extreme returns
+    double theta = NAN;     // largest Ritz value
+    double residual = NAN;  // ||B y - theta y|| / ||y|| (Lanczos)
+    int64_t iterations = 0;
+    int method = -1;
+};
+
 // A device-resident Ising problem (the reference's IsingModel, model.py:113-200).
 struct Problem {
     int device = 0;
@@ -53,6 +65,7 @@ struct Problem {
     std::mutex mu;  // guards the lazy caches below
     double lambda0 = NAN;
     double c0 = NAN;
+    EigInfo eig;      // how c0 was obtained (vxq_problem_eig_info)
     int h_zero = -1;  // cached problem_h_zero (-1 = unknown)
     DenseOperand* dense = nullptr;
 
@@ -132,9 +145,9 @@ Problem* problem_generate(int family, int64_t n, uint64_t seed, int device);
 void problem_export(Problem* P, int64_t* rows, int64_t* cols, double* values, double* h,
                     double* offset);
 double problem_c0(Problem* p, cudaStream_t s);
-// Lanczos lambda_max of the operator w_ij = sign * data[k] (row i lists field weights)
-double lanczos_lambda_max(int64_t n, const int64_t* indptr, const int32_t* indices,
-                          const double* data, double sign, cudaStream_t s);
+
+// ---- eigen.cu: lambda_max of the operator w_ij = sign * data[k] (eig_extreme "max")
+EigInfo eig_max(const Problem* p, double sign, cudaStream_t s);
 
 // ---- energy.cu
 // energies of bit-packed spins sb[n][W] (bit (r%32) of word r/32) for replicas r < R

@@ -49,6 +49,15 @@ class DeviceProblem:
         return {"n": int(out[0]), "num_couplings": int(out[1]), "nnz": int(out[2]),
                 "max_row_nnz": int(out[3]), "uniform_magnitude": bool(out[4])}
 
+    def dense_eligible(self, solver: str, replicas: int, q_cap: float = 1.0,
+                       init_noise: float = 1.0) -> bool:
+        """Would path="auto" run this fp32 solve on the tensor cores (vxq_dense_eligible)?"""
+        v = ctypes.c_int32()
+        _lib.check(_lib.load().vxq_dense_eligible(self.handle, 0 if solver == "pa" else 1,
+                                                  int(replicas), float(q_cap),
+                                                  float(init_noise), ctypes.byref(v)))
+        return bool(v.value)
+
     def lambda0(self) -> float:
         v = ctypes.c_double()
         _lib.check(_lib.load().vxq_problem_lambda0(self.handle, ctypes.byref(v)))
@@ -58,6 +67,16 @@ class DeviceProblem:
         v = ctypes.c_double()
         _lib.check(_lib.load().vxq_problem_c0(self.handle, ctypes.byref(v)))
         return v.value
+
+    def eig_info(self) -> dict:
+        """How the automatic c0 was obtained (vxq_problem_eig_info)."""
+        out = np.zeros(6)
+        _lib.check(_lib.load().vxq_problem_eig_info(self.handle, _lib.ptr(out)))
+        return {"lambda_max": float(out[0]), "theta": float(out[1]), "residual": float(out[2]),
+                "iterations": int(out[3]) if out[3] == out[3] else 0,
+                "method": {0: "dense-exact", 1: "lanczos", 2: "gershgorin"}.get(int(out[4]),
+                                                                                "none"),
+                "c0": float(out[5])}
 
     def close(self):
         self._finalizer()
@@ -105,6 +124,10 @@ def get_problem(model, device: int = 0, cache: bool = True) -> DeviceProblem:
         return model._dp
     if not cache:
         return DeviceProblem(model, device)
+    try:  # identity-keyed caching needs a finalizer on the model to drop the entry
+        weakref.ref(model)
+    except TypeError:  # no weakref support: a later object could reuse the id -> no cache
+        return DeviceProblem(model, device)
     key = (id(model), device)
     with _cache_lock:
         dp = _cache.get(key)
@@ -117,10 +140,7 @@ def get_problem(model, device: int = 0, cache: bool = True) -> DeviceProblem:
             dp.close()
             return existing
         _cache[key] = dp
-    try:
-        weakref.finalize(model, _drop, key)
-    except TypeError:  # model type without weakref support: keep until clear_cache()
-        pass
+    weakref.finalize(model, _drop, key)
     return dp
 
 

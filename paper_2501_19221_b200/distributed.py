@@ -2,7 +2,8 @@
 
 Replica r of a solve seeded with `seed` always draws from Philox stream r
 (solvers/common.py:1-6), so a rank that owns global replicas [b, e) computes exactly
-the rows the single-GPU run would (``replica_begin = b``) -- no per-step communication.
+the rows the single-GPU run would (``replica_begin = b``; the kernel path is chosen once
+from the global replica count, ``shard_path``) -- no per-step communication.
 The only data-path collective is the final merge: an all-gather of the per-rank
 (energy, global replica) keys and of the bit-packed states, followed by the reference's
 ordering (ascending energy, ties by replica index; common.py:57) on every rank.
@@ -93,6 +94,23 @@ def sharded_solve(local_solve: Callable[[int, int], tuple[np.ndarray, np.ndarray
                      info={"world": world, "rank": rank, "shard": (b, e)})
 
 
+def shard_path(model, solver: str, params, precision: str, path: str, device: int) -> str:
+    """The kernel path every shard runs, chosen ONCE from the global replica count.
+
+    path="auto" picks the tensor-core path only from R >= 128 replicas, so a shard's local
+    count could fall back to the CSR path and compute different (fp32-rounded differently)
+    rows than the single-GPU solve.  Resident and sparse are the same arithmetic, so only
+    the dense decision is pinned: if the global solve would run dense, every shard does."""
+    if path != "auto" or precision != "fp32":
+        return path
+    from .device import get_problem
+    dp = get_problem(model, device)
+    if dp.dense_eligible(solver, int(params.replicas), float(getattr(params, "q_cap", 1.0)),
+                         float(getattr(params, "init_noise", 1.0))):
+        return "dense"
+    return "auto"
+
+
 def solve_pa_sharded(model, params, group=None, precision: str = "fp32",
                      path: str = "auto") -> SampleSet:
     """PA over `params.replicas` global replicas split across the ranks of `group` (NCCL)."""
@@ -102,6 +120,7 @@ def solve_pa_sharded(model, params, group=None, precision: str = "fp32",
 
     params.validate()
     dev = torch.cuda.current_device()
+    path = shard_path(model, "pa", params, precision, path, dev)
 
     def local(begin, count):
         p = type(params)(**{**params.__dict__, "replicas": max(count, 1)})
@@ -120,6 +139,7 @@ def solve_sbm_sharded(model, params, group=None, precision: str = "fp32",
 
     params.validate()
     dev = torch.cuda.current_device()
+    path = shard_path(model, "sbm", params, precision, path, dev)
 
     def local(begin, count):
         p = type(params)(**{**params.__dict__, "replicas": max(count, 1)})

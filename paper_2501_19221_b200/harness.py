@@ -14,14 +14,38 @@ without the reference; ``time_to_target`` (solvers.py) reads the per-step energy
 
 from __future__ import annotations
 
+import functools
 import sys
 
 import numpy as np
 
 from . import solvers
-from .errors import ValidationError
+from .errors import QubokitError, ValidationError
 
 _NAMES = ("solve_pa", "solve_sbm", "solve_sa")
+
+
+def _translating(fn, qubokit):
+    """`fn` raising the reference's own exception classes (qubokit/errors.py) instead of
+    this package's, so the reference's `except` clauses see what they expect."""
+    ref_val = getattr(qubokit, "ValidationError", None)
+    ref_base = getattr(qubokit, "QubokitError", None)
+
+    @functools.wraps(fn)
+    def call(*a, **kw):
+        try:
+            return fn(*a, **kw)
+        except ValidationError as e:
+            if ref_val is None:
+                raise
+            raise ref_val(str(e)) from e
+        except QubokitError as e:
+            if ref_base is None:
+                raise
+            raise ref_base(str(e)) from e
+
+    call._vxq_wrapped = fn
+    return call
 
 
 def use_in_reference(qubokit, restore: bool = False) -> dict:
@@ -45,7 +69,7 @@ def use_in_reference(qubokit, restore: bool = False) -> dict:
                 else:
                     if not hasattr(m, f"_vxq_orig_{name}"):
                         setattr(m, f"_vxq_orig_{name}", prev[name])
-                    setattr(m, name, getattr(solvers, name))
+                    setattr(m, name, _translating(getattr(solvers, name), qubokit))
         saved[m.__name__] = prev
     return saved
 

@@ -102,14 +102,21 @@ class GpuSession:
         out.order = ctypes.c_void_p(order_ptr) if order_ptr else None
         _lib.check(_lib.load().vxq_session_finish(self.handle, ctypes.byref(out)))
 
-    def finish(self):
+    def finish(self, want_state: bool = False):
+        """States/energies/order after the steps taken; want_state (a session over all
+        rows only): also info["x"], info["m"] = X, M (PA) or Q, P (SBM) as (R, n) fp64."""
         st = np.empty((self.R, self.n), dtype=np.int8)
         en = np.empty(self.R)
         order = np.empty(self.R, dtype=np.int64)
         out = _lib.OutputsC()
         out.states, out.energies, out.order = _lib.ptr(st), _lib.ptr(en), _lib.ptr(order)
+        x = m = None
+        if want_state:
+            x = np.empty((self.R, self.n))
+            m = np.empty((self.R, self.n))
+            out.x, out.m = _lib.ptr(x), _lib.ptr(m)
         _lib.check(_lib.load().vxq_session_finish(self.handle, ctypes.byref(out)))
-        return st, en, order, {"lambda0": out.lambda0_used, "c0": out.c0_used}
+        return st, en, order, {"lambda0": out.lambda0_used, "c0": out.c0_used, "x": x, "m": m}
 
     def close(self):
         if self.handle:

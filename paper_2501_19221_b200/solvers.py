@@ -24,7 +24,6 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import json
-import math
 import time
 from dataclasses import dataclass, field
 from typing import NamedTuple
@@ -447,5 +446,3 @@ def sbm_schedule(a0: float, steps: int) -> np.ndarray:
     _lib.check(_lib.load().vxq_sbm_schedule(float(a0), int(steps), _lib.ptr(out)))
     return out
 
-
-_ = math  # keep import for type checkers

@@ -48,7 +48,8 @@ def test_reference_run_suite_with_b200_solvers(qk):
     for r in recs:
         assert r.gap <= 1e-9, (r.instance_id, r.solver_id, r.gap)
     # the records came from this package's solvers (wall time of GPU calls, exact energies)
-    assert qk.bench.solve_pa is vxq.solve_pa and qk.bench.solve_sa is vxq.solve_sa
+    assert qk.bench.solve_pa._vxq_wrapped is vxq.solve_pa
+    assert qk.bench.solve_sa._vxq_wrapped is vxq.solve_sa
 
 
 def test_reference_models_and_params_accepted_directly(qk):

@@ -95,10 +95,32 @@ def test_use_in_reference_patches_every_lookup(monkeypatch):
         setattr(pkg, name, name)
     harness.use_in_reference(pkg)
     for m in [pkg, *subs.values()]:
-        assert m.solve_pa is vxq.solve_pa and m.solve_sa is vxq.solve_sa
+        assert m.solve_pa._vxq_wrapped is vxq.solve_pa and m.solve_sa._vxq_wrapped is vxq.solve_sa
     harness.use_in_reference(pkg, restore=True)
     for m in [pkg, *subs.values()]:
         assert m.solve_pa == "solve_pa" and m.solve_sbm == "solve_sbm"
+
+
+def test_use_in_reference_translates_errors(monkeypatch):
+    """The product never imports the reference; swapped into it, our errors surface as the
+    reference's own classes (qubokit/errors.py) so its `except` clauses still catch them."""
+    import types
+    from paper_2501_19221_b200 import harness
+
+    class RefBase(Exception):
+        pass
+
+    class RefVal(RefBase, ValueError):
+        pass
+
+    pkg = types.ModuleType("fakeqk2")
+    pkg.QubokitError, pkg.ValidationError = RefBase, RefVal
+    pkg.solve_pa = pkg.solve_sbm = pkg.solve_sa = None
+    harness.use_in_reference(pkg)
+    with pytest.raises(RefVal):
+        pkg.solve_pa(None, vxq.PaParams(steps=0))
+    import paper_2501_19221_b200.errors as E
+    assert E.ValidationError.__module__ == "paper_2501_19221_b200.errors"
 
 
 def test_run_opts_stream_mapping():
