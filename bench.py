@@ -19,9 +19,11 @@ the job value is N * R * n * T / max-over-ranks time.
           bytes * units per launch / mean launch time (library CUDA events).
   cpu_baseline  the oracle's C port (1 thread) timed on a bounded sample (fewer
           replicas / steps of the same instance) on this host, rank 0 at N=1.
-  time_to_target  (cfg2) first step whose best replica (min over all ranks) reaches
-          E/N <= -0.70 in a traced solve, at the measured per-step cost; the same for
-          shorter annealing schedules (reference defaults otherwise), best_ms = fastest.
+  time_to_target  first step whose best replica (min over all ranks) reaches the target
+          (cfg2: E/N <= -0.75; cfg1/3/4: the reference's best energy at equal steps, from
+          the bit-exact fp64 path) in a traced solve, at the measured per-step cost; the
+          same for other annealing schedules (reference defaults otherwise), best_ms =
+          fastest.
 
 --impl reference runs the unmodified reference (baseline/_ref/qubokit) on a bounded
 sample of the same workload: its own IsingModel, coupling_operator() and sign_pm,
@@ -63,8 +65,14 @@ def parse():
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true")
+    ap.add_argument("--replica-split", action="store_true",
+                    help="split the config's replica count across the ranks (strong scaling, "
+                         "e.g. cfg3: 4096 = 8 x 512) instead of R per rank (weak scaling)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="cfg5 row partition at N>1: NCCL all-gather or fused peer stores")
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="cfg5 NCCL exchange pipelined over this many row chunks (1 = serial)")
     return ap.parse_args()
 
 
@@ -89,13 +97,38 @@ def measured_traffic(kernel: str, config: str):
     return None, None
 
 
-def _uniform(model, device) -> bool:
-    """All |J_ij| equal (the SK-family tensor path) -- else the general dense-J kernel."""
-    from paper_2501_19221_b200.device import get_problem
-    try:
-        return get_problem(model, device).info()["uniform_magnitude"]
-    except Exception:
-        return True
+# dense_kind -> (tcgen05 MMA kind, plane products issued per update, operand scheme)
+DENSE_KIND_INFO = {
+    "mxf4": ("mxf4", 1, "K and spins packed E2M1 (unit UE8M0 scales)"),
+    "f8f6f4": ("f8f6f4", 1, "K and spins as 8-bit floats"),
+    "i8x3": ("i8", 3, "K int8 x three int8 digit planes of the fixed-point q (exact field)"),
+    "f16x2": ("f16", 2, "K fp16 x two fp16 q planes"),
+    "bf16x3": ("f16", 3, "K bf16 x three bf16 q planes"),
+    "j16x2": ("f16", 2, "two fp16 planes of 2^e J x fp16 spins"),
+    "jq16": ("f16", 4, "two fp16 J planes x two fp16 q planes"),
+}
+MMA_PEAK_KEYS = {"mxf4": "e2m1", "f8f6f4": "e4m3", "i8": "s8", "f16": "bf16"}
+MMA_PEAK_MULT = {"mxf4": 4.0, "f8f6f4": 2.0, "i8": 2.0, "f16": 1.0}
+
+
+def mma_peak(mma_kind: str, bf16: float, src: str):
+    """Measured dense peak (TFLOP/s) of one tcgen05 MMA kind on CTA pairs (newest committed
+    profiles/r*/mma_peak.json, tools/mma_peak.cu), else a multiple of the bf16 peak."""
+    import glob
+    key = MMA_PEAK_KEYS[mma_kind]
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "mma_peak.json")),
+                       reverse=True):
+        for line in open(path):
+            line = line.strip()
+            if not line.startswith("{"):
+                continue
+            d = json.loads(line)
+            if d.get("kind", "").startswith(key):
+                return float(d["tflops"]), (f"measured kind::{mma_kind} peak on CTA pairs "
+                                            f"({os.path.relpath(path, ROOT)}, "
+                                            f"{d.get('sm_mhz_from_clock64')} MHz)")
+    mult = MMA_PEAK_MULT[mma_kind]
+    return mult * bf16, f"{mult:g} x measured bf16 sustained ({bf16} TF/s, {src})"
 
 
 def bytes_per_update(solver: str, dbar: float, R: int) -> float:
@@ -212,6 +245,120 @@ def cpu_baseline(model, solver, R, T):
                       f"same instance ({dt:.2f} s)"}
 
 
+# ----------------------------------------------------------------------------- time to target
+TTT_SWEEPS = {  # annealing schedules tried besides the timed one (reference defaults otherwise)
+    "cfg2": (500, 600, 700, 850, 2000, 5000, 10000, 20000),
+    "cfg1": (100, 200, 500), "cfg3": (100, 200, 500), "cfg4": (100, 200, 500),
+}
+
+
+def ttt_target(args, vxq, model, params, R_job, T, rbegin, local, world):
+    """(target energy, rule).  cfg2 (SK): energy density E/N <= -0.75 (J = +-1/sqrt N; the
+    Parisi ground state is ~-0.763), BASELINE.md 4.6.  cfg1/3/4: the reference's best energy
+    at equal steps on the same seed -- produced by this package's fp64 path, which is
+    bit-exact with the reference's CSR loop (tests/test_gpu_parity.py) -- so the target is
+    what the reference itself would reach with the same R, T and seed."""
+    import torch
+    import torch.distributed as dist
+    from paper_2501_19221_b200.solvers import run_pa, run_sbm
+    if args.config == "cfg2":
+        return -0.75 * model.n, "SK energy density E/N <= -0.75 (best replica of the job)"
+    if args.config not in ("cfg1", "cfg3", "cfg4"):
+        return None, None
+    fn = run_pa if args.solver == "pa" else run_sbm
+    ref = fn(model, params, precision="fp64", path="sparse" if model.n > 4096 else "auto",
+             device=local, replica_begin=rbegin)
+    best = torch.tensor([float(ref.energies.min())], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(best, op=dist.ReduceOp.MIN)
+    return float(best.item()), ("best final energy of the reference-equivalent fp64 solve "
+                                f"(same R={R_job}, T={T}, seed 0; bit-exact with the "
+                                "reference's CSR loop)")
+
+
+def time_to_target(args, vxq, model, params, R, R_job, T, rbegin, local, world, stream,
+                   flush, states, energies, order, solve_ms):
+    """First point at which the best replica of the job reaches the target energy.
+
+    For the timed schedule (T steps): a traced solve gives min_r E(s_t) for every step, so
+    the hit step t is timed as (t + 1) / T of the measured solve time.  Paths without a
+    per-step trace (dense SBM) count a hit only on the final states, at the whole solve's
+    time.  The same is done for other annealing schedules (TTT_SWEEPS; the reference's
+    defaults otherwise), each timed at its own measured solve cost (one untimed warm-up,
+    one timed solve); best_ms is the fastest hit."""
+    import torch
+    import torch.distributed as dist
+    from paper_2501_19221_b200.solvers import run_device, run_pa, run_sbm
+
+    target, rule = ttt_target(args, vxq, model, params, R_job, T, rbegin, local, world)
+    if target is None:
+        return None
+    fn = run_pa if args.solver == "pa" else run_sbm
+
+    def reduce_min(a):
+        a = np.nan_to_num(np.asarray(a, dtype=np.float64), nan=np.inf)
+        if world > 1:
+            tt = torch.tensor(a, dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MIN)
+            a = tt.cpu().numpy()
+        return a
+
+    def probe(ps):
+        """(hit step or None, steps, best energy seen, traced) for schedule ps."""
+        r = fn(model, ps, path=args.path, device=local, trace=True, replica_begin=rbegin)
+        tr = r.info["energy_trace"]
+        traced = tr is not None and not np.all(np.isnan(tr))
+        seq = np.append(tr if traced else np.full(ps.steps, np.inf), r.energies.min())
+        seq = reduce_min(seq)
+        hit = np.nonzero(seq <= target)[0]
+        return (int(hit[0]) if hit.size else None), ps.steps, float(seq.min()), traced
+
+    def timed(ps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            for w in range(2):
+                flush.fill_(w)
+                e0.record(stream)
+                run_device(args.solver, model, ps, states.data_ptr(), energies.data_ptr(),
+                           order_ptr=order.data_ptr(), stream=stream.cuda_stream,
+                           precision=args.precision, path=args.path, device=local,
+                           replica_begin=rbegin)
+                e1.record(stream)
+            torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+    out = {"target": target, "rule": rule}
+    hit, steps, best, traced = probe(params)
+    out.update({"steps": T, "step": hit, "best_energy_seen": best, "traced": traced,
+                "ms": (solve_ms * max(hit, 1) / T if traced else solve_ms)
+                if hit is not None else None})
+    sweep = []
+    for Ts in TTT_SWEEPS.get(args.config, ()):
+        if Ts == T:
+            continue
+        ps = make_params(vxq, args.solver, R, Ts, seed=0)
+        h, _, b, tr = probe(ps)
+        ent = {"steps": Ts, "step": h, "best_energy_seen": b}
+        if h is not None:
+            ms = timed(ps)
+            ent["solve_ms"] = ms
+            ent["ms"] = ms * max(h, 1) / Ts if tr else ms
+        sweep.append(ent)
+    out["schedule_sweep"] = sweep
+    cands = [(e["ms"], e["steps"]) for e in sweep if e.get("ms") is not None]
+    if out["ms"] is not None:
+        cands.append((out["ms"], T))
+    out["best_ms"], out["best_schedule_steps"] = min(cands) if cands else (None, None)
+    if not cands:
+        out["note"] = (f"target not reached by any schedule tried (best seen {best:.6g} at "
+                       f"T={T}; the schedules' best is in schedule_sweep)")
+    return out
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
@@ -268,17 +415,33 @@ def run_reference(args):
             P = np.stack([s.uniform(-1.0, 1.0, size=n) for s in streams])
             integrate(-A, -model.h, Q, P, 0.05, np.linspace(0.0, 1.0, T)[:Ts], 1.0, 0.5, 1.0)
 
+    def measure(nsteps):
+        times = []
+        for k in range(nsteps):
+            t0 = time.perf_counter()
+            one_step(100 + k)
+            times.append(time.perf_counter() - t0)
+        return float(np.sum(times))
+
     for w in range(args.warmup):
         one_step(w)
-    times = []
-    for k in range(args.steps):
-        t0 = time.perf_counter()
-        one_step(100 + k)
-        times.append(time.perf_counter() - t0)
-    dt = float(np.sum(times))
+    dt = measure(args.steps)
     units = Rs * n * Ts * args.steps
     v = units / dt
-    threads = os.environ.get("OPENBLAS_NUM_THREADS") or str(os.cpu_count())
+    # the same sample with ONE BLAS/OpenMP thread as well (scipy's CSR
+    # product is single-threaded either way; the dense dgemm path of n <= 2048 threads)
+    k1 = max(1, min(args.steps, 5))
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        threads = max([int(d.get("num_threads", 1)) for d in threadpool_info()] or [1])
+        with threadpool_limits(limits=1):
+            one_step(0)
+            dt1 = measure(k1)
+        one = {"value": Rs * n * Ts * k1 / dt1, "unit": "rv-updates/s", "cores": 1,
+               "steps": k1}
+    except Exception as e:  # noqa: BLE001
+        threads = os.cpu_count()
+        one = {"value": None, "note": f"threadpoolctl unavailable: {e}"}
     line = {
         "impl": "reference", "metric": "replica-variable updates/s", "value": v,
         "unit": "rv-updates/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -289,12 +452,14 @@ def run_reference(args):
                    "sample": f"{Rs} replicas x {Ts} steps per bench step"
                              + (f" on the same family at n={scaled} (host mirror of the "
                                 f"device generator)" if scaled else "")},
-        "cpu_baseline": {"value": v, "unit": "rv-updates/s", "cores": os.cpu_count(),
+        "cpu_baseline": {"value": v, "unit": "rv-updates/s", "cores": threads,
+                         "host_cpus": os.cpu_count(), "one_thread": one,
                          "kind": "reference",
                          "sample": (f"unmodified qubokit (baseline/_ref) "
                                     + ("solve_" + args.solver if args.config == "cfg1" else
                                        "loop lines with its own coupling_operator/sign_pm")
-                                    + f", {Rs} replicas x {Ts} steps, BLAS threads {threads}")},
+                                    + f", {Rs} replicas x {Ts} steps, BLAS threads {threads}"
+                                    + " (and 1 thread: one_thread)")},
         "e2e": {"value": v, "unit": "rv-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -332,8 +497,17 @@ def run_ours(args):
     model = instances.build(args.config, args.n)
     t_build = time.perf_counter() - t_build
     n = model.n
+    R_job = R * world  # weak scaling: rank g owns global replicas [gR, (g+1)R)
+    rbegin = rank * R
+    if args.replica_split:  # strong scaling: the config's R split across the ranks
+        from paper_2501_19221_b200.distributed import shard_path, shard_range
+        R_job = R
+        rbegin, rend = shard_range(R, world, rank)
+        if args.path == "auto":  # choose the kernel path once from the job's replica count
+            args.path = shard_path(model, args.solver, make_params(vxq, args.solver, R, T, 0),
+                                   args.precision, "auto", local)
+        R = rend - rbegin
     params = make_params(vxq, args.solver, R, T, seed=0)
-    rbegin = rank * R  # replica sharding: rank g owns global replicas [gR, (g+1)R)
 
     stream = torch.cuda.Stream()
     states = torch.empty((R, n), dtype=torch.int8, device="cuda")
@@ -345,41 +519,47 @@ def run_ours(args):
     if rowpart:
         # config 5: the instance is split by rows (strong scaling); every rank holds the
         # generated problem and all-gathers the bit-packed spins after each step (NCCL)
-        from paper_2501_19221_b200.rowpart import (GpuSession, PeerExchange, drive,
-                                                    exchange_row_bytes, gather_inplace,
-                                                    row_split)
+        from paper_2501_19221_b200.rowpart import (GpuSession, PeerExchange,
+                                                    chunked_row_split, drive_chunked,
+                                                    exchange_row_bytes, gather_chunk_async)
         rbegin = 0
-        spans, Bq = row_split(n, world)
         rbytes = exchange_row_bytes(args.solver, R, args.precision)
+        C = max(1, args.chunks) if args.exchange == "nccl" else 1
+        cspans, Bc = chunked_row_split(n, world, C)
+        rows_alloc = C * world * Bc
         px = None
         if args.exchange == "p2p":  # IPC-shared buffers, allocated once
-            px = PeerExchange(Bq * world * rbytes, world, rank, local)
+            px = PeerExchange(rows_alloc * rbytes, world, rank, local)
             xbufs = px.bufs()
         else:
-            xbufs = [torch.zeros(Bq * world * rbytes, dtype=torch.uint8, device="cuda")
+            xbufs = [torch.zeros(rows_alloc * rbytes, dtype=torch.uint8, device="cuda")
                      for _ in range(2)]
 
     def solve_dev():
         if rowpart:
-            sess = GpuSession(model, args.solver, params, spans[rank][0], spans[rank][1],
-                              Bq * world, xbufs, args.precision, local, stream.cuda_stream,
-                              outputs_on_device=True)
+            sessions = [GpuSession(model, args.solver, params, b, e, rows_alloc, xbufs,
+                                   args.precision, local, stream.cuda_stream,
+                                   outputs_on_device=True) for b, e in cspans[rank]]
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if px is not None:
-                px.attach(sess)  # the step kernels store into every rank's buffers
+                px.attach(sessions[0])  # the step kernels store into every rank's buffers
                 for t in range(T):
-                    sess.step(t)
-            else:
-                drive(sess, xbufs, T, lambda b: gather_inplace(b, rank, world, Bq * rbytes))
+                    sessions[0].step(t)
+            else:  # chunk c's all-gather overlaps chunk c+1's step (NCCL stream)
+                drive_chunked(sessions, xbufs, T,
+                              lambda v: gather_chunk_async(v, rank, world),
+                              world * Bc * rbytes)
             e1.record(stream)
-            sess.finish_device(states.data_ptr(), energies.data_ptr(), order.data_ptr())
-            sess.close()
+            sessions[0].finish_device(states.data_ptr(), energies.data_ptr(),
+                                      order.data_ptr())
+            for s_ in sessions:
+                s_.close()
             torch.cuda.synchronize()
             if px is not None:  # no rank reuses the buffers while a peer is still finishing
                 dist.barrier()
-            return {"loop_ms": e0.elapsed_time(e1), "launches": T + 4, "path": "rowpart"}
+            return {"loop_ms": e0.elapsed_time(e1), "launches": C * T + 4, "path": "rowpart"}
         return run_device(args.solver, model, params, states.data_ptr(), energies.data_ptr(),
                           order_ptr=order.data_ptr(), stream=stream.cuda_stream,
                           precision=args.precision, path=args.path, device=local,
@@ -410,78 +590,46 @@ def run_ours(args):
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = float(np.sum(step_ms))
+    # best energy of the last timed solve (before any later solve reuses the buffers)
+    best_timed = torch.tensor([energies.min().item()], dtype=torch.float64, device="cuda")
     t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         # final argmin reduce over replica shards (the only data-path collective)
-        best = torch.tensor([energies.min().item()], dtype=torch.float64, device="cuda")
-        dist.all_reduce(best, op=dist.ReduceOp.MIN)
+        dist.all_reduce(best_timed, op=dist.ReduceOp.MIN)
     tot_ms = float(t.item())
-    units = (1 if rowpart else world) * R * n * T * args.steps
+    units = (R if rowpart else R_job) * n * T * args.steps
     value = units / (tot_ms / 1e3)
 
     # roofline of the dominant kernel (per-step dynamics kernel)
     hbm, bf16, src = peaks()
     mean_step_kernel_ms = float(np.mean(loop_ms)) / T
     dbar = 2.0 * model.num_couplings / n
-    if info.get("path") == "dense" and args.solver == "sbm":
-        # SBM on the tensor cores: q enters as 2 fp16 terms (default) or 3 exact bf16 terms
-        # (VXQ_SBM_PLANES=3), kind::f16, so the kernel issues planes x 2N flops per update at
-        # the bf16 rate; useful work is 2N
-        planes = 3 if os.environ.get("VXQ_SBM_PLANES") == "3" else 2
-        if not _uniform(model, local):
-            planes = 4  # general dense J: 2 fp16 J planes x 2 fp16 q planes
-        flops = planes * 2.0 * n * R * n
-        achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
-        tr, tsrc = measured_traffic("k_dense_run_sbm", args.config)
-        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": tr, "traffic_unit": "bytes/step",
-                "traffic_source": tsrc,
-                "kernel": (f"k_dense_run<{ {3: 'bf16x3', 2: 'f16x2', 4: 'JQ16'}[planes] }>: "
-                           f"tcgen05.mma kind::f16, {planes} plane products per k-block + "
-                           "fused symplectic SBM epilogue (persistent)"),
-                "peak_note": f"measured bf16 sustained ({bf16} TF/s, {src})",
-                "flops_per_update_issued": planes * 2.0 * n, "flops_per_update_useful": 2.0 * n,
-                "useful_frac_of_fp8_peak": achieved / planes / (2.0 * bf16),
-                "units_per_launch": R * n, "mean_launch_ms": mean_step_kernel_ms}
-    elif info.get("path") == "dense" and not _uniform(model, local):
-        # general (non-uniform) dense J: J as two fp16 planes (kind::f16 on CTA pairs), so the
-        # kernel issues 2 x 2N flops per update at the bf16 rate; useful work is 2N
-        flops = 2 * 2.0 * n * R * n
-        achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
-        tr, tsrc = measured_traffic("k_dense_run_general", args.config)
-        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": tr, "traffic_unit": "bytes/step",
-                "traffic_source": tsrc,
-                "kernel": "k_dense_run<J16x2>: tcgen05.mma.cta_group::2 kind::f16, J as two "
-                          "fp16 planes x fp16 +-1 spins + fused PA epilogue (persistent)",
-                "peak_note": f"measured bf16 sustained ({bf16} TF/s, {src})",
-                "flops_per_update_issued": 4.0 * n, "flops_per_update_useful": 2.0 * n,
-                "units_per_launch": R * n, "mean_launch_ms": mean_step_kernel_ms}
-    elif info.get("path") == "dense":
-        # The default dense kernel issues tcgen05.mma kind::mxf4 (block-scaled E2M1, unit
-        # scales), which runs at 4x the dense bf16 rate on B200 (fp8 kinds: 2x).  The
-        # denominator is the measured bf16 number (MEASURED_PEAKS.json, sustained: the kernel
-        # runs inside a 1000-step loop) times 4; the fp8 and bf16 fractions are reported
-        # beside it.  VXQ_DENSE_MXF4=0 selects kind::f8f6f4 (peak 2 x bf16).
+    if info.get("path") == "dense":
+        # Tensor-core kernels: achieved = ALGORITHMIC flops (2N per replica-variable update,
+        # SURVEY 8d) / mean step time; peak = the measured dense peak of the MMA kind the
+        # kernel issues (tools/mma_peak.cu -> profiles/r*/mma_peak.json; else 4x / 2x / 1x
+        # the bf16 number of MEASURED_PEAKS.json for fp4 / 8-bit / 16-bit kinds).  Kinds that
+        # issue several plane products per update (digit / fp16 / bf16 planes) report
+        # issued_frac = planes x frac beside it.
+        kind = info.get("dense_kind") or "mxf4"
+        mma_kind, planes, what = DENSE_KIND_INFO[kind]
+        peak, peak_note = mma_peak(mma_kind, bf16, src)
         flops = 2.0 * n * R * n
         achieved = flops / (mean_step_kernel_ms / 1e3) / 1e12
-        mx = os.environ.get("VXQ_DENSE_MXF4", "1") != "0"
-        mult = 4.0 if mx else 2.0
-        peak = mult * bf16
-        tr, tsrc = measured_traffic("k_dense_run", args.config)
+        tkey = {"mxf4": "k_dense_run", "f8f6f4": "k_dense_run", "i8x3": "k_dense_run_sbm_i8",
+                "j16x2": "k_dense_run_general", "jq16": "k_dense_run_general_sbm"}.get(
+                    kind, "k_dense_run_sbm")
+        tr, tsrc = measured_traffic(tkey, args.config)
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": tr, "traffic_unit": "bytes/step",
-                "traffic_source": tsrc,
-                "kernel": ("k_dense_run: tcgen05.mma.cta_group::2 kind::" +
-                           ("mxf4 (packed e2m1 K and spins, unit ue8m0 scales)" if mx else
-                            "f8f6f4 (e2m1 operands unpacked by TMA)") +
-                           " J.S + fused PA epilogue (persistent, CTA pairs)"),
-                "peak_note": f"{mult:g} x measured bf16 sustained ({bf16} TF/s, {src})",
-                "frac_of_fp8_peak": achieved / (2.0 * bf16),
-                "frac_of_bf16_measured": achieved / bf16,
-                "flops_per_update": 2.0 * n, "units_per_launch": R * n,
-                "mean_launch_ms": mean_step_kernel_ms}
+                "frac": achieved / peak, "issued_frac": planes * achieved / peak,
+                "traffic": tr, "traffic_unit": "bytes/step", "traffic_source": tsrc,
+                "kernel": f"k_dense_run<{kind}>: tcgen05.mma.cta_group::2 kind::{mma_kind}, "
+                          f"{what} + fused {'PA' if args.solver == 'pa' else 'SBM'} epilogue "
+                          "(persistent, CTA pairs, dynamic tile queue)",
+                "peak_note": peak_note, "frac_of_bf16_measured": achieved / bf16,
+                "flops_per_update": 2.0 * n, "plane_products_per_update": planes,
+                "units_per_launch": R * n, "mean_launch_ms": mean_step_kernel_ms}
     else:
         B = bytes_per_update(args.solver, dbar, R)
         achieved = B * R * n / (mean_step_kernel_ms / 1e3) / 1e9
@@ -534,81 +682,16 @@ def run_ours(args):
         wt = torch.tensor([float(np.sum(walls))], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(wt, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * R * n * T * len(walls) / float(wt.item()),
+        e2e = {"value": R_job * n * T * len(walls) / float(wt.item()),
                "unit": "rv-updates/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "walls_ms": [round(1e3 * w, 2) for w in walls],
                "best_energy": float(ss.best.energy)}
 
-    # time-to-target (BASELINE metric): one traced solve outside the timed region; the
-    # per-step trace gives the first step whose best replica reaches the target, timed at
-    # the measured per-step cost of the timed solves
+    # time-to-target (BASELINE metric), outside the timed region
     ttt = None
-    if not rowpart:
-        target = {"cfg2": -0.70 * n}.get(args.config)
-        if target is not None:
-            from paper_2501_19221_b200.solvers import run_pa as _rp, run_sbm as _rs
-            fn = _rp if args.solver == "pa" else _rs
-            tr = fn(model, params, path=args.path, device=local, trace=True,
-                    replica_begin=rbegin).info["energy_trace"]
-            if world > 1:  # best replica of the whole job = min over the replica shards
-                tt = torch.tensor(np.nan_to_num(tr, nan=np.inf), dtype=torch.float64,
-                                  device="cuda")
-                dist.all_reduce(tt, op=dist.ReduceOp.MIN)
-                tr = tt.cpu().numpy()
-            step_ms = tot_ms / args.steps / T
-            if np.all(np.isnan(tr)):
-                ttt = {"target": target, "note": "no per-step energy trace on this path"}
-            else:
-                hit = np.nonzero(tr <= target)[0]
-                ttt = {"target": target, "rule": "SK energy density E/N <= -0.70 (best "
-                                                  "replica of the whole job)",
-                       "step": int(hit[0]) if hit.size else None,
-                       "ms": float(step_ms * (hit[0] + 1)) if hit.size else None,
-                       "best_trace_energy": float(np.nanmin(tr))}
-                # shorter annealing schedules (the reference's defaults except `steps`): the
-                # first step of each traced run that reaches the target, timed at that
-                # schedule's own measured per-step cost (one untimed warm-up + one timed solve)
-                sweep = []
-                for Ts in (500, 550, 600, 650, 700, 850):
-                    if Ts >= T:
-                        continue
-                    ps = make_params(vxq, args.solver, R, Ts, seed=0)
-                    trs = fn(model, ps, path=args.path, device=local, trace=True,
-                             replica_begin=rbegin).info["energy_trace"]
-                    if world > 1:
-                        tt = torch.tensor(np.nan_to_num(trs, nan=np.inf),
-                                          dtype=torch.float64, device="cuda")
-                        dist.all_reduce(tt, op=dist.ReduceOp.MIN)
-                        trs = tt.cpu().numpy()
-                    hs = np.nonzero(trs <= target)[0]
-                    ent = {"steps": Ts, "step": int(hs[0]) if hs.size else None,
-                           "best_trace_energy": float(np.nanmin(trs))}
-                    if hs.size:
-                        e0 = torch.cuda.Event(enable_timing=True)
-                        e1 = torch.cuda.Event(enable_timing=True)
-                        with torch.cuda.stream(stream):
-                            for w in range(2):
-                                flush.fill_(w)
-                                e0.record(stream)
-                                run_device(args.solver, model, ps, states.data_ptr(),
-                                           energies.data_ptr(), order_ptr=order.data_ptr(),
-                                           stream=stream.cuda_stream,
-                                           precision=args.precision, path=args.path,
-                                           device=local, replica_begin=rbegin)
-                                e1.record(stream)
-                            torch.cuda.synchronize()
-                        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
-                                          device="cuda")
-                        if world > 1:
-                            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-                        ent["ms"] = float(ms.item()) / Ts * (hs[0] + 1)
-                    sweep.append(ent)
-                ttt["schedule_sweep"] = sweep
-                cands = [(e["ms"], e["steps"]) for e in sweep if e.get("ms") is not None]
-                if ttt["ms"] is not None:
-                    cands.append((ttt["ms"], T))
-                if cands:
-                    ttt["best_ms"], ttt["best_schedule_steps"] = min(cands)
+    if not rowpart and not args.no_ttt:
+        ttt = time_to_target(args, vxq, model, params, R, R_job, T, rbegin, local, world,
+                             stream, flush, states, energies, order, tot_ms / args.steps)
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu and hasattr(model, "rows"):
@@ -619,17 +702,19 @@ def run_ours(args):
             "metric": "replica-variable updates/s", "value": value, "unit": "rv-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if rowpart else "weak",
+            "scaling": "strong" if (rowpart or args.replica_split) else "weak",
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic (seeded instance, see config)",
             "config": {"workload": f"{args.config}: {desc}", "solver": args.solver, "n": n,
                        "couplings": int(model.num_couplings), "replicas_per_gpu": R,
+                       "replicas_job": R_job,
                        "steps_per_solve": T, "path": info.get("path"),
                        "precision": args.precision,
                        "l2": "flushed between timed solves (256 MiB write)",
                        "parallelism": (f"row-partitioned x{world} ("
                                        + ("fused peer-memory stores" if args.exchange == "p2p"
-                                          else "NCCL all-gather")
+                                          else f"NCCL all-gather pipelined over {args.chunks} "
+                                               "row chunks")
                                        + " of spins "
                                        f"per step)" if rowpart else f"replica-sharded x{world}"),
                        "instance_build_s": round(t_build, 2)},
@@ -639,7 +724,7 @@ def run_ours(args):
             "time_to_target": ttt,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "best_energy": float(energies.min().item()),
+            "best_energy": float(best_timed.item()),
         }
         print(json.dumps(line))
     if world > 1:

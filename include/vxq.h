@@ -129,8 +129,18 @@ typedef struct {
     double loop_ms;      /* device time of the dynamics loop (CUDA events)   */
     int64_t launches;    /* kernels launched by this call                    */
     int32_t path_used;   /* VXQ_PATH_* actually run                          */
-    int32_t reserved;
+    int32_t dense_kind;  /* VXQ_DENSE_KIND_*: operand scheme of the tensor-core path */
 } vxq_outputs;
+
+/* tensor-core operand schemes (vxq_outputs.dense_kind) */
+#define VXQ_DENSE_KIND_NONE 0
+#define VXQ_DENSE_KIND_MXF4 1    /* PA, uniform |J|: K, spins packed E2M1, kind::mxf4       */
+#define VXQ_DENSE_KIND_F8F6F4 2  /* PA, uniform |J|: kind::f8f6f4 (VXQ_DENSE_MXF4=0)        */
+#define VXQ_DENSE_KIND_I8X3 3    /* SBM, uniform |J|: exact int8 digit planes, kind::i8     */
+#define VXQ_DENSE_KIND_F16X2 4   /* SBM, uniform |J|: two fp16 q planes (VXQ_SBM_PLANES=2)  */
+#define VXQ_DENSE_KIND_BF16X3 5  /* SBM, uniform |J|: three bf16 q planes (VXQ_SBM_PLANES=3) */
+#define VXQ_DENSE_KIND_J16X2 6   /* PA, general J: two fp16 J planes                        */
+#define VXQ_DENSE_KIND_JQ16 7    /* SBM, general J: two fp16 J x two fp16 q planes          */
 
 /* Build a device problem from the reference's canonical arrays:
  * rows/cols int64 with rows[k] < cols[k], sorted unique (model.py:81-104),

@@ -338,7 +338,6 @@ int vxq_session_finish(vxq_session* s, vxq_outputs* out) {
     return guarded([&] {
         VXQ_REQUIRE(s, "null session");
         check_outputs(out);
-        VXQ_REQUIRE(!out->x && !out->m, "session outputs: x/m must be NULL");
         SessionBox* b = reinterpret_cast<SessionBox*>(s);
         VXQ_CUDA(cudaSetDevice(b->device));
         vxq::session_finish(b->S, out, &b->opts);

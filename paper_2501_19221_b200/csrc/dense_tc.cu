@@ -5,9 +5,16 @@
 //   PA  (parallel_annealing.py:42-45): F = K.s with s in {-1,+1}; K and s are exact in FP8
 //       E4M3, the f32 TMEM accumulator holds the integer K.s exactly (|K.s| < 2^24), and
 //       f = c * (K.s) carries a single rounding.                     (Kind::kFp8, 1 plane)
-//   SBM (bifurcation.py:40-46): F = K.q with continuous fp32 q, split exactly into three
-//       bf16 terms q = q1 + q2 + q3 (8 + 8 + 8 significant bits); K.q1 + K.q2 + K.q3
-//       accumulate into one f32 TMEM accumulator (kind::f16).     (Kind::kBf16x3, 3 planes)
+//   SBM (bifurcation.py:40-46), default: F = K.q exactly in integers.  q is taken in fixed
+//       point, Q = rint(q * 2^S) (|Q| <= 2^22), written as three signed 8-bit digits
+//       Q = d0 + 2^8 d1 + 2^16 d2; K (int8) . d_p accumulate into three S32 TMEM
+//       accumulators (kind::i8, exact integer sums), combined in the epilogue as
+//       F = fp32(a0 + 2^8 a1 + 2^16 a2) * 2^-S (one rounding).  The tensor cores' f32
+//       accumulation of fractional fp16/bf16 products is not IEEE round-to-nearest and its
+//       error grows with n (profiles/r02/field_probe.txt); the integer path has none, so the
+//       result is bit-exact against a numpy emulation.            (Kind::kI8x3, 3 planes)
+//       Fallbacks (VXQ_SBM_PLANES=2/3 or |q| beyond 2^14): q as two fp16 / three exact bf16
+//       planes into one f32 accumulator (kind::f16).   (Kind::kF16x2 / Kind::kBf16x3)
 //
 //   F^T[i, r] = sum_j K[i, j] B[r, j]     M = n rows (i), N = replicas (r), K = n
 //   A = K  [ld][ld] K-major                 (TMA, SWIZZLE_128B, 128 rows x 128 B boxes)
@@ -46,7 +53,7 @@ constexpr int DSMEM = RING_BYTES + 1024 + 512;
 constexpr int QN = 8;  // tile-ticket ring depth (dynamic tile queue, see k_dense_run)
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
-enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3, kJQ16 = 4 };
+enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3, kJQ16 = 4, kI8x3 = 5 };
 
 template <Kind K>
 struct KindTraits;
@@ -90,6 +97,16 @@ struct KindTraits<Kind::kJQ16> {
     static constexpr uint32_t kIdescBase = (1u << 4);
 };
 
+// SBM exact default: K int8 (A) x three int8 digit planes of the fixed-point q (B), one S32
+// accumulator per plane (3 x bn <= 240 TMEM columns per buffer), CTA pairs only
+template <>
+struct KindTraits<Kind::kI8x3> {
+    static constexpr int kPlanes = 3, kAPlanes = 1, kStages = 3, kBnMax = 80, kElemBytes = 1;
+    static constexpr int kKPerMma = 32;  // i8: K = 32 per tcgen05.mma (32 B)
+    // D=S32 (2), A=B=signed int8 (1), K-major
+    static constexpr uint32_t kIdescBase = (2u << 4) | (1u << 7) | (1u << 10);
+};
+
 template <Kind K>
 constexpr int stage_bytes() {
     return DA_BYTES * KindTraits<K>::kAPlanes + KindTraits<K>::kPlanes * KindTraits<K>::kBnMax * DROW;
@@ -107,14 +124,16 @@ struct DenseOperand {
     __nv_bfloat16* K16 = nullptr;  // [ld][ld] bf16 in {-1, 0, +1} (SBM bf16x3, built lazily)
     __half* K16h = nullptr;        // [ld][ld] fp16 in {-1, 0, +1} (SBM f16x2, built lazily)
     __half* J16 = nullptr;         // [2][ld][ld] fp16 planes of 2^e J (general dense J)
+    int8_t* Ki8 = nullptr;         // [ld][ld] int8 in {-1, 0, +1} (SBM exact path, lazily)
     float jscale_inv = 0.f;        // 2^-e
     CUtensorMap tmJ;
-    CUtensorMap tmA8, tmA16, tmA16h;
+    CUtensorMap tmA8, tmA16, tmA16h, tmAi8;
     ~DenseOperand() {
         if (K8) cudaFreeAsync(K8, 0);  // back to the retained pool
         if (K16) cudaFreeAsync(K16, 0);
         if (K16h) cudaFreeAsync(K16h, 0);
         if (J16) cudaFreeAsync(J16, 0);
+        if (Ki8) cudaFreeAsync(Ki8, 0);
     }
 };
 
@@ -206,7 +225,7 @@ __global__ void k_build_sign_matrix(int64_t n, int64_t ld, const int64_t* __rest
                                     const int32_t* __restrict__ indices,
                                     const double* __restrict__ data, uint8_t* __restrict__ K8,
                                     __nv_bfloat16* __restrict__ K16, uint32_t* __restrict__ K4,
-                                    __half* __restrict__ K16h) {
+                                    __half* __restrict__ K16h, int8_t* __restrict__ Ki8) {
     int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -215,6 +234,7 @@ __global__ void k_build_sign_matrix(int64_t n, int64_t ld, const int64_t* __rest
         if (K8) K8[row * ld + indices[k]] = pos ? FP8_P1 : FP8_M1;
         if (K16) K16[row * ld + indices[k]] = __float2bfloat16_rn(pos ? 1.f : -1.f);
         if (K16h) K16h[row * ld + indices[k]] = __float2half_rn(pos ? 1.f : -1.f);
+        if (Ki8) Ki8[row * ld + indices[k]] = pos ? (int8_t)1 : (int8_t)-1;
         if (K4) {  // neighbours share bytes: OR the nibble into its 32-bit word
             const int64_t e = row * ld + indices[k];
             atomicOr(K4 + (e >> 3), (pos ? FP4_P1 : FP4_M1) << (4 * (e & 7)));
@@ -253,6 +273,19 @@ __device__ __forceinline__ void split3(float v, __nv_bfloat16& q1, __nv_bfloat16
     q2 = __float2bfloat16_rn(r1);
     const float r2 = __fsub_rn(r1, __bfloat162float(q2));
     q3 = __float2bfloat16_rn(r2);
+}
+
+// fixed-point digits of q for the exact SBM field: Q = rint(q * 2^S) (|Q| <= 2^22 by the
+// choice of S), Q = d0 + 2^8 d1 + 2^16 d2 with balanced signed digits d_p in [-128, 127]
+__device__ __forceinline__ void digits3(float q, float qscale, int8_t& d0, int8_t& d1,
+                                        int8_t& d2) {
+    const int Q = __float2int_rn(q * qscale);  // power-of-two scaling: exact, then rint
+    const int e0 = ((Q + 128) & 255) - 128;
+    const int r1 = (Q - e0) >> 8;
+    const int e1 = ((r1 + 128) & 255) - 128;
+    d0 = (int8_t)e0;
+    d1 = (int8_t)e1;
+    d2 = (int8_t)((r1 - e1) >> 8);
 }
 
 // 2-way fp16 split: v ~= h1 + h2 (h1 = fp16(v), h2 = fp16(v - h1); v - h1 is exact in fp32)
@@ -295,7 +328,7 @@ __global__ void k_init_pa_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, in
 // q0, p0 (stream r: n q-draws then n p-draws, as k_init_sbm) + the bf16 q-splits
 __global__ void k_init_sbm_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, int64_t rbegin,
                               double amp, float* __restrict__ q, float* __restrict__ p,
-                              void* __restrict__ planes_raw, int nplanes) {
+                              void* __restrict__ planes_raw, int nplanes, float qscale) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nq = (2 * n + 3) / 4;
     if (idx >= nq * R) return;
@@ -309,7 +342,14 @@ __global__ void k_init_sbm_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, i
         float v = (float)uniform_from_raw(o.v[w], lo, range);
         if (k < n) {
             q[r * ld + k] = v;
-            if (nplanes == 3) {
+            if (qscale > 0.f) {  // exact path: int8 digit planes
+                int8_t* planes = reinterpret_cast<int8_t*>(planes_raw);
+                int8_t a, b, c;
+                digits3(v, qscale, a, b, c);
+                planes[r * ld + k] = a;
+                planes[plane + r * ld + k] = b;
+                planes[2 * plane + r * ld + k] = c;
+            } else if (nplanes == 3) {
                 __nv_bfloat16* planes = reinterpret_cast<__nv_bfloat16*>(planes_raw);
                 __nv_bfloat16 a, b, c;
                 split3(v, a, b, c);
@@ -427,6 +467,7 @@ struct DenseRunArgs {
     int8_t* best_s;          // [R][ld] best spins so far
     unsigned* decided;       // [T][n_tiles] tiles that made their step-(t-1) decisions
     unsigned* ticket;        // [1] next tile of the dynamic queue (zeroed per launch)
+    float qscale, qscale_inv;  // kI8x3: 2^S and 2^-S of the fixed-point q
 };
 
 // stats slots: 0 producer<-empty, 1 producer<-dependency, 2 mma<-full, 3 mma<-tempty,
@@ -491,6 +532,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const __grid_constant__ CUtensorMap tmM, DenseRunArgs a) {
     using TR = KindTraits<KD>;
     static_assert(!PAIR || (KD != Kind::kBf16x3 && CL == 1), "pair MMA: f8f6f4 / f16x2, no B multicast");
+    static_assert(KD != Kind::kI8x3 || PAIR, "int8 digit planes: CTA pairs only");
     static_assert((KD != Kind::kJ16x2 && KD != Kind::kJQ16) || PAIR,
                   "general-J planes: CTA pairs only");
     constexpr int A_BYTES = DA_BYTES * TR::kAPlanes;  // A planes of one stage, back to back
@@ -752,6 +794,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 #pragma unroll
                         for (int k = 0; k < DROW / 32; ++k) {  // 32 B of K per MMA
                             const uint32_t accum = (kb | pl | k) != 0;
+                            if constexpr (KD == Kind::kI8x3) {  // one S32 accumulator per plane
+                                ptx::mma2_i8(d + pl * (uint32_t)a.bn, da + 2 * k, db + 2 * k,
+                                             idesc, (kb | k) != 0);
+                                continue;
+                            }
                             if constexpr (MX && PAIR)
                                 ptx::mma2_mxf4(d, da + 2 * k, db + 2 * k, idesc,
                                                tmem_base + kSfCol, tmem_base + kSfCol + 16,
@@ -941,8 +988,12 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const float st = __ldg(a.sched + t);
                 const float hi = row_ok ? __ldg(a.h + i) : 0.f;
                 auto process = [&](int c, const float* xo, const float* mo) {
-                    uint32_t v[16];
+                    uint32_t v[16], v1[16], v2[16];
                     ptx::tmem_ld_32x32b_x16(tbase + c * 16, v);
+                    if constexpr (KD == Kind::kI8x3) {  // the digit planes' accumulators
+                        ptx::tmem_ld_32x32b_x16(tbase + (uint32_t)a.bn + c * 16, v1);
+                        ptx::tmem_ld_32x32b_x16(tbase + 2u * (uint32_t)a.bn + c * 16, v2);
+                    }
                     const int r0 = nb * a.bn + c * 16;
                     const int64_t base = (int64_t)r0 * a.ld + i;
                     ptx::tmem_ld_wait();
@@ -950,7 +1001,16 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     for (int jj = 0; jj < 16; ++jj) {
                         const bool ok = row_ok && (r0 + jj) < a.R;
                         const int64_t off = base + (int64_t)jj * a.ld;
-                        const float f = O::mul(a.scale, __uint_as_float(v[jj]));
+                        float f;
+                        if constexpr (KD == Kind::kI8x3) {
+                            // K.Q exactly (|K.Q| < 2^37), rounded once to fp32, * 2^-S (exact)
+                            const long long kq = (long long)(int)v[jj] +
+                                                 256LL * (long long)(int)v1[jj] +
+                                                 65536LL * (long long)(int)v2[jj];
+                            f = O::mul(a.scale, __fmul_rn(__ll2float_rn(kq), a.qscale_inv));
+                        } else {
+                            f = O::mul(a.scale, __uint_as_float(v[jj]));
+                        }
                         if constexpr (PA_KIND) {
                             if (KD == Kind::kFp8 && a.qtrace) {  // exact energy of s_t
                                 const int kk = (int)__uint_as_float(v[jj]);
@@ -999,7 +1059,14 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             if (ok) {
                                 ptx::st_stream(xg + off, qn, stream);
                                 ptx::st_stream(mg + off, pn, stream);
-                                if constexpr (KD == Kind::kF16x2 || KD == Kind::kJQ16) {
+                                if constexpr (KD == Kind::kI8x3) {
+                                    int8_t d0, d1, d2;
+                                    digits3(qn, a.qscale, d0, d1, d2);
+                                    int8_t* pl = reinterpret_cast<int8_t*>(nxt);
+                                    pl[off] = d0;
+                                    pl[a.plane_elems + off] = d1;
+                                    pl[2 * a.plane_elems + off] = d2;
+                                } else if constexpr (KD == Kind::kF16x2 || KD == Kind::kJQ16) {
                                     __half q1, q2;
                                     split2(qn, q1, q2);
                                     __half* pl = reinterpret_cast<__half*>(nxt);
@@ -1272,6 +1339,17 @@ bool dense_eligible(const Problem* p, int64_t R) {
 
 bool dense_sbm_fp16_ok(double q_cap, double amp) { return std::max(q_cap, amp) <= 16384.0; }
 
+// S of the exact SBM path's fixed-point q (Q = rint(q 2^S), |Q| <= 2^22): the largest S with
+// max(q_cap, init_noise) <= 2^(22-S); -1 if |q| is unbounded (q_cap = inf) or out of range
+int sbm_fixed_point_shift(double q_cap, double amp) {
+    const double b = std::max(q_cap, amp);
+    if (!(b > 0) || !std::isfinite(b)) return -1;
+    int e = 0;
+    const double m = std::frexp(b, &e);  // b = m 2^e, m in [0.5, 1)
+    const int ceil_log2 = (m == 0.5) ? e - 1 : e;
+    return 22 - ceil_log2;
+}
+
 // general (non-uniform) dense J on the tensor cores: no in-kernel energies
 bool dense_general_eligible(const Problem* p, int64_t R) {
     if (p->uniform_magnitude || p->n < 512 || p->n > 32768 || R < 128 || !(p->magnitude > 0))
@@ -1319,7 +1397,7 @@ static DenseOperand* dense_jplanes(Problem* p, cudaStream_t s) {
 }
 
 // Lazily build the sign matrix K (fp8 for PA/energies, bf16 for SBM) and its TMA maps.
-// need16: 0 none, 1 bf16 K (SBM bf16x3), 2 fp16 K (SBM f16x2)
+// need16: 0 none, 1 bf16 K (SBM bf16x3), 2 fp16 K (SBM f16x2), 3 int8 K (SBM exact)
 DenseOperand* dense_operand(Problem* p, cudaStream_t s, int need16) {
     std::lock_guard<std::mutex> g(p->mu);
     if (!p->uniform_magnitude)
@@ -1338,6 +1416,13 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, int need16) {
         __nv_bfloat16* k16 = nullptr;
         __half* k16h = nullptr;
         uint32_t* k4 = nullptr;
+        int8_t* ki8 = nullptr;
+        if (need16 == 3 && !d->Ki8) {
+            VXQ_CUDA(cudaMallocAsync((void**)&d->Ki8, ld * ld, s));
+            VXQ_CUDA(cudaMemsetAsync(d->Ki8, 0, ld * ld, s));
+            ki8 = d->Ki8;
+            d->tmAi8 = make_map(d->Ki8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, ld, 1, DROW, DBM, 1);
+        }
         if (!d->K8) {
             // default: K as packed E2M1 (51 MB at n = 10^4: stays L2-resident, -60 % DRAM
             // traffic, higher clocks under the power cap); VXQ_DENSE_FP4=0 -> FP8 E4M3
@@ -1371,9 +1456,9 @@ DenseOperand* dense_operand(Problem* p, cudaStream_t s, int need16) {
             d->tmA16 = make_map(d->K16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ld, ld, 1, DROW / 2,
                                 DBM, 1);
         }
-        if (k8 || k16 || k4 || k16h) {
+        if (k8 || k16 || k4 || k16h || ki8) {
             k_build_sign_matrix<<<(unsigned)ceil_div(p->n * 32, TB), TB, 0, s>>>(
-                p->n, ld, p->indptr, p->indices, p->data64, k8, k16, k4, k16h);
+                p->n, ld, p->indptr, p->indices, p->data64, k8, k16, k4, k16h, ki8);
             VXQ_CHECK_LAUNCH();
             VXQ_CUDA(cudaStreamSynchronize(s));
         }
@@ -1422,6 +1507,9 @@ static void energy_pass(DenseOperand* d, const float* x, int64_t n, int64_t R, l
     VXQ_CUDA(cudaStreamSynchronize(s));
 }
 
+static thread_local int g_dense_kind = 0;  // VXQ_DENSE_KIND_* of this thread's last run
+int dense_last_kind() { return g_dense_kind; }
+
 static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap& tb0,
                        const CUtensorMap& tb1, int planes16, int cl, cudaStream_t s,
                        bool pair = false, const CUtensorMap* tmX = nullptr,
@@ -1434,6 +1522,12 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
         VXQ_CUDA(cudaMemsetAsync(stats.get(), 0, 9 * sizeof(unsigned long long), s));
         a.stats = stats.get();
     }
+    g_dense_kind = jplanes ? VXQ_DENSE_KIND_J16X2
+                   : jq ? VXQ_DENSE_KIND_JQ16
+                   : planes16 == 8 ? VXQ_DENSE_KIND_I8X3
+                   : planes16 == 3 ? VXQ_DENSE_KIND_BF16X3
+                   : planes16 == 2 ? VXQ_DENSE_KIND_F16X2
+                   : mx ? VXQ_DENSE_KIND_MXF4 : VXQ_DENSE_KIND_F8F6F4;
     cudaEvent_t e0, e1;
     VXQ_CUDA(cudaEventCreate(&e0));
     VXQ_CUDA(cudaEventCreate(&e1));
@@ -1442,6 +1536,7 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
         if (jplanes)
             launch_run<Kind::kJ16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
         else if (jq) launch_run<Kind::kJQ16, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (planes16 == 8) launch_run<Kind::kI8x3, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 3) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 2 && pair)
             launch_run<Kind::kF16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
@@ -1712,41 +1807,61 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                     int64_t* launches) {
     // general (non-uniform) J: J as two fp16 planes too (kJQ16, the caller checked the range)
     const bool general = !p->uniform_magnitude;
-    int planes = 2;
-    if (const char* e = getenv("VXQ_SBM_PLANES")) planes = atoi(e) == 3 ? 3 : 2;
-    if (!dense_sbm_fp16_ok(q_cap, amp)) planes = 3;  // fp16 max is 65504
+    // uniform |J|: exact integer field (kI8x3) when |q| <= max(q_cap, init_noise) <= 2^14;
+    // VXQ_SBM_PLANES=2 / 3 select the fp16 / bf16 plane paths (A/B, round 1)
+    const int S = sbm_fixed_point_shift(q_cap, amp);
+    int planes = (!general && S >= 8) ? 8 : 2;
+    if (const char* e = getenv("VXQ_SBM_PLANES")) {
+        const int v = atoi(e);
+        if (v == 2 || v == 3) planes = v;
+    }
+    if (planes == 2 && !dense_sbm_fp16_ok(q_cap, amp)) planes = 3;  // fp16 max is 65504
+    if (planes == 8 && ceil_div(p->n, DBM) < 2) planes = 2;  // pairs need two row tiles
+    const bool exact = planes == 8;
     VXQ_REQUIRE(!general || planes == 2, "general dense J on the tensor cores needs fp16 q");
-    DenseOperand* d = general ? dense_jplanes(p, s) : dense_operand(p, s, planes == 3 ? 1 : 2);
+    DenseOperand* d = general ? dense_jplanes(p, s)
+                              : dense_operand(p, s, exact ? 3 : (planes == 3 ? 1 : 2));
     const int64_t n = p->n, ld = d->ld, T = (int64_t)a_sched.size();
     const int64_t plane = R * ld;
+    const int nb_planes = exact ? 3 : planes;
+    const int esz = exact ? 1 : 2;
     DevBuf<float> q(R * ld, s), pm(R * ld, s);
-    DevBuf<uint16_t> b0(planes * plane, s), b1(planes * plane, s);
-    VXQ_CUDA(cudaMemsetAsync(b0.get(), 0, planes * plane * 2, s));
-    VXQ_CUDA(cudaMemsetAsync(b1.get(), 0, planes * plane * 2, s));
+    DevBuf<uint8_t> b0(nb_planes * plane * esz, s), b1(nb_planes * plane * esz, s);
+    VXQ_CUDA(cudaMemsetAsync(b0.get(), 0, nb_planes * plane * esz, s));
+    VXQ_CUDA(cudaMemsetAsync(b1.get(), 0, nb_planes * plane * esz, s));
+    const float qscale = exact ? std::ldexp(1.0f, S) : 0.f;
     k_init_sbm_rm<<<nblk(((2 * n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, amp,
-                                                            q.get(), pm.get(), b0.get(), planes);
+                                                            q.get(), pm.get(), b0.get(), planes,
+                                                            qscale);
     VXQ_CHECK_LAUNCH();
-    // f16x2 on tcgen05 CTA pairs (M = 256, bn <= 256, each CTA stages its 128 K rows and
-    // bn/2 replicas of both planes): half the replica blocks -> half the K re-reads per step
-    bool pair = planes == 2 && ceil_div(n, DBM) >= 2;
-    if (const char* e = getenv("VXQ_DENSE_2CTA")) pair = pair && atoi(e) == 1;
+    // CTA pairs (M = 256; each CTA stages its 128 K rows and bn/2 replicas of every plane):
+    // half the replica blocks -> half the K re-reads per step
+    bool pair = (planes == 2 || exact) && ceil_div(n, DBM) >= 2;
+    if (const char* e = getenv("VXQ_DENSE_2CTA")) pair = pair && (atoi(e) == 1 || exact);
     if (general) {
         VXQ_REQUIRE(ceil_div(n, DBM) >= 2, "general dense path needs n > 128");
         pair = true;
     }
     int bn;
     if (pair) {
-        const int64_t blocks = ceil_div(R, (int64_t)256);
-        bn = (int)std::min<int64_t>(256, ceil_div(ceil_div(R, blocks), 16) * 16);
+        const int64_t bmax = exact ? KindTraits<Kind::kI8x3>::kBnMax : 256;
+        const int64_t blocks = ceil_div(R, bmax);
+        bn = (int)std::min<int64_t>(bmax, ceil_div(ceil_div(R, blocks), 16) * 16);
     } else {
         bn = planes == 3 ? choose_bn(n, R, 3, KindTraits<Kind::kBf16x3>::kBnMax)
                          : choose_bn(n, R, 2, KindTraits<Kind::kF16x2>::kBnMax);
     }
     const int bbox = pair ? bn / 2 : bn;
-    const CUtensorMapDataType bt =
-        planes == 3 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    CUtensorMap tmB0 = make_map(b0.get(), bt, 2, ld, R, planes, DROW / 2, bbox, planes);
-    CUtensorMap tmB1 = make_map(b1.get(), bt, 2, ld, R, planes, DROW / 2, bbox, planes);
+    CUtensorMap tmB0, tmB1;
+    if (exact) {
+        tmB0 = make_map(b0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 3, DROW, bbox, 3);
+        tmB1 = make_map(b1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 3, DROW, bbox, 3);
+    } else {
+        const CUtensorMapDataType bt =
+            planes == 3 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+        tmB0 = make_map(b0.get(), bt, 2, ld, R, planes, DROW / 2, bbox, planes);
+        tmB1 = make_map(b1.get(), bt, 2, ld, R, planes, DROW / 2, bbox, planes);
+    }
     std::vector<float> s32(T);
     for (int64_t t = 0; t < T; ++t) s32[t] = (float)a_sched[t];
     DevBuf<float> sc(std::max<int64_t>(T, 1), s);
@@ -1757,7 +1872,9 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     a.n = (int)n;
     a.R = (int)R;
     a.ld = (int)ld;
-    a.kblocks = (int)(ld / (DROW / 2));
+    a.kblocks = (int)(ld / (exact ? DROW : DROW / 2));
+    a.qscale = qscale;
+    a.qscale_inv = exact ? std::ldexp(1.0f, -S) : 0.f;
     a.m_tiles = (int)ceil_div(n, DBM);
     a.n_tiles = (int)ceil_div(R, bn);
     a.bn = bn;
@@ -1780,8 +1897,8 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
-    *loop_ms = run_loop(a, general ? d->tmJ : (planes == 3 ? d->tmA16 : d->tmA16h), tmB0, tmB1,
-                        planes, 1, s, pair, nullptr, nullptr, false, false, general);
+    *loop_ms = run_loop(a, general ? d->tmJ : (exact ? d->tmAi8 : (planes == 3 ? d->tmA16 : d->tmA16h)),
+                        tmB0, tmB1, planes, 1, s, pair, nullptr, nullptr, false, false, general);
     *launches += 2;
     if (q2 && !general) energy_pass(d, q.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(q.get(), n, R, ld, R_pad, V, q_il);

@@ -1088,6 +1088,7 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         if (trk.best) sb_final = trk.best_sb.get();
     }
     out->path_used = (dense || dense_gen) ? VXQ_PATH_DENSE : path;
+    out->dense_kind = (dense || dense_gen) ? dense_last_kind() : VXQ_DENSE_KIND_NONE;
     // q2 (coupling energy counts of the final spins) only describes sb_final without tracking
     finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s,
                       dense && !want_best ? q2.get() : nullptr);
@@ -1152,7 +1153,10 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
         *q_final = qs[T_ & 1];
         if (out) out->loop_ms = tm.ms();
     }
-    if (out) out->path_used = path;
+    if (out) {
+        out->path_used = path;
+        out->dense_kind = VXQ_DENSE_KIND_NONE;
+    }
 }
 
 template <typename T>
@@ -1204,6 +1208,7 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
                            &launches);
         }
         out->path_used = VXQ_PATH_DENSE;
+        out->dense_kind = dense_last_kind();
         finish_outputs<T>(p, L, sb.get(), q.get(), pm.get(), opts, out, s,
                           p->uniform_magnitude ? qq.get() : nullptr);
         out->launches = launches + 4;

@@ -300,6 +300,15 @@ __device__ __forceinline__ void mma2_f8f6f4(uint32_t d_tmem, uint64_t adesc, uin
         "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// CTA-pair kind::i8 (S8 x S8 -> S32, exact integer accumulation), M = 256
+__device__ __forceinline__ void mma2_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 // arrive (when the pair's prior MMAs complete) on `bar` in every CTA of `mask`
 __device__ __forceinline__ void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
     asm volatile(

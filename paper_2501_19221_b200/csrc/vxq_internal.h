@@ -215,6 +215,8 @@ void session_set_own_stream(Session* S, bool own);
 bool dense_eligible(const Problem* p, int64_t R);
 bool dense_general_eligible(const Problem* p, int64_t R);
 bool dense_sbm_fp16_ok(double q_cap, double amp);  // |q| stays in the fp16 q-plane range
+int sbm_fixed_point_shift(double q_cap, double amp);  // exact SBM path: 2^S scaling of q
+int dense_last_kind();  // VXQ_DENSE_KIND_* of the calling thread's last dense loop
 void dense_pa_general_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                            const std::vector<double>& sched, float eta, float alpha,
                            uint64_t seed, int64_t rbegin, float* x_il, float* m_il, uint32_t* sb,

@@ -57,6 +57,61 @@ def drive(session, bufs, T: int, gather) -> None:
         gather(bufs[(t + 1) & 1])
 
 
+def chunked_row_split(n: int, world: int, chunks: int):
+    """Row ownership for the pipelined exchange: the rows are cut into `chunks` x `world`
+    equal blocks of Bc rows, chunk c being the contiguous global range
+    [c*world*Bc, (c+1)*world*Bc) and rank g owning its g-th block.  Chunk c of the exchange
+    buffer is then exactly the [world][Bc] layout an in-place all-gather fills, so each
+    chunk can be exchanged on its own.  Returns (spans[g][c] = (row_begin, row_end), Bc);
+    rows_alloc = chunks * world * Bc (trailing padding rows are never read)."""
+    C, W = int(chunks), int(world)
+    Bc = -(-int(n) // (C * W))
+    spans = [[(min(n, (c * W + g) * Bc), min(n, (c * W + g + 1) * Bc)) for c in range(C)]
+             for g in range(W)]
+    return spans, Bc
+
+
+def drive_chunked(sessions, bufs, T: int, gather_async, chunk_bytes: int) -> None:
+    """Pipelined row-partitioned loop: per step, chunk c's rows are stepped and
+    their exchange is started asynchronously (NCCL runs it on its own stream) while chunk
+    c+1 steps, so all but the last chunk's all-gather overlap the step kernels.  Step t+1
+    of every chunk waits for all of state t+1 (the steps read every row).
+
+    sessions[c]: this rank's session over its rows of chunk c (all share `bufs`);
+    gather_async(view) -> handle with .wait() (in-place all-gather of one chunk's
+    [world][Bc] block); chunk_bytes = world * Bc * row_bytes."""
+    C = len(sessions)
+
+    def view(k, c):
+        return bufs[k][c * chunk_bytes:(c + 1) * chunk_bytes]
+
+    pend = [gather_async(view(0, c)) for c in range(C)]
+    for t in range(T):
+        for h in pend:  # state t complete on every row
+            h.wait()
+        pend = []
+        for c in range(C):
+            sessions[c].step(t)
+            pend.append(gather_async(view((t + 1) & 1, c)))
+    for h in pend:
+        h.wait()
+
+
+def gather_chunk_async(view, rank: int, world: int, group=None):
+    """In-place all-gather of one chunk (uint8 tensor of world * piece bytes), async."""
+    import torch.distributed as dist
+
+    class _Done:
+        def wait(self):
+            return None
+
+    if world == 1:
+        return _Done()
+    piece = view.numel() // world
+    return dist.all_gather_into_tensor(view, view[rank * piece:(rank + 1) * piece],
+                                       group=group, async_op=True)
+
+
 class GpuSession:
     """One rank's vxq_session (GPU kernels over rows [row_begin, row_end))."""
 
@@ -209,12 +264,15 @@ class PeerExchange:
 
 
 def solve_rowpart(solver: str, model, params, group=None, precision: str = "fp32",
-                  timing: dict | None = None, exchange: str = "nccl") -> SampleSet:
+                  timing: dict | None = None, exchange: str = "nccl",
+                  chunks: int = 1) -> SampleSet:
     """Row-partitioned PA/SBM over the ranks of `group` (one GPU per rank).
 
-    exchange="nccl": in-place all-gather after every step; "p2p": the fused peer-memory
-    exchange (PeerExchange).  Every rank returns the same best-first SampleSet.  With a
-    single rank this is the ordinary sparse path (bit-identical)."""
+    exchange="nccl": in-place all-gather after every step -- with chunks > 1 pipelined
+    (chunked_row_split / drive_chunked: chunk c's all-gather overlaps chunk c+1's step);
+    "p2p": the fused peer-memory exchange (PeerExchange).  Every rank returns the same
+    best-first SampleSet.  With a single rank this is the ordinary sparse path
+    (bit-identical)."""
     import torch
     import torch.distributed as dist
 
@@ -234,11 +292,36 @@ def solve_rowpart(solver: str, model, params, group=None, precision: str = "fp32
     if exchange == "p2p":
         px = PeerExchange(rows_alloc * rb, world, rank, dev, group)
         bufs = px.bufs()
-    else:
+    elif chunks <= 1:
         bufs = [torch.zeros(rows_alloc * rb, dtype=torch.uint8, device=f"cuda:{dev}")
                 for _ in range(2)]
     stream = torch.cuda.current_stream()
     t0 = time.perf_counter()
+    if exchange == "nccl" and chunks > 1:
+        cspans, Bc = chunked_row_split(n, world, chunks)
+        rows_alloc = chunks * world * Bc
+        bufs = [torch.zeros(rows_alloc * rb, dtype=torch.uint8, device=f"cuda:{dev}")
+                for _ in range(2)]
+        sessions = [GpuSession(model, solver, params, b, e, rows_alloc, bufs, precision, dev,
+                               stream.cuda_stream) for b, e in cspans[rank]]
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        drive_chunked(sessions, bufs, int(params.steps),
+                      lambda v: gather_chunk_async(v, rank, world, group), world * Bc * rb)
+        ev1.record(stream)
+        st, en, order, info = sessions[0].finish()
+        for s_ in sessions:
+            s_.close()
+        if timing is not None:
+            torch.cuda.synchronize()
+            timing["loop_ms"] = ev0.elapsed_time(ev1)
+            timing["exchange_bytes_per_step"] = rows_alloc * rb
+        samples = [Sample(st[r].copy(), float(en[r]), int(r)) for r in order]
+        return SampleSet(samples=samples, replica_count=int(params.replicas), seed=params.seed,
+                         wall_time=time.perf_counter() - t0,
+                         info={**info, "world": world, "rank": rank, "rows": cspans[rank],
+                               "path": "rowpart", "exchange": f"nccl-pipelined x{chunks}"})
     sess = GpuSession(model, solver, params, spans[rank][0], spans[rank][1], rows_alloc, bufs,
                       precision, dev, stream.cuda_stream)
     ev0 = torch.cuda.Event(enable_timing=True)

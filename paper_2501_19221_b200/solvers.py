@@ -225,7 +225,8 @@ def run_pa(model, params, *, precision="fp32", path="auto", device=0, replica_be
                                         ctypes.byref(out)))
     info = {"lambda0": out.lambda0_used, "loop_ms": out.loop_ms, "launches": out.launches,
             "path": _lib.PATH_NAMES.get(out.path_used, "?"), "precision": precision,
-            "energy_trace": tr, "track_best": track_best}
+            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind), "energy_trace": tr,
+            "track_best": track_best}
     return RunResult(st, en, order, x, m, info)
 
 
@@ -243,7 +244,8 @@ def run_sbm(model, params, *, precision="fp32", path="auto", device=0, replica_b
                                          ctypes.byref(out)))
     info = {"c0": out.c0_used, "loop_ms": out.loop_ms, "launches": out.launches,
             "path": _lib.PATH_NAMES.get(out.path_used, "?"), "precision": precision,
-            "energy_trace": tr, "track_best": track_best}
+            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind), "energy_trace": tr,
+            "track_best": track_best}
     return RunResult(st, en, order, x, m, info)
 
 
@@ -307,7 +309,8 @@ def run_device(kind: str, model, params, states_ptr: int, energies_ptr: int, *,
         _lib.check(L.vxq_sbm_solve(dp.handle, ctypes.byref(c), ctypes.byref(opts),
                                    ctypes.byref(out)))
     return {"lambda0": out.lambda0_used, "c0": out.c0_used, "loop_ms": out.loop_ms,
-            "launches": out.launches, "path": _lib.PATH_NAMES.get(out.path_used, "?")}
+            "launches": out.launches, "path": _lib.PATH_NAMES.get(out.path_used, "?"),
+            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind)}
 
 
 def sampleset_from(res: RunResult, R: int, seed, wall_time: float, replica_begin: int = 0):

@@ -169,3 +169,50 @@ def test_row_partitioned_exchange_equals_single_process():
     want = O.sign_pm(X)
     for rank in range(world):
         assert np.array_equal(np.array(out[rank], dtype=np.int8), want)
+
+
+def _rowpart_chunked_worker(rank, world, port, chunks, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_19221_b200.rowpart import (chunked_row_split, drive_chunked,
+                                               gather_chunk_async)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = _model()
+        R, T = 40, 25
+        spans, Bc = chunked_row_split(m.n, world, chunks)
+        W = (R + 31) // 32
+        row_bytes = 4 * W
+        rows_alloc = chunks * world * Bc
+        bufs = [torch.zeros(rows_alloc * row_bytes, dtype=torch.uint8) for _ in range(2)]
+        sessions = [_OracleRowSession(m, R, T, 3, b, e, bufs) for b, e in spans[rank]]
+        drive_chunked(sessions, bufs, T, lambda v: gather_chunk_async(v, rank, world),
+                      world * Bc * row_bytes)
+        out[rank] = sessions[0]._spins(T)[:, : m.n].astype(np.int8).tolist()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("chunks", [2, 3])
+def test_row_partitioned_pipelined_exchange_equals_single_process(chunks):
+    """Pipelined exchange (chunk c's async all-gather overlaps chunk c+1's step): the rows
+    are owned chunk-interleaved across the ranks; the result equals the 1-process loop."""
+    from paper_2501_19221_b200.rowpart import chunked_row_split
+    spans, Bc = chunked_row_split(24, 2, chunks)
+    owned = sorted(r for g in range(2) for b, e in spans[g] for r in range(b, e))
+    assert owned == list(range(24))  # every row owned exactly once
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_rowpart_chunked_worker, args=(world, _free_port(), chunks, out),
+                       nprocs=world, join=True, start_method="spawn")
+    m = _model()
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    X = O.pa_init(3, 40, m.n)
+    X, _ = O.pa_run(ip, ix, dv, m.h, O.pa_schedule(O.resolve_lambda0(m), 25), 0.05, 0.9, X,
+                    np.zeros_like(X))
+    want = O.sign_pm(X)
+    for rank in range(world):
+        assert np.array_equal(np.array(out[rank], dtype=np.int8), want)
