@@ -51,6 +51,9 @@ constexpr int RING_BYTES = 224 * 1024;  // operand stages + x/m staging slots
 constexpr int XM_SLOT_BYTES = 2 * 16 * DBM * 4;  // x and m of 16 replicas x 128 rows (fp32)
 constexpr int DSMEM = RING_BYTES + 1024 + 512;
 constexpr int QN = 8;  // tile-ticket ring depth (dynamic tile queue, see k_dense_run)
+#ifndef VXQ_I8_STAGES
+#define VXQ_I8_STAGES 6  // operand ring depth of the exact SBM kernel (31 KB stages)
+#endif
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
 enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3, kJQ16 = 4, kI8x3 = 5 };
@@ -540,11 +543,17 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     constexpr uint32_t ACC_COLS = MX ? kAccMx : 256;
     constexpr int NCTA = PAIR ? 2 : CL;
     // pair: each CTA stages its 128 A rows and <= 128 B rows per plane
+    // kI8x3: each CTA stages <= kBnMax/2 = 40 replicas per digit plane, so a stage packs
+    // into 31 KB and the ring holds VXQ_I8_STAGES of them (no x/m slots: SBM)
+    constexpr int SBYTES_I8 = ((A_BYTES + 3 * (KindTraits<Kind::kI8x3>::kBnMax / 2) * DROW +
+                                1023) / 1024) * 1024;
     constexpr int STAGES =
-        PAIR ? ((TR::kPlanes == 1 && TR::kAPlanes == 1) ? VXQ_PAIR_STAGES
-                                                        : (TR::kPlanes * TR::kAPlanes > 2 ? 3 : 4))
-             : TR::kStages;
-    constexpr int SBYTES = PAIR ? A_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
+        KD == Kind::kI8x3 ? VXQ_I8_STAGES
+        : PAIR ? ((TR::kPlanes == 1 && TR::kAPlanes == 1) ? VXQ_PAIR_STAGES
+                                                          : (TR::kPlanes * TR::kAPlanes > 2 ? 3 : 4))
+               : TR::kStages;
+    constexpr int SBYTES = KD == Kind::kI8x3 ? SBYTES_I8
+                           : PAIR ? A_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
     static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
     static_assert((KD != Kind::kFp8 && KD != Kind::kJ16x2) || XMS >= 2, "x/m staging slots");
@@ -1844,7 +1853,9 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     }
     int bn;
     if (pair) {
-        const int64_t bmax = exact ? KindTraits<Kind::kI8x3>::kBnMax : 256;
+        int64_t bmax = exact ? KindTraits<Kind::kI8x3>::kBnMax : 256;
+        if (const char* e = getenv("VXQ_DENSE_BN"))  // A/B: cap the replica tile width
+            if (exact) bmax = std::max<int64_t>(16, std::min<int64_t>(bmax, atoi(e) / 16 * 16));
         const int64_t blocks = ceil_div(R, bmax);
         bn = (int)std::min<int64_t>(bmax, ceil_div(ceil_div(R, blocks), 16) * 16);
     } else {
