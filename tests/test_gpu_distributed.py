@@ -166,3 +166,80 @@ def test_fused_exchange_rejects_foreign_own_buffers():
             sess.handle, 2, 0, 1, arr(bufs[2].data_ptr(), bufs[0].data_ptr()),
             arr(bufs[1].data_ptr(), bufs[1].data_ptr()), arr(fl.data_ptr(), fl.data_ptr())))
     sess.close()
+
+
+@pytest.mark.parametrize("solver", ["pa", "sbm"])
+def test_chunked_row_sessions_match_sparse_path(solver):
+    """Pipelined exchange ownership (chunk-interleaved rows, rowpart.chunked_row_split) for
+    2 "ranks" x 3 chunks sharing one exchange buffer == the 1-GPU sparse path; and
+    solve_rowpart(chunks=4) at world 1 through the public API."""
+    import torch
+
+    from paper_2501_19221_b200.rowpart import (GpuSession, chunked_row_split,
+                                               exchange_row_bytes, solve_rowpart)
+    m = maxcut_model(3000, 3, 13)
+    if solver == "pa":
+        params = vxq.PaParams(steps=30, replicas=64, seed=2)
+        ref = vxq.run_pa(m, params, path="sparse")
+    else:
+        params = vxq.SbmParams(steps=30, dt=0.05, replicas=64, seed=2, c0=0.3)
+        ref = vxq.run_sbm(m, params, path="sparse")
+    spans, Bc = chunked_row_split(m.n, 2, 3)
+    rows_alloc = 3 * 2 * Bc
+    rb = exchange_row_bytes(solver, params.replicas)
+    bufs = [torch.zeros(rows_alloc * rb, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    stream = torch.cuda.current_stream().cuda_stream
+    sess = [GpuSession(m, solver, params, b, e, rows_alloc, bufs, stream=stream)
+            for g in range(2) for b, e in spans[g]]
+    for t in range(params.steps):
+        for s in sess:
+            s.step(t)
+    st, en, order, _ = sess[0].finish()
+    assert np.array_equal(st, ref.states) and np.array_equal(en, ref.energies)
+    ss = solve_rowpart(solver, m, params, chunks=4)
+    assert [s.replica for s in ss.samples] == list(ref.order)
+
+
+def test_session_snapshot_state_sbm():
+    """A one-rank session over all rows, stopped after k < T steps of the T-step schedule,
+    returns Q/P equal to the oracle's fp32 loop over the first k schedule entries."""
+    import torch
+
+    from paper_2501_19221_b200.rowpart import GpuSession, exchange_row_bytes
+    m = gen_complete(8, 300, "gaussian")
+    params = vxq.SbmParams(steps=100, dt=0.05, replicas=40, seed=3, c0=0.1)
+    rb = exchange_row_bytes("sbm", params.replicas)
+    bufs = [torch.zeros(m.n * rb, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    sess = GpuSession(m, "sbm", params, 0, m.n, m.n, bufs)
+    for t in range(17):
+        sess.step(t)
+    st, en, order, info = sess.finish(want_state=True)
+    sess.close()
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    Q, P = O.sbm_init(3, 40, m.n, 1.0)
+    Q, P = O.sbm_run(ip, ix, -dv, -m.h, O.sbm_schedule(1.0, 100)[:17], 0.05, 1.0, 0.1, 1.0, Q,
+                     P, np.float32)
+    assert np.array_equal(info["x"], Q.astype(np.float64))
+    assert np.array_equal(info["m"], P.astype(np.float64))
+    assert np.array_equal(en, O.energies_exact(m, st))
+
+
+def test_shard_path_pins_dense_for_small_shards():
+    """A replica shard smaller than the dense threshold (R >= 128) runs the global solve's
+    tensor-core path (distributed.shard_path), so its rows equal the 1-GPU solve's."""
+    from helpers import sk_model
+    from paper_2501_19221_b200.distributed import shard_path
+    m = sk_model(700, 4)
+    full = vxq.PaParams(steps=20, replicas=256, seed=3)
+    g = vxq.run_pa(m, full, want_state=True)
+    assert g.info["path"] == "dense"
+    path = shard_path(m, "pa", full, "fp32", "auto", 0)
+    assert path == "dense"
+    shard = vxq.run_pa(m, vxq.PaParams(steps=20, replicas=64, seed=3), path=path,
+                       replica_begin=192, want_state=True)
+    assert shard.info["path"] == "dense"
+    assert np.array_equal(shard.x, g.x[192:256])
+    assert np.array_equal(shard.energies, g.energies[192:256])
+    # below the threshold globally: auto stays auto (the CSR paths are the same arithmetic)
+    assert shard_path(m, "pa", vxq.PaParams(steps=20, replicas=64, seed=3), "fp32", "auto",
+                      0) == "auto"
