@@ -248,7 +248,7 @@ def cpu_baseline(model, solver, R, T):
 # ----------------------------------------------------------------------------- time to target
 TTT_SWEEPS = {  # annealing schedules tried besides the timed one (reference defaults otherwise)
     "cfg2": (500, 600, 700, 850, 2000, 5000, 10000, 20000),
-    "cfg1": (100, 200, 500), "cfg3": (100, 200, 500), "cfg4": (100, 200, 500),
+    "cfg1": (100, 200, 500, 2000), "cfg3": (200, 500, 2000, 5000), "cfg4": (200, 500, 2000, 5000),
 }
 
 
