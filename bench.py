@@ -634,7 +634,9 @@ def run_ours(args):
         B = bytes_per_update(args.solver, dbar, R)
         achieved = B * R * n / (mean_step_kernel_ms / 1e3) / 1e9
         kname = f"k_{args.solver}_step"
-        if args.solver == "pa" and R <= 32 and info.get("path") in ("sparse", "rowpart"):
+        if info.get("path") == "resident":
+            kname = f"k_{args.solver}_resident"
+        elif args.solver == "pa" and R <= 32 and info.get("path") in ("sparse", "rowpart"):
             kname = "k_pa_step_coop"  # one sign word per row: cooperative warp-CSR variant
         tr, tsrc = measured_traffic(kname, args.config)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
