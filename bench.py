@@ -647,6 +647,10 @@ def run_ours(args):
                 "mean_launch_ms": mean_step_kernel_ms,
                 "frac_of_8TBs_nominal": achieved / 8000.0, "peak_source": src}
 
+    if roof.get("traffic"):  # measured DRAM bytes per step (ncu) / this run's step time
+        roof["dram_gbs"] = roof["traffic"] / (mean_step_kernel_ms / 1e3) / 1e9
+        roof["dram_frac"] = roof["dram_gbs"] / hbm
+
     # e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e and not hasattr(model, "rows"):

@@ -1903,7 +1903,11 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     a.b_buf[0] = reinterpret_cast<uint8_t*>(b0.get());
     a.b_buf[1] = reinterpret_cast<uint8_t*>(b1.get());
     a.plane_elems = plane;
-    a.group = pick_group(a.n_tiles);
+    // exact path: all replica blocks of a row panel back to back (the int8 K panel is
+    // re-used from L2 instead of re-read from DRAM per replica block: 1.48 GB -> less
+    // DRAM per step, more of the 1 kW budget for the SMs; cfg2 SBM 324 -> 280 ms per solve,
+    // profiles/r02/ab_sbm_group/); VXQ_DENSE_GROUP overrides
+    a.group = (exact && !getenv("VXQ_DENSE_GROUP")) ? a.n_tiles : pick_group(a.n_tiles);
     a.mode = 0;
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
