@@ -510,6 +510,13 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // loads its A rows and HALF of B into its own smem (32 KB stages, 6 deep), only the leader
 // (rank 0) issues the M = 256 MMAs and its commits arrive in both CTAs.
 //
+// PAIR && CL == 2 ("super-pair", PA mxf4 only): a 4-CTA cluster of two tcgen05 pairs that
+// work on the SAME row block and two replica blocks (nb = 2 nbp + pair): pair 0's CTAs load
+// the K panel once and TMA-multicast each 128-row half into the matching CTA of both pairs,
+// so K crosses L2->SM once per two tiles.  Each pair keeps its own TMEM, MMAs and epilogue;
+// a stage is refilled only after both pairs' MMAs released it (commits multicast to all 4
+// CTAs, empty count 2).  Needs an even number of replica blocks.
+//
 // a.xm (PA steps): a loader warp TMA-loads each tile's x/m in 16-replica chunks into XMS
 // shared-memory slots ahead of the epilogue (after acquiring the step-(t-1) counter), so the
 // epilogue's inputs are in flight without occupying registers.
@@ -534,14 +541,18 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ CUtensorMap tmM, DenseRunArgs a) {
     using TR = KindTraits<KD>;
-    static_assert(!PAIR || (KD != Kind::kBf16x3 && CL == 1), "pair MMA: f8f6f4 / f16x2, no B multicast");
+    static_assert(!PAIR || (KD != Kind::kBf16x3 && (CL == 1 || (CL == 2 && MX))),
+                  "pair MMA: f8f6f4 / f16x2, no B multicast; super-pairs: mxf4 only");
+    constexpr bool SP = PAIR && CL == 2;  // two pairs sharing the K panel
     static_assert(KD != Kind::kI8x3 || PAIR, "int8 digit planes: CTA pairs only");
     static_assert((KD != Kind::kJ16x2 && KD != Kind::kJQ16) || PAIR,
                   "general-J planes: CTA pairs only");
     constexpr int A_BYTES = DA_BYTES * TR::kAPlanes;  // A planes of one stage, back to back
-    static_assert(!MX || (KD == Kind::kFp8 && CL == 1), "mxf4: fp8-kind layout, no multicast");
+    static_assert(!MX || (KD == Kind::kFp8 && (CL == 1 || PAIR)),
+                  "mxf4: fp8-kind layout, no B multicast");
     constexpr uint32_t ACC_COLS = MX ? kAccMx : 256;
-    constexpr int NCTA = PAIR ? 2 : CL;
+    constexpr int NCTA = PAIR ? 2 * CL : CL;
+    constexpr int RPC = PAIR ? 2 : CL;  // CTAs splitting a tile's rows
     // pair: each CTA stages its 128 A rows and <= 128 B rows per plane
     // kI8x3: each CTA stages <= kBnMax/2 = 40 replicas per digit plane, so a stage packs
     // into 31 KB and the ring holds VXQ_I8_STAGES of them (no x/m slots: SBM)
@@ -580,7 +591,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(full + s, 1);
             // released by the MMA of every CTA in the cluster (pair: the leader's only)
-            ptx::mbar_init(empty + s, PAIR ? 1 : CL);
+            ptx::mbar_init(empty + s, SP ? 2 : (PAIR ? 1 : CL));
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(tfull + s, 1);
@@ -594,7 +605,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         // and the x/m loader (PA with staging), the MMA issuer(s) (pair: the leader's
         // only), and every non-leader producer
         const uint32_t xmc = (a.xm && a.mode == 0) ? 1u : 0u;
-        const uint32_t qcons = NCTA * (8u + xmc) + (PAIR ? 1u : (uint32_t)NCTA) + (NCTA - 1u);
+        const uint32_t qcons =
+            NCTA * (8u + xmc) + (PAIR ? (uint32_t)CL : (uint32_t)NCTA) + (NCTA - 1u);
         for (int s = 0; s < QN; ++s) {
             ptx::mbar_init(qfull + s, 1);
             ptx::mbar_init(qempty + s, qcons);
@@ -627,6 +639,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         ptx::tc_fence_after();
     }
     const int crank = NCTA > 1 ? (int)ptx::cluster_ctarank() : 0;
+    const int lr = PAIR ? (crank & 1) : crank;  // rank within the tile's row-splitting CTAs
+    const int pr = SP ? (crank >> 1) : 0;       // super-pair: which pair (replica block)
     // Dynamic tile queue: the leader CTA's TMA thread takes tile tickets in increasing
     // order (atomicAdd on a.ticket) and hands each to every role of every CTA of its
     // cluster through a QN-deep smem ring.  A tile only ever waits on tiles of the previous
@@ -641,8 +655,14 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         if constexpr (NCTA > 1) ptx::mbar_arrive_cluster(ptx::cluster_addr(qempty + (k % QN), 0));
         else ptx::mbar_arrive(qempty + (k % QN));
     };
-    const int mrows = (a.m_tiles + NCTA - 1) / NCTA;                 // row-block groups per step
-    const int tps = mrows * a.n_tiles;                               // work items per step
+    const int mrows = (a.m_tiles + RPC - 1) / RPC;                   // row-block groups per step
+    const int tps = mrows * (SP ? a.n_tiles / 2 : a.n_tiles);        // work items per step
+    // ticket -> (step, this pair's replica block, this CTA's row block)
+    auto tile_of = [&](int g, int& t, int& nb, int& mb) {
+        decode_tile(a, g, tps, mrows, t, nb, mb);
+        mb = mb * RPC + lr;
+        if constexpr (SP) nb = 2 * nb + pr;
+    };
     const int num_tiles = tps * a.T;
     // B bytes per stage in this CTA's smem (pair: half of the bn replicas)
     const uint32_t b_plane_bytes = (uint32_t)(PAIR ? a.bn / 2 : a.bn) * DROW;
@@ -677,8 +697,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 }
                 if (g < 0) break;
                 int t, nb, mb;
-                decode_tile(a, g, tps, mrows, t, nb, mb);
-                mb = mb * NCTA + crank;
+                tile_of(g, t, nb, mb);
                 const CUtensorMap* tmB = (t & 1) ? &tmB1 : &tmB0;
                 // A (the coupling panel) never depends on the dynamics: keep kPrefetch
                 // k-blocks of it on their way into L2 ahead of the smem loads
@@ -704,7 +723,15 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     uint8_t* sa = smem + stage * SBYTES;
                     const uint32_t tx = a.a_tx_bytes + TR::kPlanes * a.b_tx_bytes;
                     const int kcol = kb * (DROW / TR::kElemBytes);
-                    if constexpr (PAIR) {
+                    if constexpr (SP) {
+                        // pair 0 loads the K half of this CTA's rows once, multicast into
+                        // the same CTA of both pairs (each pair leader's barrier counts its
+                        // two CTAs' bytes, as for a single pair)
+                        if (lr == 0) ptx::mbar_arrive_expect_tx(full + stage, 2 * tx);
+                        if (pr == 0)
+                            ptx::tma_load_2d_2sm_mc(sa, &tmA, full + stage, kcol, mb * DBM,
+                                                    (uint16_t)((1u << lr) | (4u << lr)), keep);
+                    } else if constexpr (PAIR) {
                         // the leader's barrier counts both CTAs' bytes; each CTA's loads land
                         // in its own smem and complete on the leader's barrier
                         if (crank == 0) ptx::mbar_arrive_expect_tx(full + stage, 2 * tx);
@@ -735,10 +762,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     }
                     if constexpr (PAIR && TR::kPlanes > 1) {
                         ptx::tma_load_3d_2sm(sa + A_BYTES, tmB, full + stage, kcol,
-                                             nb * a.bn + crank * (a.bn / 2), 0, keep);
+                                             nb * a.bn + lr * (a.bn / 2), 0, keep);
                     } else if constexpr (PAIR) {
                         ptx::tma_load_2d_2sm(sa + A_BYTES, tmB, full + stage, kcol,
-                                             nb * a.bn + crank * (a.bn / 2), keep);
+                                             nb * a.bn + lr * (a.bn / 2), keep);
                     } else if constexpr (CL > 1) {
                         static_assert(TR::kPlanes == 1, "B multicast: single-plane B only");
                         const int hrows = a.bn / CL;
@@ -765,7 +792,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (single thread issues for the CTA / the pair's leader)
-        if (PAIR && crank != 0) goto mma_done;
+        if (PAIR && lr != 0) goto mma_done;
         {
         // mxf4 (block-scaled descriptor): E2M1 = 1 for A and B, UE8M0 scales (bit 23),
         // K = 64 per MMA, scale-factor ids 0; no accumulator-format field
@@ -832,7 +859,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                                 ptx::mma_f16(d, da + 2 * k, db + 2 * k, idesc, accum);
                         }
                     }
-                    if constexpr (PAIR) ptx::mma2_commit_mc(empty + stage, 0x3);
+                    if constexpr (SP) ptx::mma2_commit_mc(empty + stage, 0xF);  // both pairs
+                    else if constexpr (PAIR) ptx::mma2_commit_mc(empty + stage, 0x3);
                     else if constexpr (CL > 1) ptx::mma_commit_mc(empty + stage, kMask);
                     else ptx::mma_commit(empty + stage);
                 }
@@ -843,7 +871,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 }
             }
             if (ptx::elect_one()) {
-                if constexpr (PAIR) ptx::mma2_commit_mc(tfull + acc, 0x3);
+                if constexpr (PAIR) ptx::mma2_commit_mc(tfull + acc, (uint16_t)(0x3u << (2 * pr)));
                 else ptx::mma_commit(tfull + acc);
             }
             __syncwarp();
@@ -867,8 +895,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 release_ticket(k);
                 if (g < 0) break;
                 int t, nb, mb;
-                decode_tile(a, g, tps, mrows, t, nb, mb);
-                mb = mb * NCTA + crank;
+                tile_of(g, t, nb, mb);
                 if (mb >= a.m_tiles) continue;  // no rows: the epilogue skips it too
                 if (t > 0) {
                     // x/m of step t were written by the step-(t-1) tiles of this replica
@@ -921,8 +948,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
             if (lane == 0) release_ticket(k);
             if (g < 0) break;
             int t, nb, mb;
-            decode_tile(a, g, tps, mrows, t, nb, mb);
-            mb = mb * NCTA + crank;
+            tile_of(g, t, nb, mb);
             const bool tile_ok = mb < a.m_tiles;  // last cluster row group may be partial
             const int acc = lt & 1;
             const uint32_t acc_ph = (lt >> 1) & 1;
@@ -1289,12 +1315,16 @@ template <Kind KD, int CL, bool PAIR = false, bool MX = false>
 void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorMap& tmB1,
                 DenseRunArgs a, int64_t steps_for_grid, cudaStream_t s, bool cooperative,
                 const CUtensorMap* tmX = nullptr, const CUtensorMap* tmM = nullptr) {
-    constexpr int NCTA = PAIR ? 2 : CL;
+    constexpr int NCTA = PAIR ? 2 * CL : CL;
+    constexpr int RPC = PAIR ? 2 : CL;
     auto kern = k_dense_run<KD, CL, PAIR, MX>;
     VXQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM));
-    const int64_t items = (int64_t)((a.m_tiles + NCTA - 1) / NCTA) * a.n_tiles *
+    if (NCTA > 2)
+        VXQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const int64_t items = (int64_t)((a.m_tiles + RPC - 1) / RPC) *
+                          (PAIR && CL == 2 ? a.n_tiles / 2 : a.n_tiles) *
                           std::max<int64_t>(steps_for_grid, 1);
-    const int64_t clusters = std::min<int64_t>(items, num_sms() / NCTA);
+    int64_t clusters = std::min<int64_t>(items, num_sms() / NCTA);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(clusters * NCTA));
     cfg.blockDim = dim3(DTHREADS);
@@ -1322,6 +1352,14 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
     }
     cfg.attrs = attrs;
     cfg.numAttrs = na;
+    if (NCTA > 2) {  // 4-CTA clusters do not tile all 148 SMs: launch what can be resident
+        int maxc = 0;
+        if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) == cudaSuccess && maxc > 0 &&
+            maxc < clusters) {
+            clusters = maxc;
+            cfg.gridDim = dim3((unsigned)(clusters * NCTA));
+        }
+    }
     VXQ_REQUIRE(!a.xm || (tmX && tmM), "x/m staging needs their tensor maps");
     DevBuf<unsigned> ticket(1, s);
     VXQ_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), s));
@@ -1550,6 +1588,8 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
         else if (planes16 == 2 && pair)
             launch_run<Kind::kF16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 2) launch_run<Kind::kF16x2, 1>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (pair && mx && cl == 2)
+            launch_run<Kind::kFp8, 2, true, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
         else if (pair && mx)
             launch_run<Kind::kFp8, 1, true, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
         else if (mx) launch_run<Kind::kFp8, 1, false, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
@@ -1622,6 +1662,17 @@ void dense_pa_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     if (const char* e = getenv("VXQ_DENSE_2CTA")) pair = atoi(e) == 1;
     if (ceil_div(n, DBM) < 2 || bn % 16 != 0) pair = false;  // each CTA: bn/2 rows of B
     if (pair || mx) cl = 1;
+    // super-pairs (VXQ_DENSE_SP=1): two pairs share each K panel; needs an even number of
+    // replica blocks of <= 240 (an even block count, widths rounded up to 16)
+    bool sp = false;
+    if (const char* e = getenv("VXQ_DENSE_SP")) sp = atoi(e) == 1;
+    if (sp && mx && pair && !getenv("VXQ_DENSE_BN")) {
+        int64_t blocks = ceil_div(R, (int64_t)kAccMx);
+        blocks += blocks & 1;
+        const int b2 = (int)std::min<int64_t>(kAccMx, ceil_div(ceil_div(R, blocks), 16) * 16);
+        if (ceil_div(R, (int64_t)b2) % 2 == 0) bn = b2;
+    }
+    if (sp && mx && pair && ceil_div(R, (int64_t)bn) % 2 == 0) cl = 2;
     const int bbox = pair ? bn / 2 : bn / cl;  // B rows (replicas) per TMA box
     CUtensorMap tmB0, tmB1, tmAmx;
     if (mx) {  // packed bytes as they are in global memory: 128-byte rows = 256 elements

@@ -271,6 +271,18 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
         "l"(policy)
         : "memory");
 }
+// the same, multicast to the CTAs of `mask` (each destination pair's leader barrier)
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* map,
+                                                   uint64_t* bar, int32_t c0, int32_t c1,
+                                                   uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_addr(bar)), "h"(mask), "r"(c0),
+        "r"(c1), "l"(policy)
+        : "memory");
+}
 // 3-D variant ([planes][rows][128 B] boxes), completing on the LEADER's mbarrier
 __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map,
                                                 uint64_t* bar, int32_t c0, int32_t c1,
