@@ -507,7 +507,7 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 //
 // PAIR: the two CTAs of a cluster form a tcgen05 CTA pair (cta_group::2): tile = 256 rows
 // (128 per CTA, each CTA's TMEM holds its rows x all bn replicas) x bn replicas, each CTA
-// loads its A rows and HALF of B into its own smem (32 KB stages, 6 deep), only the leader
+// loads its A rows and HALF of B into its own smem (mxf4: 31 KB stages, 6 deep), only the leader
 // (rank 0) issues the M = 256 MMAs and its commits arrive in both CTAs.
 //
 // PAIR && CL == 2 ("super-pair", PA mxf4 only): a 4-CTA cluster of two tcgen05 pairs that
@@ -530,7 +530,13 @@ constexpr uint32_t kAccMx = 240, kSfCol = 480;
 #define VXQ_PAIR_STAGES 5  // 5 x 32 KB operand stages + 4 x/m slots in 224 KB
 #endif
 #if VXQ_PAIR_STAGES > 5
-#error "VXQ_PAIR_STAGES > 5: the mxf4 pair kernel faulted at 6 stages (not investigated); 5 is the measured best"
+#error "VXQ_PAIR_STAGES > 5: 32 KB stages leave too few x/m slots (mxf4: VXQ_MX_STAGES)"
+#endif
+#ifndef VXQ_MX_TIGHT
+#define VXQ_MX_TIGHT 1  // mxf4 pair stages packed to A + bn_max/2 B rows (31 KB)
+#endif
+#ifndef VXQ_MX_STAGES
+#define VXQ_MX_STAGES 6  // 6 x 31 KB + 2 x/m slots: cfg2 150.1 -> 153.2 Grv/s (profiles/r02/ab_stages)
 #endif
 
 template <Kind KD, int CL, bool PAIR = false, bool MX = false>
@@ -560,10 +566,13 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                                 1023) / 1024) * 1024;
     constexpr int STAGES =
         KD == Kind::kI8x3 ? VXQ_I8_STAGES
+        : (MX && PAIR && VXQ_MX_TIGHT) ? VXQ_MX_STAGES
         : PAIR ? ((TR::kPlanes == 1 && TR::kAPlanes == 1) ? VXQ_PAIR_STAGES
                                                           : (TR::kPlanes * TR::kAPlanes > 2 ? 3 : 4))
                : TR::kStages;
+    constexpr int SBYTES_MX = ((A_BYTES + (kAccMx / 2) * DROW + 1023) / 1024) * 1024;
     constexpr int SBYTES = KD == Kind::kI8x3 ? SBYTES_I8
+                           : (MX && PAIR && VXQ_MX_TIGHT) ? SBYTES_MX
                            : PAIR ? A_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
     static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
