@@ -183,6 +183,78 @@ __global__ void k_scale_into(int64_t n, const double* w, const double* nrm, doub
     if (i < n) v[i] = w[i] / (*nrm);
 }
 
+// fused Lanczos step pieces (fixed grids and reduction orders: deterministic)
+// w = sign * A v (warp per row, grid-stride over rows); part[b] = this block's sum v_i w_i
+constexpr int kSpmvBlocks = 148 * 8;
+__global__ void __launch_bounds__(TB) k_spmv_dot(int64_t n, const int64_t* indptr,
+                                                 const int32_t* indices, const double* data,
+                                                 double sign, const double* v, double* w,
+                                                 double* part) {
+    __shared__ double sh[TB / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double dsum = 0.0;
+    for (int64_t row = (int64_t)blockIdx.x * (TB / 32) + wid; row < n;
+         row += (int64_t)gridDim.x * (TB / 32)) {
+        double acc = 0.0;
+        for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32)
+            acc += data[k] * v[indices[k]];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        acc *= sign;
+        if (lane == 0) {
+            w[row] = acc;
+            dsum += v[row] * acc;
+        }
+    }
+    if (lane == 0) sh[wid] = dsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < TB / 32; ++k) t += sh[k];
+        part[blockIdx.x] = t;
+    }
+}
+
+// w = w - alpha v - beta vprev; part[b] = this block's sum w_i^2
+__global__ void __launch_bounds__(TB) k_axpy2_norm(int64_t n, double* w, const double* v,
+                                                   const double* vp, const double* alpha,
+                                                   const double* beta, double* part) {
+    __shared__ double sh[TB];
+    const double a = *alpha, b = *beta;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)TB + threadIdx.x; i < n; i += (int64_t)TB * gridDim.x) {
+        const double x = w[i] - a * v[i] - b * vp[i];
+        w[i] = x;
+        acc += x * x;
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = TB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// v = w / beta, and (optionally) the same into the stored basis row
+__global__ void k_scale_store(int64_t n, const double* w, const double* nrm, double* v,
+                              double* vstore) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double x = w[i] / (*nrm);
+    v[i] = x;
+    if (vstore) vstore[i] = x;
+}
+
+// y (+)= sum_j u_j V[j] over one chunk of the stored basis (V row-major [k][n])
+__global__ void k_basis_combine(int64_t n, int64_t k, const double* V, const double* u,
+                                double* y, int accumulate) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = accumulate ? y[i] : 0.0;
+    for (int64_t j = 0; j < k; ++j) acc += u[j] * V[j * n + i];
+    y[i] = acc;
+}
+
 __global__ void k_start_vec(int64_t n, double* v) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) v[i] = start_entry(i);
@@ -337,10 +409,24 @@ struct Lanczos {
     double* vp;
     double* v;
     unsigned spmv_blocks;
+    // stored basis V[j] = v_j for j < basis_rows, grown in chunks of kChunk rows while the
+    // total stays within basis_cap rows (memory comes from the retained stream-ordered pool)
+    static constexpr int64_t kChunk = 128;
+    std::vector<DevBuf<double>> chunks;
+    int64_t basis_rows = 0, basis_cap = 0;
+    bool storing = false;
+
+    double* basis_row(int64_t j) {  // row j of the stored basis, allocating its chunk
+        if (!storing || j >= basis_cap) return nullptr;
+        const int64_t c = j / kChunk;
+        if (c >= (int64_t)chunks.size()) chunks.emplace_back((size_t)kChunk * n, s);
+        basis_rows = std::max(basis_rows, j + 1);
+        return chunks[c].get() + (j % kChunk) * n;
+    }
 
     Lanczos(const Problem* p_, double sign_, cudaStream_t s_)
-        : n(p_->n), p(p_), sign(sign_), s(s_), v0(n, s_), v1(n, s_), w(n, s_), part(RB, s_),
-          zero(1, s_) {
+        : n(p_->n), p(p_), sign(sign_), s(s_), v0(n, s_), v1(n, s_), w(n, s_),
+          part(std::max(RB, kSpmvBlocks), s_), zero(1, s_) {
         spmv_blocks = (unsigned)ceil_div(n * 32, TB);
         VXQ_CUDA(cudaMemsetAsync(zero.get(), 0, sizeof(double), s));
     }
@@ -353,26 +439,25 @@ struct Lanczos {
         k_start_vec<<<nblk(n), TB, 0, s>>>(n, w.get());
         k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get(), nullptr);
         k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), nrm, 1);
-        k_scale_into<<<nblk(n), TB, 0, s>>>(n, w.get(), nrm, v);
+        k_scale_store<<<nblk(n), TB, 0, s>>>(n, w.get(), nrm, v, basis_row(0));
         VXQ_CHECK_LAUNCH();
     }
 
-    // step k: w = B v_k - alpha_k v_k - beta_{k-1} v_{k-1}; beta_k = ||w||
+    // step k: w = B v_k - alpha_k v_k - beta_{k-1} v_{k-1}; beta_k = ||w||  (4 launches)
     void step(int64_t k, double* alpha, double* beta) {
-        k_spmv<<<spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, v, w.get());
-        k_dot_partial<<<RB, TB, 0, s>>>(n, v, w.get(), part.get(), nullptr);
-        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), alpha + k, 0);
-        k_axpy2<<<nblk(n), TB, 0, s>>>(n, w.get(), v, vp, alpha + k,
-                                       k > 0 ? beta + k - 1 : zero.get());
-        k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get(), nullptr);
+        k_spmv_dot<<<kSpmvBlocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, v,
+                                              w.get(), part.get());
+        k_sum_partials<<<1, TB, 0, s>>>(kSpmvBlocks, part.get(), alpha + k, 0);
+        k_axpy2_norm<<<RB, TB, 0, s>>>(n, w.get(), v, vp, alpha + k,
+                                       k > 0 ? beta + k - 1 : zero.get(), part.get());
         k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), beta + k, 1);
         VXQ_CHECK_LAUNCH();
     }
 
-    // v_{k+1} = w / beta_k
+    // v_{k+1} = w / beta_k (stored as basis row k+1 when it fits)
     void advance(int64_t k, const double* beta) {
         std::swap(vp, v);
-        k_scale_into<<<nblk(n), TB, 0, s>>>(n, w.get(), beta + k, v);
+        k_scale_store<<<nblk(n), TB, 0, s>>>(n, w.get(), beta + k, v, basis_row(k + 1));
         VXQ_CHECK_LAUNCH();
     }
 };
@@ -386,6 +471,16 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
     DevBuf<double> alpha(kmax + 1, s), beta(kmax + 1, s), nrm(1, s), theta(1, s), rho(1, s),
         u(kmax + 1, s), l(kmax + 1, s), d(kmax + 1, s);
     Lanczos lz(p, sign, s);
+    // keep the Lanczos basis while it fits a quarter of the free memory (<= 16 GB): the
+    // Ritz vector is then one pass over it instead of a replay of the recurrence
+    {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+            const double budget = std::min<double>((double)fr / 4, 16.0 * (1ull << 30));
+            lz.basis_cap = std::min<int64_t>(kmax + 1, (int64_t)(budget / (8.0 * n)));
+            lz.storing = lz.basis_cap >= Lanczos::kChunk;
+        }
+    }
     lz.start(nrm.get());
     EigInfo r;
     int64_t kk = -1;  // T_{kk} converged (size kk)
@@ -441,18 +536,31 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
         r.method = kEigGershgorin;
         return r;
     }
-    // replay the recurrence (same kernels, same start => the same v_j) and assemble the
-    // Ritz vector y = sum_j u_j v_j, then the explicit residual ||B y - theta y|| / ||y||
+    // the Ritz vector y = sum_j u_j v_j -- from the stored basis, or by replaying the
+    // recurrence (same kernels, same start => the same v_j) -- then the explicit residual
+    // ||B y - theta y|| / ||y||
     DevBuf<double> y(n, s), by(n, s), ynrm(1, s), rnrm(1, s);
-    VXQ_CUDA(cudaMemsetAsync(y.get(), 0, n * sizeof(double), s));
-    DevBuf<double> alpha2(kk, s), beta2(kk, s);
-    lz.start(nrm.get());
-    for (int64_t j = 0; j < kk; ++j) {
-        k_axpy<<<nblk(n), TB, 0, s>>>(n, y.get(), lz.v, u.get() + j);
+    if (lz.storing && kk <= lz.basis_rows) {
+        for (int64_t c = 0; c * Lanczos::kChunk < kk; ++c) {
+            const int64_t rows = std::min<int64_t>(Lanczos::kChunk, kk - c * Lanczos::kChunk);
+            k_basis_combine<<<nblk(n), TB, 0, s>>>(n, rows, lz.chunks[c].get(),
+                                                   u.get() + c * Lanczos::kChunk, y.get(),
+                                                   c > 0);
+        }
         VXQ_CHECK_LAUNCH();
-        if (j + 1 == kk) break;
-        lz.step(j, alpha2.get(), beta2.get());
-        lz.advance(j, beta2.get());
+    } else {
+        VXQ_CUDA(cudaMemsetAsync(y.get(), 0, n * sizeof(double), s));
+        DevBuf<double> alpha2(kk, s), beta2(kk, s);
+        lz.storing = false;
+        lz.chunks.clear();
+        lz.start(nrm.get());
+        for (int64_t j = 0; j < kk; ++j) {
+            k_axpy<<<nblk(n), TB, 0, s>>>(n, y.get(), lz.v, u.get() + j);
+            VXQ_CHECK_LAUNCH();
+            if (j + 1 == kk) break;
+            lz.step(j, alpha2.get(), beta2.get());
+            lz.advance(j, beta2.get());
+        }
     }
     k_spmv<<<lz.spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, y.get(),
                                          by.get());
