@@ -517,6 +517,8 @@ def run_ours(args):
 
     rowpart = args.config == "cfg5" and world > 1
     if rowpart:
+        R_job = R  # every rank steps all R replicas of its rows
+    if rowpart:
         # config 5: the instance is split by rows (strong scaling); every rank holds the
         # generated problem and all-gathers the bit-packed spins after each step (NCCL)
         from paper_2501_19221_b200.rowpart import (GpuSession, PeerExchange,
