@@ -21,9 +21,12 @@
 //       (eigen.py:21-32).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <chrono>
 
 #include "vxq_internal.h"
 
@@ -184,8 +187,8 @@ __global__ void k_scale_into(int64_t n, const double* w, const double* nrm, doub
 }
 
 // fused Lanczos step pieces (fixed grids and reduction orders: deterministic)
-// w = sign * A v (warp per row, grid-stride over rows); part[b] = this block's sum v_i w_i
-constexpr int kSpmvBlocks = 148 * 8;
+// w = sign * A v (one warp per row, one row per warp: short rows are latency-bound, so every
+// row gets its own warp); part[b] = this block's sum v_i w_i
 __global__ void __launch_bounds__(TB) k_spmv_dot(int64_t n, const int64_t* indptr,
                                                  const int32_t* indices, const double* data,
                                                  double sign, const double* v, double* w,
@@ -193,8 +196,8 @@ __global__ void __launch_bounds__(TB) k_spmv_dot(int64_t n, const int64_t* indpt
     __shared__ double sh[TB / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double dsum = 0.0;
-    for (int64_t row = (int64_t)blockIdx.x * (TB / 32) + wid; row < n;
-         row += (int64_t)gridDim.x * (TB / 32)) {
+    const int64_t row = (int64_t)blockIdx.x * (TB / 32) + wid;
+    if (row < n) {
         double acc = 0.0;
         for (int64_t k = indptr[row] + lane; k < indptr[row + 1]; k += 32)
             acc += data[k] * v[indices[k]];
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(TB) k_spmv_dot(int64_t n, const int64_t* indpt
         acc *= sign;
         if (lane == 0) {
             w[row] = acc;
-            dsum += v[row] * acc;
+            dsum = v[row] * acc;
         }
     }
     if (lane == 0) sh[wid] = dsum;
@@ -426,7 +429,7 @@ struct Lanczos {
 
     Lanczos(const Problem* p_, double sign_, cudaStream_t s_)
         : n(p_->n), p(p_), sign(sign_), s(s_), v0(n, s_), v1(n, s_), w(n, s_),
-          part(std::max(RB, kSpmvBlocks), s_), zero(1, s_) {
+          part(std::max<int64_t>(RB, ceil_div(n * 32, TB)), s_), zero(1, s_) {
         spmv_blocks = (unsigned)ceil_div(n * 32, TB);
         VXQ_CUDA(cudaMemsetAsync(zero.get(), 0, sizeof(double), s));
     }
@@ -445,9 +448,9 @@ struct Lanczos {
 
     // step k: w = B v_k - alpha_k v_k - beta_{k-1} v_{k-1}; beta_k = ||w||  (4 launches)
     void step(int64_t k, double* alpha, double* beta) {
-        k_spmv_dot<<<kSpmvBlocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, v,
+        k_spmv_dot<<<spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, v,
                                               w.get(), part.get());
-        k_sum_partials<<<1, TB, 0, s>>>(kSpmvBlocks, part.get(), alpha + k, 0);
+        k_sum_partials<<<1, TB, 0, s>>>((int)spmv_blocks, part.get(), alpha + k, 0);
         k_axpy2_norm<<<RB, TB, 0, s>>>(n, w.get(), v, vp, alpha + k,
                                        k > 0 ? beta + k - 1 : zero.get(), part.get());
         k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), beta + k, 1);
@@ -464,6 +467,11 @@ struct Lanczos {
 
 EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
     const int64_t n = p->n;
+    const bool timing = getenv("VXQ_EIG_TIMING") != nullptr;  // debugging: phase times
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t_begin = now();
+    double check_ms = 0.0;
     int64_t cap = kMaxIter;
     if (const char* e = getenv("VXQ_LANCZOS_MAXITER"))  // tests: force the fallback
         cap = std::max<int64_t>(1, atoll(e));
@@ -491,6 +499,7 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
         lz.step(k, alpha.get(), beta.get());
         const bool last = k + 1 == kmax;
         if (last || k + 1 == next_check) {
+            const auto tc = now();
             // an (almost) invariant subspace ends the recurrence at the first tiny beta
             hb.resize(k + 1 - last_check);
             VXQ_CUDA(cudaMemcpyAsync(hb.data(), beta.get() + last_check,
@@ -513,6 +522,7 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
             last_check = k + 1;
             // check interval grows with k (at most ~6 % extra steps past convergence)
             next_check = k + 1 + std::max<int64_t>(10, ((k + 1) / 16) / 10 * 10);
+            if (timing) check_ms += ms(tc, now());
             if (breakdown || res_est <= kTol * std::fabs(th)) {
                 kk = size;
                 break;
@@ -536,6 +546,7 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
         r.method = kEigGershgorin;
         return r;
     }
+    const auto t_iter = now();
     // the Ritz vector y = sum_j u_j v_j -- from the stored basis, or by replaying the
     // recurrence (same kernels, same start => the same v_j) -- then the explicit residual
     // ||B y - theta y|| / ||y||
@@ -570,6 +581,10 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
     k_sum_partials<<<1, TB, 0, s>>>(RB, lz.part.get(), rnrm.get(), 1);
     VXQ_CHECK_LAUNCH();
     const double yn = to_host(ynrm.get(), s), rn = to_host(rnrm.get(), s);
+    if (timing)
+        fprintf(stderr, "[vxq eig] n=%lld steps=%lld iterate %.1f ms (checks %.1f) ritz+residual "
+                "%.1f ms stored=%d\n", (long long)n, (long long)kk, ms(t_begin, t_iter), check_ms,
+                ms(t_iter, now()), (int)(lz.storing && kk <= lz.basis_rows));
     r.theta = th;
     r.residual = rn / yn;
     r.value = th + r.residual;  // eigen.py:56: theta + residual for "max"
