@@ -9,11 +9,13 @@
 //       eigenvalue by Sturm bisection -- the exact value to a few ulps of ||B||.
 //   n > 512 (eigen.py:50-56): the reference runs ARPACK (k=1, 'LA', tol 1e-8) and returns
 //       theta + ||B v - theta v||, the Ritz value pushed outward by its residual.  Here:
-//       Lanczos without reorthogonalisation; every check computes the largest Ritz value
-//       theta of T_k and, by inverse iteration on T_k, the residual estimate
-//       |beta_k u_k| of its Ritz vector; converged when that is <= tol |theta| (ARPACK's
-//       criterion, tol 1e-8).  Then the recurrence is replayed from the same start vector
-//       (identical kernels => identical v_j) to assemble y = sum_j u_j v_j, and the
+//       Lanczos without reorthogonalisation (the O(nnz) steps on the device); every check
+//       computes, on the host as ARPACK does for its small projected problem, the largest
+//       Ritz value theta of the k x k tridiagonal T_k and, by inverse iteration on T_k, the
+//       residual estimate |beta_k u_k| of its Ritz vector; converged when that is
+//       <= tol |theta| (ARPACK's criterion, tol 1e-8).  Then y = sum_j u_j v_j is assembled
+//       from the Lanczos basis (kept in pool memory while it fits; else the recurrence is
+//       replayed from the same start vector: identical kernels => identical v_j), and the
 //       returned value is theta + ||B y - theta y|| / ||y|| -- the explicit residual, as
 //       the reference computes it.
 //   No convergence within the iteration cap (eigen.py:49-52: ArpackNoConvergence): the
@@ -24,9 +26,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <vector>
-
 #include <chrono>
+#include <vector>
 
 #include "vxq_internal.h"
 
@@ -326,45 +327,6 @@ __global__ void __launch_bounds__(kMS) k_tridiag_max(int64_t k, const double* a,
     }
 }
 
-// Ritz vector of theta = lambda_max(T_k): two steps of inverse iteration with
-// M = (theta + delta) I - T_k, which is positive definite, so its LDL^T needs no pivoting
-// (delta grows tenfold if rounding leaves a non-positive pivot).  u[0..k) normalised;
-// out[0] = |beta_{k-1} u_{k-1}|, the residual norm ||B y - theta y|| of y = V_k u in exact
-// arithmetic (ARPACK's convergence estimate).  l, d: [k] scratch.
-__global__ void k_ritz_vector(int64_t k, const double* a, const double* b, const double* theta,
-                              double* u, double* l, double* d, double* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double tn = 0.0;
-    for (int64_t i = 0; i < k; ++i)
-        tn = fmax(tn, fabs(a[i]) + (i > 0 ? fabs(b[i - 1]) : 0.0) + (i + 1 < k ? fabs(b[i]) : 0.0));
-    double delta = 1e-11 * fmax(tn, 1e-300);
-    for (int attempt = 0; attempt < 8; ++attempt, delta *= 10.0) {
-        const double mu = *theta + delta;
-        bool ok = true;
-        d[0] = mu - a[0];
-        if (!(d[0] > 0)) ok = false;
-        for (int64_t i = 1; ok && i < k; ++i) {
-            l[i] = -b[i - 1] / d[i - 1];
-            d[i] = (mu - a[i]) - b[i - 1] * b[i - 1] / d[i - 1];
-            if (!(d[i] > 0)) ok = false;
-        }
-        if (!ok) continue;
-        for (int64_t i = 0; i < k; ++i) u[i] = 1.0;
-        for (int it = 0; it < 2; ++it) {
-            for (int64_t i = 1; i < k; ++i) u[i] -= l[i] * u[i - 1];  // L y = u
-            for (int64_t i = 0; i < k; ++i) u[i] /= d[i];             // D z = y
-            for (int64_t i = k - 2; i >= 0; --i) u[i] -= l[i + 1] * u[i + 1];  // L^T x = z
-            double s = 0.0;
-            for (int64_t i = 0; i < k; ++i) s += u[i] * u[i];
-            s = 1.0 / sqrt(s);
-            for (int64_t i = 0; i < k; ++i) u[i] *= s;
-        }
-        out[0] = fabs(b[k - 1] * u[k - 1]);
-        return;
-    }
-    out[0] = INFINITY;  // no usable factorisation: report "not converged"
-}
-
 // Gershgorin bound of B = -A (zero diagonal): max_i sum_j |A_ij|
 __global__ void k_row_abs_max(int64_t n, const int64_t* indptr, const double* data,
                               unsigned long long* maxbits) {
@@ -383,6 +345,74 @@ T to_host(const T* dev, cudaStream_t s) {
     VXQ_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
     VXQ_CUDA(cudaStreamSynchronize(s));
     return h;
+}
+
+// ---- host side of the convergence checks (T_k is k x k: O(k) work per check, like the
+// small dense problems ARPACK itself solves on the host; the O(nnz) work stays on the GPU)
+int sturm_count_host(int64_t k, const double* a, const double* b, double x) {
+    int c = 0;
+    double q = a[0] - x;
+    if (q < 0) ++c;
+    for (int64_t i = 1; i < k; ++i) {
+        const double d = (q == 0.0) ? 1e-300 : q;
+        q = a[i] - x - b[i - 1] * b[i - 1] / d;
+        if (q < 0) ++c;
+    }
+    return c;
+}
+
+// largest eigenvalue of T_k by bisection on the Sturm count (Gershgorin bracket)
+double tridiag_max_host(int64_t k, const double* a, const double* b) {
+    double lo = 1e300, hi = -1e300;
+    for (int64_t i = 0; i < k; ++i) {
+        const double r = (i > 0 ? std::fabs(b[i - 1]) : 0.0) + (i < k - 1 ? std::fabs(b[i]) : 0.0);
+        lo = std::fmin(lo, a[i] - r);
+        hi = std::fmax(hi, a[i] + r);
+    }
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        if (sturm_count_host(k, a, b, mid) >= k) hi = mid;
+        else lo = mid;
+    }
+    return hi;
+}
+
+// Ritz vector u of theta = lambda_max(T_k) by two steps of inverse iteration with the
+// positive-definite (theta + delta) I - T_k (LDL^T without pivoting; delta grows tenfold if
+// rounding leaves a non-positive pivot); returns |beta_{k-1} u_{k-1}| (ARPACK's residual
+// estimate), +inf if no factorisation was usable
+double ritz_vector_host(int64_t k, const double* a, const double* b, double theta,
+                        std::vector<double>& u) {
+    std::vector<double> l(k), d(k);
+    u.assign(k, 1.0);
+    double tn = 0.0;
+    for (int64_t i = 0; i < k; ++i)
+        tn = std::fmax(tn, std::fabs(a[i]) + (i > 0 ? std::fabs(b[i - 1]) : 0.0) +
+                               (i + 1 < k ? std::fabs(b[i]) : 0.0));
+    double delta = 1e-11 * std::fmax(tn, 1e-300);
+    for (int attempt = 0; attempt < 8; ++attempt, delta *= 10.0) {
+        const double mu = theta + delta;
+        bool ok = (d[0] = mu - a[0]) > 0;
+        for (int64_t i = 1; ok && i < k; ++i) {
+            l[i] = -b[i - 1] / d[i - 1];
+            d[i] = (mu - a[i]) - b[i - 1] * b[i - 1] / d[i - 1];
+            ok = d[i] > 0;
+        }
+        if (!ok) continue;
+        u.assign(k, 1.0);
+        for (int it = 0; it < 2; ++it) {
+            for (int64_t i = 1; i < k; ++i) u[i] -= l[i] * u[i - 1];
+            for (int64_t i = 0; i < k; ++i) u[i] /= d[i];
+            for (int64_t i = k - 2; i >= 0; --i) u[i] -= l[i + 1] * u[i + 1];
+            double ss = 0.0;
+            for (int64_t i = 0; i < k; ++i) ss += u[i] * u[i];
+            ss = 1.0 / std::sqrt(ss);
+            for (int64_t i = 0; i < k; ++i) u[i] *= ss;
+        }
+        return std::fabs(b[k - 1] * u[k - 1]);
+    }
+    return INFINITY;
 }
 
 EigInfo eig_max_small(const Problem* p, double sign, cudaStream_t s) {
@@ -422,9 +452,31 @@ struct Lanczos {
     double* basis_row(int64_t j) {  // row j of the stored basis, allocating its chunk
         if (!storing || j >= basis_cap) return nullptr;
         const int64_t c = j / kChunk;
-        if (c >= (int64_t)chunks.size()) chunks.emplace_back((size_t)kChunk * n, s);
+        if (c >= (int64_t)chunks.size()) {
+            // only from memory the pool already holds: growing it maps fresh pages (seconds
+            // for GBs), far more than replaying the recurrence costs
+            if (!pool_has((size_t)kChunk * n * sizeof(double))) {
+                storing = false;
+                return nullptr;
+            }
+            chunks.emplace_back((size_t)kChunk * n, s);
+        }
         basis_rows = std::max(basis_rows, j + 1);
         return chunks[c].get() + (j % kChunk) * n;
+    }
+
+    static bool pool_has(size_t bytes) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess)
+            return false;
+        uint64_t reserved = 0, used = 0;
+        if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) !=
+                cudaSuccess ||
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) != cudaSuccess)
+            return false;
+        return reserved >= used + bytes + bytes / 2;  // headroom for fragmentation
     }
 
     Lanczos(const Problem* p_, double sign_, cudaStream_t s_)
@@ -476,8 +528,9 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
     if (const char* e = getenv("VXQ_LANCZOS_MAXITER"))  // tests: force the fallback
         cap = std::max<int64_t>(1, atoll(e));
     const int64_t kmax = std::min<int64_t>(n, cap);
-    DevBuf<double> alpha(kmax + 1, s), beta(kmax + 1, s), nrm(1, s), theta(1, s), rho(1, s),
-        u(kmax + 1, s), l(kmax + 1, s), d(kmax + 1, s);
+    DevBuf<double> alpha(kmax + 1, s), beta(kmax + 1, s), nrm(1, s), theta(1, s),
+        u(kmax + 1, s);
+    std::vector<double> ha, hb, hu;  // host copies of T_k and the Ritz vector
     Lanczos lz(p, sign, s);
     // keep the Lanczos basis while it fits a quarter of the free memory (<= 16 GB): the
     // Ritz vector is then one pass over it instead of a replay of the recurrence
@@ -494,37 +547,44 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
     int64_t kk = -1;  // T_{kk} converged (size kk)
     double th = 0.0;
     int64_t next_check = 10, last_check = 0;
-    std::vector<double> hb;
     for (int64_t k = 0; k < kmax; ++k) {
         lz.step(k, alpha.get(), beta.get());
         const bool last = k + 1 == kmax;
         if (last || k + 1 == next_check) {
             const auto tc = now();
-            // an (almost) invariant subspace ends the recurrence at the first tiny beta
-            hb.resize(k + 1 - last_check);
-            VXQ_CUDA(cudaMemcpyAsync(hb.data(), beta.get() + last_check,
-                                     hb.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            // the new entries of T_k; theta and the Ritz vector of T_k on the host
+            ha.resize(k + 1);
+            hb.resize(k + 1);
+            VXQ_CUDA(cudaMemcpyAsync(ha.data() + last_check, alpha.get() + last_check,
+                                     (k + 1 - last_check) * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
+            VXQ_CUDA(cudaMemcpyAsync(hb.data() + last_check, beta.get() + last_check,
+                                     (k + 1 - last_check) * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
             VXQ_CUDA(cudaStreamSynchronize(s));
+            // an (almost) invariant subspace ends the recurrence at the first tiny beta
             int64_t size = k + 1;
             bool breakdown = false;
             for (int64_t j = last_check; j <= k; ++j)
-                if (!(hb[j - last_check] > 1e-12)) {
+                if (!(hb[j] > 1e-12)) {
                     size = j + 1;
                     breakdown = true;
                     break;
                 }
-            k_tridiag_max<<<1, kMS, 0, s>>>(size, alpha.get(), beta.get(), theta.get());
-            k_ritz_vector<<<1, 32, 0, s>>>(size, alpha.get(), beta.get(), theta.get(), u.get(),
-                                           l.get(), d.get(), rho.get());
-            VXQ_CHECK_LAUNCH();
-            th = to_host(theta.get(), s);
-            const double res_est = breakdown ? 0.0 : to_host(rho.get(), s);
+            th = tridiag_max_host(size, ha.data(), hb.data());
+            double res_est = ritz_vector_host(size, ha.data(), hb.data(), th, hu);
+            if (breakdown) res_est = 0.0;
             last_check = k + 1;
             // check interval grows with k (at most ~6 % extra steps past convergence)
             next_check = k + 1 + std::max<int64_t>(10, ((k + 1) / 16) / 10 * 10);
             if (timing) check_ms += ms(tc, now());
             if (breakdown || res_est <= kTol * std::fabs(th)) {
                 kk = size;
+                VXQ_CUDA(cudaMemcpyAsync(u.get(), hu.data(), kk * sizeof(double),
+                                         cudaMemcpyHostToDevice, s));
+                VXQ_CUDA(cudaMemcpyAsync(theta.get(), &th, sizeof(double),
+                                         cudaMemcpyHostToDevice, s));
+                VXQ_CUDA(cudaStreamSynchronize(s));  // host sources go out of scope
                 break;
             }
         }
