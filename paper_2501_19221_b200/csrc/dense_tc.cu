@@ -491,8 +491,11 @@ __device__ __forceinline__ void decode_tile(const DenseRunArgs& a, int g, int tp
     const int rem = g % tps;
     const int per_group = mrows * a.group;
     const int grp = rem / per_group, w = rem % per_group;
-    mb = w / a.group;
-    nb = grp * a.group + w % a.group;
+    // the last group may be smaller (n_tiles not a multiple of group)
+    const int nt = tps / mrows;
+    const int gsz = min(a.group, nt - grp * a.group);
+    mb = w / gsz;
+    nb = grp * a.group + w % gsz;
 }
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
@@ -1316,8 +1319,7 @@ int choose_bn(int64_t n, int64_t R, int planes, int bn_max) {
 int pick_group(int n_tiles) {
     int gsz = 1;
     if (const char* e = getenv("VXQ_DENSE_GROUP")) gsz = std::max(1, atoi(e));
-    while (gsz > 1 && n_tiles % gsz) --gsz;
-    return gsz;
+    return std::min(gsz, std::max(n_tiles, 1));  // the last group may be smaller
 }
 
 template <Kind KD, int CL, bool PAIR = false, bool MX = false>

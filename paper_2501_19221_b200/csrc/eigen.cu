@@ -156,14 +156,26 @@ __global__ void k_dot_partial(int64_t n, const double* a, const double* b, doubl
     if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
 
-__global__ void k_sum_partials(int nb, const double* part, double* out, int root) {
-    __shared__ double sh[TB];
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < nb; i += TB) acc += part[i];
-    sh[threadIdx.x] = acc;
+// out = sum of nb partials (sqrt if root): 1024 threads, four independent accumulators per
+// thread so loads overlap (a 125k-entry sum was ~200 us when each add waited on its load);
+// fixed order => deterministic
+constexpr int kSumThreads = 1024;
+__global__ void __launch_bounds__(kSumThreads) k_sum_partials(int nb, const double* part,
+                                                              double* out, int root) {
+    __shared__ double sh[kSumThreads];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int i = threadIdx.x;
+    for (; i + 3 * kSumThreads < nb; i += 4 * kSumThreads) {
+        a0 += part[i];
+        a1 += part[i + kSumThreads];
+        a2 += part[i + 2 * kSumThreads];
+        a3 += part[i + 3 * kSumThreads];
+    }
+    for (; i < nb; i += kSumThreads) a0 += part[i];
+    sh[threadIdx.x] = (a0 + a1) + (a2 + a3);
     __syncthreads();
-    for (int o = TB / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    for (int o = kSumThreads / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
         __syncthreads();
     }
     if (threadIdx.x == 0) *out = root ? sqrt(sh[0]) : sh[0];
@@ -493,7 +505,7 @@ struct Lanczos {
         VXQ_CUDA(cudaMemsetAsync(vp, 0, n * sizeof(double), s));
         k_start_vec<<<nblk(n), TB, 0, s>>>(n, w.get());
         k_dot_partial<<<RB, TB, 0, s>>>(n, w.get(), w.get(), part.get(), nullptr);
-        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), nrm, 1);
+        k_sum_partials<<<1, kSumThreads, 0, s>>>(RB, part.get(), nrm, 1);
         k_scale_store<<<nblk(n), TB, 0, s>>>(n, w.get(), nrm, v, basis_row(0));
         VXQ_CHECK_LAUNCH();
     }
@@ -502,10 +514,10 @@ struct Lanczos {
     void step(int64_t k, double* alpha, double* beta) {
         k_spmv_dot<<<spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, v,
                                               w.get(), part.get());
-        k_sum_partials<<<1, TB, 0, s>>>((int)spmv_blocks, part.get(), alpha + k, 0);
+        k_sum_partials<<<1, kSumThreads, 0, s>>>((int)spmv_blocks, part.get(), alpha + k, 0);
         k_axpy2_norm<<<RB, TB, 0, s>>>(n, w.get(), v, vp, alpha + k,
                                        k > 0 ? beta + k - 1 : zero.get(), part.get());
-        k_sum_partials<<<1, TB, 0, s>>>(RB, part.get(), beta + k, 1);
+        k_sum_partials<<<1, kSumThreads, 0, s>>>(RB, part.get(), beta + k, 1);
         VXQ_CHECK_LAUNCH();
     }
 
@@ -636,9 +648,9 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
     k_spmv<<<lz.spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, y.get(),
                                          by.get());
     k_dot_partial<<<RB, TB, 0, s>>>(n, y.get(), y.get(), lz.part.get(), nullptr);
-    k_sum_partials<<<1, TB, 0, s>>>(RB, lz.part.get(), ynrm.get(), 1);
+    k_sum_partials<<<1, kSumThreads, 0, s>>>(RB, lz.part.get(), ynrm.get(), 1);
     k_dot_partial<<<RB, TB, 0, s>>>(n, by.get(), y.get(), lz.part.get(), theta.get());
-    k_sum_partials<<<1, TB, 0, s>>>(RB, lz.part.get(), rnrm.get(), 1);
+    k_sum_partials<<<1, kSumThreads, 0, s>>>(RB, lz.part.get(), rnrm.get(), 1);
     VXQ_CHECK_LAUNCH();
     const double yn = to_host(ynrm.get(), s), rn = to_host(rnrm.get(), s);
     if (timing)
