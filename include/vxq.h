@@ -46,7 +46,7 @@ extern "C" {
 #define VXQ_API
 #endif
 
-#define VXQ_ABI_VERSION 3
+#define VXQ_ABI_VERSION 4  /* 4: eig_info, dense_eligible, outputs.dense_kind, session snapshots */
 
 #define VXQ_OK 0
 #define VXQ_ERR_INVALID 1     /* -> ValidationError */

@@ -230,6 +230,32 @@ __global__ void __launch_bounds__(TB) k_spmv_dot(int64_t n, const int64_t* indpt
     }
 }
 
+// the same for short rows (mean degree < 16): one THREAD per row -- a warp per 3-entry row
+// leaves 29 lanes idle and needs ~n/9472 dependent load waves (n = 10^6: ~200 us per step)
+__global__ void __launch_bounds__(TB) k_spmv_dot_rows(int64_t n, const int64_t* indptr,
+                                                      const int32_t* indices,
+                                                      const double* data, double sign,
+                                                      const double* v, double* w,
+                                                      double* part) {
+    __shared__ double sh[TB];
+    const int64_t row = (int64_t)blockIdx.x * TB + threadIdx.x;
+    double d = 0.0;
+    if (row < n) {
+        double acc = 0.0;
+        for (int64_t k = indptr[row]; k < indptr[row + 1]; ++k) acc += data[k] * v[indices[k]];
+        acc *= sign;
+        w[row] = acc;
+        d = v[row] * acc;
+    }
+    sh[threadIdx.x] = d;
+    __syncthreads();
+    for (int o = TB / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
 // w = w - alpha v - beta vprev; part[b] = this block's sum w_i^2
 __global__ void __launch_bounds__(TB) k_axpy2_norm(int64_t n, double* w, const double* v,
                                                    const double* vp, const double* alpha,
@@ -454,6 +480,7 @@ struct Lanczos {
     double* vp;
     double* v;
     unsigned spmv_blocks;
+    bool short_rows;  // mean row length < 16: one thread per row
     // stored basis V[j] = v_j for j < basis_rows, grown in chunks of kChunk rows while the
     // total stays within basis_cap rows (memory comes from the retained stream-ordered pool)
     static constexpr int64_t kChunk = 128;
@@ -494,7 +521,8 @@ struct Lanczos {
     Lanczos(const Problem* p_, double sign_, cudaStream_t s_)
         : n(p_->n), p(p_), sign(sign_), s(s_), v0(n, s_), v1(n, s_), w(n, s_),
           part(std::max<int64_t>(RB, ceil_div(n * 32, TB)), s_), zero(1, s_) {
-        spmv_blocks = (unsigned)ceil_div(n * 32, TB);
+        short_rows = p_->nnz < 16 * n;
+        spmv_blocks = (unsigned)ceil_div(short_rows ? n : n * 32, TB);
         VXQ_CUDA(cudaMemsetAsync(zero.get(), 0, sizeof(double), s));
     }
 
@@ -512,8 +540,12 @@ struct Lanczos {
 
     // step k: w = B v_k - alpha_k v_k - beta_{k-1} v_{k-1}; beta_k = ||w||  (4 launches)
     void step(int64_t k, double* alpha, double* beta) {
-        k_spmv_dot<<<spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, v,
-                                              w.get(), part.get());
+        if (short_rows)
+            k_spmv_dot_rows<<<spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64,
+                                                       sign, v, w.get(), part.get());
+        else
+            k_spmv_dot<<<spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, v,
+                                                  w.get(), part.get());
         k_sum_partials<<<1, kSumThreads, 0, s>>>((int)spmv_blocks, part.get(), alpha + k, 0);
         k_axpy2_norm<<<RB, TB, 0, s>>>(n, w.get(), v, vp, alpha + k,
                                        k > 0 ? beta + k - 1 : zero.get(), part.get());
@@ -645,8 +677,8 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
             lz.advance(j, beta2.get());
         }
     }
-    k_spmv<<<lz.spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, y.get(),
-                                         by.get());
+    k_spmv<<<(unsigned)ceil_div(n * 32, TB), TB, 0, s>>>(n, p->indptr, p->indices, p->data64,
+                                                         sign, y.get(), by.get());
     k_dot_partial<<<RB, TB, 0, s>>>(n, y.get(), y.get(), lz.part.get(), nullptr);
     k_sum_partials<<<1, kSumThreads, 0, s>>>(RB, lz.part.get(), ynrm.get(), 1);
     k_dot_partial<<<RB, TB, 0, s>>>(n, by.get(), y.get(), lz.part.get(), theta.get());

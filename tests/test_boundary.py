@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
-    assert L.vxq_abi_version() == 3
+    assert L.vxq_abi_version() == 4
 
 
 def test_struct_layouts_match_header():
