@@ -576,16 +576,10 @@ EigInfo eig_max_lanczos(const Problem* p, double sign, cudaStream_t s) {
         u(kmax + 1, s);
     std::vector<double> ha, hb, hu;  // host copies of T_k and the Ritz vector
     Lanczos lz(p, sign, s);
-    // keep the Lanczos basis while it fits a quarter of the free memory (<= 16 GB): the
-    // Ritz vector is then one pass over it instead of a replay of the recurrence
-    {
-        size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-            const double budget = std::min<double>((double)fr / 4, 16.0 * (1ull << 30));
-            lz.basis_cap = std::min<int64_t>(kmax + 1, (int64_t)(budget / (8.0 * n)));
-            lz.storing = lz.basis_cap >= Lanczos::kChunk;
-        }
-    }
+    // keep the Lanczos basis (<= 16 GB, only in memory the pool already holds: see
+    // basis_row) -- the Ritz vector is then one pass over it instead of a replay
+    lz.basis_cap = std::min<int64_t>(kmax + 1, (int64_t)(16.0 * (1ull << 30) / (8.0 * n)));
+    lz.storing = lz.basis_cap >= Lanczos::kChunk;
     lz.start(nrm.get());
     EigInfo r;
     int64_t kk = -1;  // T_{kk} converged (size kk)
