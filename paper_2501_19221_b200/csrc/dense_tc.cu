@@ -580,6 +580,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
     static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
     static_assert((KD != Kind::kFp8 && KD != Kind::kJ16x2) || XMS >= 2, "x/m staging slots");
+    // x/m slots are split between the two epilogue halves (chunk c goes to half c & 1) so
+    // each half waits on every phase of its own slots in order: with shared slots a half
+    // could wait on a slot two phases ahead of the loader and pass the parity check on a
+    // stale phase (the ABA of mbarrier parity waits)
+    constexpr int XHS = XMS / 2 > 0 ? XMS / 2 : 1;
     constexpr bool PA_KIND = KD == Kind::kFp8 || KD == Kind::kJ16x2;
     extern __shared__ uint8_t smem_raw[];
     __shared__ int s_last;  // fused tracking: this tile completed its step's decisions
@@ -900,8 +905,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         if (a.xm && a.mode == 0 && ptx::elect_one()) {
             const uint64_t pol = ptx::policy_evict_first();
             const int nch = a.bn / 16;
-            int slot = 0;
-            uint32_t ph = 0;
+            int jh[2] = {0, 0};  // chunks loaded per epilogue half
             for (int k = 0;; ++k) {
                 const int g = next_ticket(k);
                 release_ticket(k);
@@ -926,17 +930,15 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 for (int c = 0; c < nch; ++c) {
-                    ptx::mbar_wait(xempty + slot, ph ^ 1, a.timeout_ns);
+                    const int h = c & 1, j = jh[h]++;
+                    const int slot = h * XHS + j % XHS;
+                    ptx::mbar_wait(xempty + slot, ((uint32_t)(j / XHS) & 1u) ^ 1u, a.timeout_ns);
                     uint8_t* xs = xm_smem + slot * XM_SLOT_BYTES;
                     ptx::mbar_arrive_expect_tx(xfull + slot, XM_SLOT_BYTES);
                     ptx::tma_load_2d_hint(xs, &tmX, xfull + slot, mb * DBM, nb * a.bn + c * 16,
                                           pol);
                     ptx::tma_load_2d_hint(xs + XM_SLOT_BYTES / 2, &tmM, xfull + slot, mb * DBM,
                                           nb * a.bn + c * 16, pol);
-                    if (++slot == XMS) {
-                        slot = 0;
-                        ph ^= 1;
-                    }
                 }
             }
         }
@@ -952,7 +954,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         const int nch = a.bn / 16;
         float* __restrict__ xg = a.x;
         float* __restrict__ mg = a.m;
-        int lt = 0, xm_tiles = 0;
+        int lt = 0, xm_chunks = 0;  // x/m chunks this half consumed
         long long ep_wait = 0, ep_busy = 0, ep_xwait = 0;
         for (int k = 0;; ++k, ++lt) {
             const int g = next_ticket(k);
@@ -1168,10 +1170,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     if (tile_ok) {
 #pragma unroll 1
                         for (int c = half; c < nch; c += 2) {
-                            const int seq = xm_tiles * nch + c;
-                            const int slot = seq % XMS;
+                            const int slot = half * XHS + xm_chunks % XHS;
+                            const uint32_t par = (uint32_t)(xm_chunks / XHS) & 1u;
+                            ++xm_chunks;
                             const long long cx = (a.stats && ep_tid == 0) ? clk() : 0;
-                            ptx::mbar_wait(xfull + slot, (uint32_t)(seq / XMS) & 1u, a.timeout_ns);
+                            ptx::mbar_wait(xfull + slot, par, a.timeout_ns);
                             if (a.stats && ep_tid == 0) ep_xwait += clk() - cx;
                             const float* xs =
                                 reinterpret_cast<const float*>(xm_smem + slot * XM_SLOT_BYTES);
@@ -1186,7 +1189,6 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             if (fast_ok && nb * a.bn + c * 16 + 16 <= a.R) process_fast(c, xA, mA);
                             else process(c, xA, mA);
                         }
-                        ++xm_tiles;
                     }
                 } else {
 #pragma unroll 1
