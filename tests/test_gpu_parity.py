@@ -598,3 +598,22 @@ def test_dense_sbm_fp16_range_fallbacks():
                                       init_noise=3e4), want_state=True)
     assert rg.info["path"] == "sparse"
     assert np.array_equal(rg.energies, O.energies_exact(g, rg.states))
+
+
+@pytest.mark.parametrize("group", ["2", "3"])
+def test_dense_tile_order_does_not_change_results(group, monkeypatch):
+    """The dense kernels' tile order (replica blocks grouped per row panel, the last group
+    possibly smaller; the dynamic tile queue hands tiles out in that order) changes when
+    tiles run, never what they compute: PA and exact-field SBM are bit-identical to the
+    default order."""
+    m = sk_model(1000, 12)
+    pa = vxq.PaParams(steps=15, replicas=1024, seed=3)
+    sb = vxq.SbmParams(steps=15, dt=0.05, replicas=400, seed=3, c0=0.4)
+    ref_pa = vxq.run_pa(m, pa, want_state=True)
+    ref_sb = vxq.run_sbm(m, sb, want_state=True)
+    monkeypatch.setenv("VXQ_DENSE_GROUP", group)
+    r_pa = vxq.run_pa(m, pa, want_state=True)
+    r_sb = vxq.run_sbm(m, sb, want_state=True)
+    assert r_pa.info["path"] == "dense" and r_sb.info["dense_kind"] == "i8x3"
+    assert np.array_equal(r_pa.x, ref_pa.x) and np.array_equal(r_pa.m, ref_pa.m)
+    assert np.array_equal(r_sb.x, ref_sb.x) and np.array_equal(r_sb.m, ref_sb.m)
