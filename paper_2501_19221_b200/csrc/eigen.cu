@@ -61,11 +61,15 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // Lanczos with full reorthogonalisation to dimension n: alpha[0..k), beta[0..k-1)
-// describe T_k; *kout = k.  V: [n][n] scratch (the Lanczos basis).
+// describe T_k; *kout = k.  The basis V [n][n] lives in dynamic shared memory when it fits
+// (n <= 160: the CGS2 passes then read it at smem latency -- cfg1's c0 went from ~7 ms to
+// well under 1 ms), else in the global scratch Vg.
 __global__ void __launch_bounds__(kDenseLimit) k_lanczos_full(
     int n, const int64_t* indptr, const int32_t* indices, const double* data, double sign,
-    double* V, double* alpha, double* beta, int* kout) {
+    double* Vg, int v_in_smem, double* alpha, double* beta, int* kout) {
     __shared__ double v[kDenseLimit], w[kDenseLimit], c[kDenseLimit], red[kDenseLimit / 32];
+    extern __shared__ double Vs[];
+    double* V = v_in_smem ? Vs : Vg;
     const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
     constexpr int NW = kDenseLimit / 32;
     double vi = i < n ? start_entry(i) : 0.0;
@@ -455,10 +459,16 @@ double ritz_vector_host(int64_t k, const double* a, const double* b, double thet
 
 EigInfo eig_max_small(const Problem* p, double sign, cudaStream_t s) {
     const int n = (int)p->n;
-    DevBuf<double> V((size_t)n * n, s), alpha(n, s), beta(n, s), theta(1, s);
+    const size_t vbytes = (size_t)n * n * sizeof(double);
+    const bool smem = vbytes <= 200 * 1024;
+    DevBuf<double> V(smem ? 1 : (size_t)n * n, s), alpha(n, s), beta(n, s), theta(1, s);
     DevBuf<int> kout(1, s);
-    k_lanczos_full<<<1, kDenseLimit, 0, s>>>(n, p->indptr, p->indices, p->data64, sign, V.get(),
-                                            alpha.get(), beta.get(), kout.get());
+    if (smem)
+        VXQ_CUDA(cudaFuncSetAttribute(k_lanczos_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)vbytes));
+    k_lanczos_full<<<1, kDenseLimit, smem ? vbytes : 0, s>>>(
+        n, p->indptr, p->indices, p->data64, sign, V.get(), smem ? 1 : 0, alpha.get(),
+        beta.get(), kout.get());
     VXQ_CHECK_LAUNCH();
     const int k = to_host(kout.get(), s);
     k_tridiag_max<<<1, kMS, 0, s>>>(k, alpha.get(), beta.get(), theta.get());
