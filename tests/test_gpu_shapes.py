@@ -260,6 +260,26 @@ def test_dense_sbm_general_j_tolerance(T, tol):
     assert np.array_equal(r.energies[reps], O.energies_exact(m, r.states[reps]))
 
 
+@pytest.mark.parametrize("T,tol", [(10, 1e-5), (100, 5e-5)])
+def test_dense_pa_general_j_tolerance(T, tol):
+    """General dense J (Gaussian SK) on the tensor cores (k_dense_run<J16x2>: two fp16 J
+    planes x fp16 +-1 spins, f32 accumulation): within 1e-5 of the fp64 reference loop at
+    t = 10 and 5e-5 at t = 100 (the f32 tensor-core accumulation; the fp32 CSR
+    restatement is 2.2e-6 from fp64 here), no sign mismatch; energies exact."""
+    m = gaussian_sk(1000, 9)
+    R = 256
+    r = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=5), want_state=True)
+    assert r.info["path"] == "dense" and r.info["dense_kind"] == "j16x2"
+    reps = subset(R, 4)
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    X, M = O.pa_run(ip, ix, dv, m.h, O.pa_schedule(O.resolve_lambda0(m), T), 0.05, 0.9,
+                    pa_init_rows(5, reps, m.n), np.zeros((len(reps), m.n)))
+    assert np.abs(r.x[reps] - X).max() <= tol
+    assert np.abs(r.m[reps] - M).max() <= tol
+    assert np.array_equal(r.states[reps], np.where(X >= 0, 1, -1).astype(np.int8))
+    assert np.array_equal(r.energies[reps], O.energies_exact(m, r.states[reps]))
+
+
 # ------------------------------------------------------------------- config 4 (HBM path)
 def test_cfg4_full_shape_pa_and_sbm_replica_subset_bitexact():
     """cfg 4 as benchmarked: 3-regular MaxCut N = 10^6, R = 256, sparse path; 10 steps.
