@@ -247,7 +247,7 @@ def cpu_baseline(model, solver, R, T):
 
 # ----------------------------------------------------------------------------- time to target
 TTT_SWEEPS = {  # annealing schedules tried besides the timed one (reference defaults otherwise)
-    "cfg2": (500, 600, 700, 850, 2000, 5000, 10000, 20000),
+    "cfg2": (500, 700, 2000, 5000, 6000, 7000, 8000, 10000, 20000),
     "cfg1": (100, 200, 500, 2000), "cfg3": (200, 500, 2000, 5000), "cfg4": (200, 500, 2000, 5000),
 }
 
