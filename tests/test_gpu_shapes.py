@@ -341,6 +341,27 @@ def test_cfg3_full_shape_replica_subset_bitexact(solver):
     assert np.array_equal(r.order, np.argsort(r.energies, kind="stable"))
 
 
+@pytest.mark.parametrize("config,R,T", [("cfg3", 4096, 10), ("cfg4", 256, 10)])
+def test_fp64_parity_mode_at_benchmarked_shapes(config, R, T):
+    """The fp64 path -- which bench.py uses to produce the reference-equivalent best energy
+    (the time-to-target goal of cfg 3 / cfg 4) -- equals the oracle's fp64 restatement
+    bit for bit at the benchmarked shapes (the restatement equals the reference's scipy
+    CSR loop, tests/test_oracle.py), PA and SBM, first and last replicas."""
+    m = instances.build(config)
+    reps = subset(R)
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    r = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=0), precision="fp64",
+                   path="sparse", want_state=True)
+    X, M = O.pa_run(ip, ix, dv, m.h, O.pa_schedule(O.resolve_lambda0(m), T), 0.05, 0.9,
+                    pa_init_rows(0, reps, m.n), np.zeros((len(reps), m.n)))
+    assert np.array_equal(r.x[reps], X) and np.array_equal(r.m[reps], M)
+    s = vxq.run_sbm(m, vxq.SbmParams(steps=T, dt=0.05, replicas=R, seed=0, c0=0.3),
+                    precision="fp64", path="sparse", want_state=True)
+    Q, P = sbm_init_rows(0, reps, m.n)
+    Q, P = O.sbm_run(ip, ix, -dv, -m.h, O.sbm_schedule(1.0, T), 0.05, 1.0, 0.3, 1.0, Q, P)
+    assert np.array_equal(s.x[reps], Q) and np.array_equal(s.m[reps], P)
+
+
 # ------------------------------------------------------------------- config 1 snapshots
 @pytest.mark.parametrize("precision,tol", [("fp64", 1e-12), ("fp32", TOL32)])
 def test_cfg1_pa_short_horizon_snapshots(golden, precision, tol):
