@@ -34,6 +34,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -1337,6 +1338,8 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
     const int64_t items = (int64_t)((a.m_tiles + RPC - 1) / RPC) *
                           (PAIR && CL == 2 ? a.n_tiles / 2 : a.n_tiles) *
                           std::max<int64_t>(steps_for_grid, 1);
+    // tile tickets are 32-bit ints in the kernel (steps x tiles per step)
+    VXQ_REQUIRE(items < (int64_t)INT32_MAX - 4096, "too many dense tiles (steps x tiles) for one launch");
     int64_t clusters = std::min<int64_t>(items, num_sms() / NCTA);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(clusters * NCTA));
