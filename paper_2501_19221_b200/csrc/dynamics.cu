@@ -506,12 +506,33 @@ __host__ __device__ inline size_t resident_csr_bytes(int64_t n, int64_t nnz) {
     return align16((n + 1) * 4) + align16((size_t)nnz * 4) + align16((size_t)nnz * sizeof(T));
 }
 
-// f = sum_k val[k] * v(idx[k]) over [kb, ke) in order; v(j) provided by the callable
+// f = sum_k val[k] * v(idx[k]) over [kb, ke) in order; v(j) provided by the callable.
+// Long rows are software-pipelined: the shared-memory loads of batch b+1 (indices, values,
+// then the neighbours' states) are issued before batch b's adds, so the sum runs at the
+// rate of its dependent FADD chain instead of two shared-memory round trips per batch.
 template <typename T, typename F>
 __device__ __forceinline__ T row_sum(const ResidentSmem<T>& S, int kb, int ke, F&& v) {
     using O = Ops<T>;
+    constexpr int B = 8;
     T f = (T)0;
     int k = kb;
+    if (ke - kb >= 2 * B) {
+        T w[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) w[u] = v(S.idx[k + u], S.val[k + u]);
+        k += B;
+        for (; k + B <= ke; k += B) {
+            T wn[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) wn[u] = v(S.idx[k + u], S.val[k + u]);
+#pragma unroll
+            for (int u = 0; u < B; ++u) f = O::add(f, w[u]);
+#pragma unroll
+            for (int u = 0; u < B; ++u) w[u] = wn[u];
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) f = O::add(f, w[u]);
+    }
     for (; k + 4 <= ke; k += 4) {
         int j[4];
         T a[4], w[4];
