@@ -510,13 +510,15 @@ __host__ __device__ inline size_t resident_csr_bytes(int64_t n, int64_t nnz) {
 // Long rows are software-pipelined: the shared-memory loads of batch b+1 (indices, values,
 // then the neighbours' states) are issued before batch b's adds, so the sum runs at the
 // rate of its dependent FADD chain instead of two shared-memory round trips per batch.
-template <typename T, typename F>
+// (SBM resident step: cfg1 1.65 -> 1.41 us/step; the PA step, whose terms are a select of
+// +-a on a spin byte, measured no gain and keeps the plain loop: PIPE = false.)
+template <typename T, bool PIPE = true, typename F>
 __device__ __forceinline__ T row_sum(const ResidentSmem<T>& S, int kb, int ke, F&& v) {
     using O = Ops<T>;
     constexpr int B = 8;
     T f = (T)0;
     int k = kb;
-    if (ke - kb >= 2 * B) {
+    if (PIPE && ke - kb >= 2 * B) {
         T w[B];
 #pragma unroll
         for (int u = 0; u < B; ++u) w[u] = v(S.idx[k + u], S.val[k + u]);
@@ -582,8 +584,8 @@ __global__ void k_pa_resident(int64_t n64, int64_t R_pad, int V, int RG, int nnz
         for (int it = threadIdx.x; it < items; it += blockDim.x) {
             const int g = it / n, i = it - g * n;
             const uint8_t* sg = sc + g * n;
-            const T f = row_sum<T>(S, S.ptr[i], S.ptr[i + 1],
-                                   [&](int j, T a) { return sg[j] ? a : -a; });
+            const T f = row_sum<T, false>(S, S.ptr[i], S.ptr[i + 1],
+                                          [&](int j, T a) { return sg[j] ? a : -a; });
             const T xo = xs[it];
             const T grad = O::add(O::add(O::mul(lam, xo), f), __ldg(h + i));
             const T mn = O::sub(O::mul(alpha, ms[it]), O::mul(eta, grad));
