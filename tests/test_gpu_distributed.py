@@ -14,18 +14,21 @@ from helpers import gen_complete, maxcut_model
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("R", [96, 32])
 @pytest.mark.parametrize("solver", ["pa", "sbm"])
 @pytest.mark.parametrize("parts", [1, 2, 3])
-def test_row_partition_sessions_match_sparse_path(solver, parts):
+def test_row_partition_sessions_match_sparse_path(solver, parts, R):
+    """R = 32 runs the cooperative 8-rows-per-warp step kernels (config 5's shape), here
+    with row ranges that do not start at 0."""
     import torch
 
     from paper_2501_19221_b200.rowpart import GpuSession, exchange_row_bytes, row_split
     m = maxcut_model(3000, 3, 11) if solver == "pa" else gen_complete(8, 300, "gaussian")
     if solver == "pa":
-        params = vxq.PaParams(steps=40, replicas=96, seed=4)
+        params = vxq.PaParams(steps=40, replicas=R, seed=4)
         ref = vxq.run_pa(m, params, path="sparse")
     else:
-        params = vxq.SbmParams(steps=40, dt=0.05, replicas=96, seed=4, c0=0.1)
+        params = vxq.SbmParams(steps=40, dt=0.05, replicas=R, seed=4, c0=0.1)
         ref = vxq.run_sbm(m, params, path="sparse")
     spans, B = row_split(m.n, parts)
     rb = exchange_row_bytes(solver, params.replicas)

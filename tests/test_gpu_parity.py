@@ -617,3 +617,27 @@ def test_dense_tile_order_does_not_change_results(group, monkeypatch):
     assert r_pa.info["path"] == "dense" and r_sb.info["dense_kind"] == "i8x3"
     assert np.array_equal(r_pa.x, ref_pa.x) and np.array_equal(r_pa.m, ref_pa.m)
     assert np.array_equal(r_sb.x, ref_sb.x) and np.array_equal(r_sb.m, ref_sb.m)
+
+
+def test_sparse_sbm_r32_cooperative_step_matches_oracle():
+    """R = 32 (config 5's replica count) runs the cooperative SBM step (8 rows per warp,
+    CSR entries shuffled across the warp): bit-exact with the oracle's fp32 loop on an
+    irregular graph with rows longer than the 64-entry cooperative window."""
+    rng = np.random.default_rng(21)
+    n = 4000
+    r_, c_ = random_regular_edges(n, 6, 3)
+    extra_r = np.zeros(80, dtype=np.int64)  # row 0 gets 80 extra neighbours
+    extra_c = np.arange(1, 81, dtype=np.int64)
+    rows = np.r_[r_, extra_r]
+    cols = np.r_[c_, extra_c]
+    key = np.unique(rows * n + cols)
+    rows, cols = key // n, key % n
+    m = vxq.IsingModel.from_arrays(n, rows, cols, rng.uniform(-1, 1, len(rows)),
+                                   h=rng.uniform(-1, 1, n), canonical=True)
+    s = vxq.run_sbm(m, vxq.SbmParams(steps=30, dt=0.05, replicas=32, seed=2, c0=0.3),
+                    path="sparse", want_state=True)
+    ip, ix, dv = O.symmetric_csr(m.n, m.rows, m.cols, m.values)
+    Q, P = O.sbm_init(2, 32, m.n, 1.0)
+    Q, P = O.sbm_run(ip, ix, -dv, -m.h, O.sbm_schedule(1.0, 30), 0.05, 1.0, 0.3, 1.0, Q, P,
+                     np.float32)
+    assert np.array_equal(s.x, Q.astype(np.float64)) and np.array_equal(s.m, P.astype(np.float64))
