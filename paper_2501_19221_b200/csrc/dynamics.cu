@@ -471,99 +471,6 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
     st_cs<T, V>(p + pbase, pv);
 }
 
-// R <= 32 (one 32-replica q vector per row, V = 1): a warp owns RPW consecutive rows,
-// loads their row bounds and up to 64 CSR entries cooperatively (lane l <- entry base + l
-// and base + 32 + l), then walks each row's entries in ascending order with the column and
-// value broadcast by shuffles, issuing each batch's 128-byte q gathers before summing
-// them -- the same sequential per-row sum as k_sbm_step (bit-identical), with one CSR
-// round trip per RPW rows instead of per row.
-#ifndef VXQ_SBM_COOP
-#define VXQ_SBM_COOP 1
-#endif
-template <typename T, int RPW, bool MULTI = false>
-__global__ void __launch_bounds__(256, MULTI ? 4 : VXQ_COOP_MINB) k_sbm_step_coop(
-    int64_t row0, int64_t nrows, Operator<T> op, const T* __restrict__ g, SbmScalars<T> sc,
-    const T* __restrict__ q_in, T* __restrict__ q_one, const Dests<T> q_out,
-    T* __restrict__ p) {
-    using O = Ops<T>;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t il0 = warp * RPW;
-    if (il0 >= nrows) return;
-    const int nr = (int)min((int64_t)RPW, nrows - il0);
-    const int64_t myptr = lane <= nr ? __ldg(op.indptr + row0 + il0 + lane) : 0;
-    const int64_t kbase = __shfl_sync(0xffffffffu, myptr, 0);
-    const int64_t kend = __shfl_sync(0xffffffffu, myptr, nr);
-    // cooperative loads of entries [kbase, kbase + 64)
-    const int64_t k0 = kbase + lane, k1 = kbase + 32 + lane;
-    const bool v0 = k0 < kend, v1 = k1 < kend;
-    const int j0 = v0 ? __ldcs(op.indices + k0) : 0, j1 = v1 ? __ldcs(op.indices + k1) : 0;
-    const T a0 = v0 ? O::mul(op.sign, __ldcs(op.data + k0)) : (T)0;
-    const T a1 = v1 ? O::mul(op.sign, __ldcs(op.data + k1)) : (T)0;
-    auto entry = [&](int64_t k, int& j, T& a) {  // (column, value) of entry k, warp-uniform
-        const int64_t off = k - kbase;
-        if (off < 64) {
-            const int src = (int)(off & 31);
-            j = __shfl_sync(0xffffffffu, off < 32 ? j0 : j1, src);
-            a = __shfl_sync(0xffffffffu, off < 32 ? a0 : a1, src);
-        } else {  // rare: more than 64 entries in this warp's rows
-            j = __ldg(op.indices + k);
-            a = O::mul(op.sign, __ldg(op.data + k));
-        }
-    };
-#pragma unroll 1
-    for (int u = 0; u < nr; ++u) {
-        const int64_t kb = __shfl_sync(0xffffffffu, myptr, u);
-        const int64_t ke = __shfl_sync(0xffffffffu, myptr, u + 1);
-        const int64_t il = il0 + u, i = row0 + il;
-        const T qi = q_in[i * 32 + lane];
-        const T pi = __ldcs(p + il * 32 + lane);
-        T f = (T)0;
-        int64_t k = kb;
-        for (; k + 4 <= ke; k += 4) {
-            int j[4];
-            T a[4], qv[4];
-#pragma unroll
-            for (int w = 0; w < 4; ++w) entry(k + w, j[w], a[w]);
-#pragma unroll
-            for (int w = 0; w < 4; ++w) qv[w] = q_in[(int64_t)j[w] * 32 + lane];
-#pragma unroll
-            for (int w = 0; w < 4; ++w) f = O::add(f, O::mul(a[w], qv[w]));
-        }
-        if (k < ke) {  // 1-3 remaining entries: one gather round
-            const int rem = (int)(ke - k);
-            int j[3];
-            T a[3], qv[3];
-#pragma unroll
-            for (int w = 0; w < 3; ++w)
-                if (w < rem) entry(k + w, j[w], a[w]);
-#pragma unroll
-            for (int w = 0; w < 3; ++w)
-                if (w < rem) qv[w] = q_in[(int64_t)j[w] * 32 + lane];
-#pragma unroll
-            for (int w = 0; w < 3; ++w)
-                if (w < rem) f = O::add(f, O::mul(a[w], qv[w]));
-        }
-        const T gi = __ldg(g + i);
-        const T inner = -O::sub(O::add(O::mul(qi, qi), sc.a0), sc.a_t);
-        const T force = O::add(O::mul(inner, qi), O::mul(sc.c0, O::add(f, gi)));
-        T pn = O::add(pi, O::mul(sc.dt, force));
-        T qn = O::add(qi, O::mul(sc.dta0, pn));
-        if (fabs(qn) > sc.q_cap) {
-            qn = qn < -sc.q_cap ? -sc.q_cap : sc.q_cap;
-            pn = (T)0;
-        }
-        if constexpr (MULTI) {
-#pragma unroll
-            for (int d = 0; d < kMaxDests; ++d)
-                if (d < q_out.n) q_out.p[d][i * 32 + lane] = qn;
-        } else {
-            q_one[i * 32 + lane] = qn;
-        }
-        __stcs(p + il * 32 + lane, pn);
-    }
-}
-
 // ------------------------------------------------------------------ resident (small n)
 // One CTA owns RG replicas for all T steps: their state and the whole CSR (row pointers,
 // indices, values) live in shared memory, so the only per-step synchronisation is one
@@ -891,13 +798,8 @@ void launch_sbm_step_t(const Layout& L, const Operator<T>& op, const T* g, SbmSc
     int64_t warps = L.nrows * (L.R_pad / (32 * L.V));
     unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
     T* one = qo.p[0];
-    if (VXQ_SBM_COOP && L.R_pad == 32) {  // one q vector per row: cooperative warp-CSR
-        constexpr int RPW = 8;
-        const int64_t cw = ceil_div(L.nrows, RPW);
-        k_sbm_step_coop<T, RPW, MULTI><<<(unsigned)ceil_div(cw * 32, 256), 256, 0, s>>>(
-            L.row0, L.nrows, op, g, sc, qi, one, qo, p);
-        return;
-    }
+    // (a cooperative 8-rows-per-warp variant like k_pa_step_coop measured 23 % slower for
+    // R = 32 on config 5: one row per warp keeps 8x more 128-byte q gathers in flight)
     switch (L.V) {
         case 1: k_sbm_step<T, 1, MULTI><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, one, qo, p); break;
         case 2: k_sbm_step<T, 2, MULTI><<<blocks, 256, 0, s>>>(L.row0, L.nrows, L.R_pad, op, g, sc, qi, one, qo, p); break;

@@ -18,8 +18,8 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("solver", ["pa", "sbm"])
 @pytest.mark.parametrize("parts", [1, 2, 3])
 def test_row_partition_sessions_match_sparse_path(solver, parts, R):
-    """R = 32 runs the cooperative 8-rows-per-warp step kernels (config 5's shape), here
-    with row ranges that do not start at 0."""
+    """R = 32 is config 5's shape (PA: the cooperative 8-rows-per-warp step), here with row
+    ranges that do not start at 0."""
     import torch
 
     from paper_2501_19221_b200.rowpart import GpuSession, exchange_row_bytes, row_split

@@ -619,10 +619,9 @@ def test_dense_tile_order_does_not_change_results(group, monkeypatch):
     assert np.array_equal(r_sb.x, ref_sb.x) and np.array_equal(r_sb.m, ref_sb.m)
 
 
-def test_sparse_sbm_r32_cooperative_step_matches_oracle():
-    """R = 32 (config 5's replica count) runs the cooperative SBM step (8 rows per warp,
-    CSR entries shuffled across the warp): bit-exact with the oracle's fp32 loop on an
-    irregular graph with rows longer than the 64-entry cooperative window."""
+def test_sparse_sbm_r32_irregular_rows_match_oracle():
+    """R = 32 (config 5's replica count, one q vector per row): bit-exact with the oracle's
+    fp32 loop on an irregular graph with one row of 80+ neighbours."""
     rng = np.random.default_rng(21)
     n = 4000
     r_, c_ = random_regular_edges(n, 6, 3)
