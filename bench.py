@@ -623,8 +623,11 @@ def run_ours(args):
                 "j16x2": "k_dense_run_general", "jq16": "k_dense_run_general_sbm"}.get(
                     kind, "k_dense_run_sbm")
         tr, tsrc = measured_traffic(tkey, args.config)
+        nominal = {"mxf4": 9000.0, "f8f6f4": 4500.0, "i8": 4500.0, "f16": 2250.0}[mma_kind]
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "issued_frac": planes * achieved / peak,
+                "frac_of_nominal": achieved / nominal,  # B200_PROFILING.md dense figures
+                "nominal_peak": nominal,
                 "traffic": tr, "traffic_unit": "bytes/step", "traffic_source": tsrc,
                 "kernel": f"k_dense_run<{kind}>: tcgen05.mma.cta_group::2 kind::{mma_kind}, "
                           f"{what} + fused {'PA' if args.solver == 'pa' else 'SBM'} epilogue "
