@@ -26,6 +26,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=40)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--rmin", type=int, default=128)
+    ap.add_argument("--rmax", type=int, default=1300)
     args = ap.parse_args()
 
     import paper_2501_19221_b200 as vxq
@@ -36,7 +38,7 @@ def main():
     bad = 0
     for case in range(args.cases):
         n = int(rng.integers(256, 3200))
-        R = int(rng.integers(128, 1300))
+        R = int(rng.integers(args.rmin, args.rmax))
         T = int(rng.integers(2, 40))
         seed = int(rng.integers(0, 2 ** 31))
         density = float(rng.choice([1.0, 0.3, 0.05]))
@@ -44,7 +46,7 @@ def main():
         keep = rng.random(len(iu)) < density
         J = np.where(rng.random(keep.sum()) < 0.5, -1.0, 1.0) / np.sqrt(n)
         m = vxq.IsingModel.from_arrays(n, iu[keep], ju[keep], J, canonical=True)
-        reps = np.unique(np.r_[0, 1, R // 2, R - 2, R - 1, rng.integers(0, R, 3)])
+        reps = np.unique(np.r_[0, R // 2, R - 1, rng.integers(0, R, 3)])
         K = sign_matrix_f32(m)
         r = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=R, seed=seed), path="dense",
                        want_state=True)
