@@ -122,7 +122,9 @@ typedef struct {
                             argsort(kind="stable") of common.py:57)                  */
     double* energy_trace; /* [T] optional: min over replicas of E(s_t), the energy of
                              the spins entering step t (exact on the sparse paths and on
-                             the dense path with h = 0) -> time-to-target              */
+                             the dense uniform-|J| paths with h = 0 -- PA fused, SBM via
+                             a spin plane next to the digit planes; NaN on the general-J
+                             dense SBM) -> time-to-target                               */
     /* filled by the library */
     double lambda0_used; /* PA: lambda0;  SA: T_init  */
     double c0_used;      /* SBM: c0;      SA: T_final */

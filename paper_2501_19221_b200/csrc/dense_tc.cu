@@ -57,7 +57,7 @@ constexpr int QN = 8;  // tile-ticket ring depth (dynamic tile queue, see k_dens
 #endif
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
-enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3, kJQ16 = 4, kI8x3 = 5 };
+enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3, kJQ16 = 4, kI8x3 = 5, kI8x4 = 6 };
 
 template <Kind K>
 struct KindTraits;
@@ -110,6 +110,17 @@ struct KindTraits<Kind::kI8x3> {
     // D=S32 (2), A=B=signed int8 (1), K-major
     static constexpr uint32_t kIdescBase = (2u << 4) | (1u << 7) | (1u << 10);
 };
+
+// the same with a 4th plane holding the spins s_t = sign(q_t) (+-1 int8): its accumulator is
+// the exact K s_t, so the epilogue also reduces the exact coupling energy of s_t (per-step
+// energy trace, time-to-target); 4 x bn <= 256 TMEM columns per buffer
+template <>
+struct KindTraits<Kind::kI8x4> {
+    static constexpr int kPlanes = 4, kAPlanes = 1, kStages = 3, kBnMax = 64, kElemBytes = 1;
+    static constexpr int kKPerMma = 32;
+    static constexpr uint32_t kIdescBase = (2u << 4) | (1u << 7) | (1u << 10);
+};
+constexpr bool is_i8(Kind k) { return k == Kind::kI8x3 || k == Kind::kI8x4; }
 
 template <Kind K>
 constexpr int stage_bytes() {
@@ -332,7 +343,8 @@ __global__ void k_init_pa_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, in
 // q0, p0 (stream r: n q-draws then n p-draws, as k_init_sbm) + the bf16 q-splits
 __global__ void k_init_sbm_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, int64_t rbegin,
                               double amp, float* __restrict__ q, float* __restrict__ p,
-                              void* __restrict__ planes_raw, int nplanes, float qscale) {
+                              void* __restrict__ planes_raw, int nplanes, float qscale,
+                              int spin_plane) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nq = (2 * n + 3) / 4;
     if (idx >= nq * R) return;
@@ -353,6 +365,7 @@ __global__ void k_init_sbm_rm(int64_t n, int64_t R, int64_t ld, uint64_t seed, i
                 planes[r * ld + k] = a;
                 planes[plane + r * ld + k] = b;
                 planes[2 * plane + r * ld + k] = c;
+                if (spin_plane) planes[3 * plane + r * ld + k] = v >= 0.f ? 1 : -1;
             } else if (nplanes == 3) {
                 __nv_bfloat16* planes = reinterpret_cast<__nv_bfloat16*>(planes_raw);
                 __nv_bfloat16 a, b, c;
@@ -554,7 +567,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     static_assert(!PAIR || (KD != Kind::kBf16x3 && (CL == 1 || (CL == 2 && MX))),
                   "pair MMA: f8f6f4 / f16x2, no B multicast; super-pairs: mxf4 only");
     constexpr bool SP = PAIR && CL == 2;  // two pairs sharing the K panel
-    static_assert(KD != Kind::kI8x3 || PAIR, "int8 digit planes: CTA pairs only");
+    static_assert(!is_i8(KD) || PAIR, "int8 digit planes: CTA pairs only");
     static_assert((KD != Kind::kJ16x2 && KD != Kind::kJQ16) || PAIR,
                   "general-J planes: CTA pairs only");
     constexpr int A_BYTES = DA_BYTES * TR::kAPlanes;  // A planes of one stage, back to back
@@ -566,16 +579,15 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     // pair: each CTA stages its 128 A rows and <= 128 B rows per plane
     // kI8x3: each CTA stages <= kBnMax/2 = 40 replicas per digit plane, so a stage packs
     // into 31 KB and the ring holds VXQ_I8_STAGES of them (no x/m slots: SBM)
-    constexpr int SBYTES_I8 = ((A_BYTES + 3 * (KindTraits<Kind::kI8x3>::kBnMax / 2) * DROW +
-                                1023) / 1024) * 1024;
+    constexpr int SBYTES_I8 = ((A_BYTES + TR::kPlanes * (TR::kBnMax / 2) * DROW + 1023) / 1024) * 1024;
     constexpr int STAGES =
-        KD == Kind::kI8x3 ? VXQ_I8_STAGES
+        is_i8(KD) ? VXQ_I8_STAGES
         : (MX && PAIR && VXQ_MX_TIGHT) ? VXQ_MX_STAGES
         : PAIR ? ((TR::kPlanes == 1 && TR::kAPlanes == 1) ? VXQ_PAIR_STAGES
                                                           : (TR::kPlanes * TR::kAPlanes > 2 ? 3 : 4))
                : TR::kStages;
     constexpr int SBYTES_MX = ((A_BYTES + (kAccMx / 2) * DROW + 1023) / 1024) * 1024;
-    constexpr int SBYTES = KD == Kind::kI8x3 ? SBYTES_I8
+    constexpr int SBYTES = is_i8(KD) ? SBYTES_I8
                            : (MX && PAIR && VXQ_MX_TIGHT) ? SBYTES_MX
                            : PAIR ? A_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
@@ -848,7 +860,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 #pragma unroll
                         for (int k = 0; k < DROW / 32; ++k) {  // 32 B of K per MMA
                             const uint32_t accum = (kb | pl | k) != 0;
-                            if constexpr (KD == Kind::kI8x3) {  // one S32 accumulator per plane
+                            if constexpr (is_i8(KD)) {  // one S32 accumulator per plane
                                 ptx::mma2_i8(d + pl * (uint32_t)a.bn, da + 2 * k, db + 2 * k,
                                              idesc, (kb | k) != 0);
                                 continue;
@@ -1038,12 +1050,14 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const float st = __ldg(a.sched + t);
                 const float hi = row_ok ? __ldg(a.h + i) : 0.f;
                 auto process = [&](int c, const float* xo, const float* mo) {
-                    uint32_t v[16], v1[16], v2[16];
+                    uint32_t v[16], v1[16], v2[16], v3[16];
                     ptx::tmem_ld_32x32b_x16(tbase + c * 16, v);
-                    if constexpr (KD == Kind::kI8x3) {  // the digit planes' accumulators
+                    if constexpr (is_i8(KD)) {  // the digit planes' accumulators
                         ptx::tmem_ld_32x32b_x16(tbase + (uint32_t)a.bn + c * 16, v1);
                         ptx::tmem_ld_32x32b_x16(tbase + 2u * (uint32_t)a.bn + c * 16, v2);
                     }
+                    if constexpr (KD == Kind::kI8x4)  // K s_t (the spin plane)
+                        ptx::tmem_ld_32x32b_x16(tbase + 3u * (uint32_t)a.bn + c * 16, v3);
                     const int r0 = nb * a.bn + c * 16;
                     const int64_t base = (int64_t)r0 * a.ld + i;
                     ptx::tmem_ld_wait();
@@ -1052,7 +1066,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         const bool ok = row_ok && (r0 + jj) < a.R;
                         const int64_t off = base + (int64_t)jj * a.ld;
                         float f;
-                        if constexpr (KD == Kind::kI8x3) {
+                        if constexpr (is_i8(KD)) {
                             // K.Q exactly (|K.Q| < 2^37), rounded once to fp32, * 2^-S (exact)
                             const long long kq = (long long)(int)v[jj] +
                                                  256LL * (long long)(int)v1[jj] +
@@ -1097,6 +1111,18 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                         } else {
                             // SBM with B = -A = -c K, g = -h (field = -f)
                             const float qi = xo[jj];
+                            if constexpr (KD == Kind::kI8x4) {
+                                // exact coupling energy of s_t = sign(q_t): sum_i s_i (K s_t)_i
+                                if (a.qtrace) {
+                                    const int ks = (int)v3[jj];
+                                    const int term = ok ? (qi >= 0.f ? ks : -ks) : 0;
+                                    const int sum = __reduce_add_sync(0xffffffffu, term);
+                                    if (lane == 0 && (r0 + jj) < a.R)
+                                        atomicAdd(reinterpret_cast<unsigned long long*>(a.qtrace) +
+                                                      (int64_t)t * a.R + r0 + jj,
+                                                  (unsigned long long)(long long)sum);
+                                }
+                            }
                             const float inner = -O::sub(O::add(O::mul(qi, qi), a.a0), st);
                             const float force =
                                 O::add(O::mul(inner, qi), O::mul(a.c0, O::add(-f, hi)));
@@ -1109,13 +1135,15 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                             if (ok) {
                                 ptx::st_stream(xg + off, qn, stream);
                                 ptx::st_stream(mg + off, pn, stream);
-                                if constexpr (KD == Kind::kI8x3) {
+                                if constexpr (is_i8(KD)) {
                                     int8_t d0, d1, d2;
                                     digits3(qn, a.qscale, d0, d1, d2);
                                     int8_t* pl = reinterpret_cast<int8_t*>(nxt);
                                     pl[off] = d0;
                                     pl[a.plane_elems + off] = d1;
                                     pl[2 * a.plane_elems + off] = d2;
+                                    if constexpr (KD == Kind::kI8x4)  // s_{t+1}
+                                        pl[3 * a.plane_elems + off] = qn >= 0.f ? 1 : -1;
                                 } else if constexpr (KD == Kind::kF16x2 || KD == Kind::kJQ16) {
                                     __half q1, q2;
                                     split2(qn, q1, q2);
@@ -1268,6 +1296,11 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 
 constexpr int TB = 256;
 inline unsigned nblk(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, TB)); }
+
+__global__ void k_fill_nan(double* v, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = NAN;
+}
 
 __global__ void k_any_nonzero(int64_t n, const double* v, int* flag) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1587,7 +1620,7 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
     }
     g_dense_kind = jplanes ? VXQ_DENSE_KIND_J16X2
                    : jq ? VXQ_DENSE_KIND_JQ16
-                   : planes16 == 8 ? VXQ_DENSE_KIND_I8X3
+                   : planes16 == 8 || planes16 == 9 ? VXQ_DENSE_KIND_I8X3
                    : planes16 == 3 ? VXQ_DENSE_KIND_BF16X3
                    : planes16 == 2 ? VXQ_DENSE_KIND_F16X2
                    : mx ? VXQ_DENSE_KIND_MXF4 : VXQ_DENSE_KIND_F8F6F4;
@@ -1600,6 +1633,7 @@ static double run_loop(DenseRunArgs a, const CUtensorMap& tmA, const CUtensorMap
             launch_run<Kind::kJ16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true, tmX, tmM);
         else if (jq) launch_run<Kind::kJQ16, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 8) launch_run<Kind::kI8x3, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
+        else if (planes16 == 9) launch_run<Kind::kI8x4, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 3) launch_run<Kind::kBf16x3, 1>(tmA, tb0, tb1, a, a.T, s, true);
         else if (planes16 == 2 && pair)
             launch_run<Kind::kF16x2, 1, true>(tmA, tb0, tb1, a, a.T, s, true);
@@ -1880,7 +1914,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                     const std::vector<double>& a_sched, double dt, double a0, double c0,
                     double q_cap, double amp, uint64_t seed, int64_t rbegin, float* q_il,
                     float* p_il, uint32_t* sb, long long* q2, cudaStream_t s, double* loop_ms,
-                    int64_t* launches) {
+                    int64_t* launches, double* trace_out, bool trace_on_dev) {
     // general (non-uniform) J: J as two fp16 planes too (kJQ16, the caller checked the range)
     const bool general = !p->uniform_magnitude;
     // uniform |J|: exact integer field (kI8x3) when |q| <= max(q_cap, init_noise) <= 2^14;
@@ -1894,12 +1928,15 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     if (planes == 2 && !dense_sbm_fp16_ok(q_cap, amp)) planes = 3;  // fp16 max is 65504
     if (planes == 8 && ceil_div(p->n, DBM) < 2) planes = 2;  // pairs need two row tiles
     const bool exact = planes == 8;
+    // per-step energies (trace_out, h = 0): the exact kernel with a 4th plane holding the
+    // spins, whose accumulator is K s_t (kI8x4, bn <= 64); other kinds report NaN
+    const bool traced = exact && trace_out != nullptr && problem_h_zero(p, s);
     VXQ_REQUIRE(!general || planes == 2, "general dense J on the tensor cores needs fp16 q");
     DenseOperand* d = general ? dense_jplanes(p, s)
                               : dense_operand(p, s, exact ? 3 : (planes == 3 ? 1 : 2));
     const int64_t n = p->n, ld = d->ld, T = (int64_t)a_sched.size();
     const int64_t plane = R * ld;
-    const int nb_planes = exact ? 3 : planes;
+    const int nb_planes = exact ? (traced ? 4 : 3) : planes;
     const int esz = exact ? 1 : 2;
     DevBuf<float> q(R * ld, s), pm(R * ld, s);
     DevBuf<uint8_t> b0(nb_planes * plane * esz, s), b1(nb_planes * plane * esz, s);
@@ -1908,7 +1945,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     const float qscale = exact ? std::ldexp(1.0f, S) : 0.f;
     k_init_sbm_rm<<<nblk(((2 * n + 3) / 4) * R), TB, 0, s>>>(n, R, ld, seed, rbegin, amp,
                                                             q.get(), pm.get(), b0.get(), planes,
-                                                            qscale);
+                                                            qscale, traced ? 1 : 0);
     VXQ_CHECK_LAUNCH();
     // CTA pairs (M = 256; each CTA stages its 128 K rows and bn/2 replicas of every plane):
     // half the replica blocks -> half the K re-reads per step
@@ -1920,7 +1957,9 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     }
     int bn;
     if (pair) {
-        int64_t bmax = exact ? KindTraits<Kind::kI8x3>::kBnMax : 256;
+        int64_t bmax = exact ? (traced ? KindTraits<Kind::kI8x4>::kBnMax
+                                       : KindTraits<Kind::kI8x3>::kBnMax)
+                             : 256;
         if (const char* e = getenv("VXQ_DENSE_BN"))  // A/B: cap the replica tile width
             if (exact) bmax = std::max<int64_t>(16, std::min<int64_t>(bmax, atoi(e) / 16 * 16));
         const int64_t blocks = ceil_div(R, bmax);
@@ -1932,8 +1971,10 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     const int bbox = pair ? bn / 2 : bn;
     CUtensorMap tmB0, tmB1;
     if (exact) {
-        tmB0 = make_map(b0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 3, DROW, bbox, 3);
-        tmB1 = make_map(b1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, 3, DROW, bbox, 3);
+        tmB0 = make_map(b0.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, nb_planes, DROW, bbox,
+                        nb_planes);
+        tmB1 = make_map(b1.get(), CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ld, R, nb_planes, DROW, bbox,
+                        nb_planes);
     } else {
         const CUtensorMapDataType bt =
             planes == 3 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -1979,9 +2020,33 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
     a.done = done.get();
+    DevBuf<long long> qtr;
+    if (traced) {
+        qtr = DevBuf<long long>(std::max<int64_t>(T, 1) * R, s);
+        VXQ_CUDA(cudaMemsetAsync(qtr.get(), 0, std::max<int64_t>(T, 1) * R * sizeof(long long), s));
+        a.qtrace = qtr.get();
+    }
     *loop_ms = run_loop(a, general ? d->tmJ : (exact ? d->tmAi8 : (planes == 3 ? d->tmA16 : d->tmA16h)),
-                        tmB0, tmB1, planes, 1, s, pair, nullptr, nullptr, false, false, general);
+                        tmB0, tmB1, traced ? 9 : planes, 1, s, pair, nullptr, nullptr, false, false,
+                        general);
     *launches += 2;
+    if (trace_out) {  // min_r E(s_t) per step (NaN where no exact per-step energy exists)
+        DevBuf<double> tr(std::max<int64_t>(T, 1), s);
+        if (traced) {
+            DevBuf<int> hnz(1, s);
+            VXQ_CUDA(cudaMemsetAsync(hnz.get(), 0, sizeof(int), s));  // h = 0 (checked)
+            k_trace_from_q<<<(unsigned)std::max<int64_t>(T, 1), 256, 0, s>>>(
+                qtr.get(), T, R, p->magnitude, p->offset, hnz.get(), tr.get());
+        } else {
+            k_fill_nan<<<nblk(std::max<int64_t>(T, 1)), TB, 0, s>>>(tr.get(), T);
+        }
+        VXQ_CHECK_LAUNCH();
+        VXQ_CUDA(cudaMemcpyAsync(trace_out, tr.get(), T * sizeof(double),
+                                 trace_on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 s));
+        VXQ_CUDA(cudaStreamSynchronize(s));
+        *launches += 1;
+    }
     if (q2 && !general) energy_pass(d, q.get(), n, R, q2, s, launches);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(q.get(), n, R, ld, R_pad, V, q_il);
     k_rm_to_interleaved<<<nblk(n * R), TB, 0, s>>>(pm.get(), n, R, ld, R_pad, V, p_il);

@@ -1218,19 +1218,15 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
     const bool dense = sizeof(T) == 4 && !want_best &&
                        (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && elig));
     if (dense) {
-        if (want_trace) {  // no per-step energies on the dense SBM path (round 1): NaN
-            DevBuf<double> nan_tr(std::max<int64_t>(T_, 1), s);
-            k_fill<<<nblk(T_), TB, 0, s>>>(nan_tr.get(), T_, NAN);
-            VXQ_CUDA(cudaMemcpyAsync(out->energy_trace, nan_tr.get(), T_ * sizeof(double),
-                                     cudaMemcpyDefault, s));
-            VXQ_CUDA(cudaStreamSynchronize(s));
-        }
+        // per-step energies (want_trace): exact on the uniform-|J| exact-field kernel with
+        // h = 0 (a spin plane next to the digit planes), NaN on the other dense kinds
         DevBuf<long long> qq(R, s);
         if constexpr (sizeof(T) == 4) {
             dense_sbm_loop(p, R, L.R_pad, L.V, L.W, sched, prm->dt, prm->a0, c0, prm->q_cap,
                            prm->init_noise, prm->seed, rbegin, q.get(), pm.get(), sb.get(),
                            p->uniform_magnitude ? qq.get() : nullptr, s, &out->loop_ms,
-                           &launches);
+                           &launches, want_trace ? out->energy_trace : nullptr,
+                           opts && opts->outputs_on_device);
         }
         out->path_used = VXQ_PATH_DENSE;
         out->dense_kind = dense_last_kind();

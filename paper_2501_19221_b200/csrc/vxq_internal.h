@@ -234,7 +234,7 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
                     const std::vector<double>& a_sched, double dt, double a0, double c0,
                     double q_cap, double amp, uint64_t seed, int64_t rbegin, float* q_il,
                     float* p_il, uint32_t* sb, long long* q2, cudaStream_t s, double* loop_ms,
-                    int64_t* launches);
+                    int64_t* launches, double* trace_out = nullptr, bool trace_on_dev = false);
 
 // ---- host schedules (bit-exact with the reference's Python expressions)
 void pa_schedule(double lam0, int64_t T, double* out);   // lam0 * (1.0 - t / T)

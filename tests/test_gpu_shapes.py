@@ -148,7 +148,7 @@ def fixed_point_shift(q_cap=1.0, amp=1.0):
 
 
 def dense_sbm_exact_emulation_rows(m, K, reps, T, seed, c0, dt=0.05, a0=1.0, q_cap=1.0,
-                                   amp=1.0):
+                                   amp=1.0, schedule_T=None):
     """numpy emulation of the exact tensor-core SBM path (k_dense_run<kI8x3>): the field is
     the exact integer K.Q of the fixed-point Q = rint(q 2^S), rounded once to fp32 and
     scaled, f = fp32(c) * (fp32(K.Q) * 2^-S); then the reference's update order
@@ -162,7 +162,7 @@ def dense_sbm_exact_emulation_rows(m, K, reps, T, seed, c0, dt=0.05, a0=1.0, q_c
     f32 = np.float32
     inv = f32(2.0 ** -S)
     dta0 = f32(dt * a0)
-    for st in np.linspace(0.0, a0, T).astype(np.float32):
+    for st in np.linspace(0.0, a0, schedule_T or T).astype(np.float32)[:T]:
         Qfix = np.rint(Q.astype(np.float64) * 2.0 ** S)
         kq = Qfix @ Kd  # exact: integer partial sums < 2^53
         f = c * (kq.astype(np.float32) * inv)
@@ -214,6 +214,28 @@ def test_dense_sbm_exact_field_walls_and_scaling():
                                             q_cap=0.5, amp=3.0)
     assert np.array_equal(r.x[reps], Qe.astype(np.float64))
     assert np.array_equal(r.m[reps], Pe.astype(np.float64))
+
+
+def test_dense_sbm_exact_energy_trace():
+    """trace=True on the exact SBM kernel (a 4th B plane holds s_t = sign(q_t); its S32
+    accumulator is K s_t, reduced in the epilogue): trace[t] = min_r E(sign(q_t)) exactly,
+    for every t, against the emulation; the trajectory is the untraced run's, bit for bit."""
+    m = instances.sk(700)
+    R, T, c0 = 200, 20, 0.5
+    prm = vxq.SbmParams(steps=T, dt=0.05, replicas=R, seed=4, c0=c0)
+    r = vxq.run_sbm(m, prm, trace=True, want_state=True)
+    assert r.info["path"] == "dense" and r.info["dense_kind"] == "i8x3"
+    plain = vxq.run_sbm(m, prm, want_state=True)
+    assert np.array_equal(r.x, plain.x) and np.array_equal(r.energies, plain.energies)
+    K = sign_matrix_f32(m)
+    reps = np.arange(R)
+    want = []
+    for t in range(T):  # E(s_t) for the spins entering step t (t = 0: the initial q)
+        Qt, _ = (sbm_init_rows(4, reps, m.n) if t == 0 else
+                 dense_sbm_exact_emulation_rows(m, K, reps, t, 4, c0, schedule_T=T))
+        S = np.where(Qt >= 0, 1, -1).astype(np.int8)
+        want.append(uniform_energies(m, S, K).min())
+    assert np.array_equal(r.info["energy_trace"], np.array(want))
 
 
 @pytest.mark.parametrize("planes", ["2", "3"])
