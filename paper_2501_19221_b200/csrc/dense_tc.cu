@@ -196,6 +196,21 @@ EncodeFn get_encode() {
     return fn;
 }
 
+// L2 promotion of the TMA boxes (VXQ_TMA_PROMO: 0 none, 1 64 B, 2 128 B, 3 256 B; A/B)
+CUtensorMapL2promotion tma_promotion() {
+    static const CUtensorMapL2promotion v = [] {
+        int k = 3;
+        if (const char* e = getenv("VXQ_TMA_PROMO")) k = atoi(e);
+        switch (k) {
+            case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+            case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+            case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+            default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+        }
+    }();
+    return v;
+}
+
 // up to 3-D tensor [planes][outer][inner] (elements of `esize` bytes), SW128 boxes
 CUtensorMap make_map(const void* base, CUtensorMapDataType dt, int esize, uint64_t inner,
                      uint64_t outer, uint64_t planes, uint32_t box_inner, uint32_t box_outer,
@@ -209,7 +224,7 @@ CUtensorMap make_map(const void* base, CUtensorMapDataType dt, int esize, uint64
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = get_encode()(&m, dt, rank, const_cast<void*>(base), dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              tma_promotion(),
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(VXQ_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     return m;
@@ -228,7 +243,7 @@ CUtensorMap make_map_fp4(const void* base, uint64_t inner, uint64_t outer, uint3
     CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 2,
                               const_cast<void*>(base), dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              tma_promotion(),
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(VXQ_ERR_CUDA, "cuTensorMapEncodeTiled (fp4) failed");
     return m;
