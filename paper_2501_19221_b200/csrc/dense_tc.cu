@@ -196,10 +196,12 @@ EncodeFn get_encode() {
     return fn;
 }
 
-// L2 promotion of the TMA boxes (VXQ_TMA_PROMO: 0 none, 1 64 B, 2 128 B, 3 256 B; A/B)
+// L2 promotion of the TMA boxes (VXQ_TMA_PROMO: 0 none, 1 64 B, 2 128 B, 3 256 B).  The
+// boxes' rows are 128-byte segments of L2-resident operands: 128 B beats the round-1 256 B
+// by ~1 % on cfg2 PA and SBM (profiles/r02/ab_promo/)
 CUtensorMapL2promotion tma_promotion() {
     static const CUtensorMapL2promotion v = [] {
-        int k = 3;
+        int k = 2;
         if (const char* e = getenv("VXQ_TMA_PROMO")) k = atoi(e);
         switch (k) {
             case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
