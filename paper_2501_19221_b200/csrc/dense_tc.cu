@@ -502,6 +502,7 @@ struct DenseRunArgs {
     unsigned* decided;       // [T][n_tiles] tiles that made their step-(t-1) decisions
     unsigned* ticket;        // [1] next tile of the dynamic queue (zeroed per launch)
     float qscale, qscale_inv;  // kI8x3: 2^S and 2^-S of the fixed-point q
+    int a_prefetch;            // L2-prefetch the A panel ahead of the smem loads
 };
 
 // stats slots: 0 producer<-empty, 1 producer<-dependency, 2 mma<-full, 3 mma<-tempty,
@@ -747,16 +748,17 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 tile_of(g, t, nb, mb);
                 const CUtensorMap* tmB = (t & 1) ? &tmB1 : &tmB0;
                 // A (the coupling panel) never depends on the dynamics: keep kPrefetch
-                // k-blocks of it on their way into L2 ahead of the smem loads
+                // k-blocks of it on their way into L2 ahead of the smem loads (a.a_prefetch;
+                // an L2-resident K gains nothing from it and the prefetches cost L2 lookups)
                 constexpr int kPrefetch = 8;
-                for (int kb = 0; kb < kPrefetch && kb < a.kblocks; ++kb) {
+                for (int kb = 0; a.a_prefetch && kb < kPrefetch && kb < a.kblocks; ++kb) {
                     if constexpr (TR::kAPlanes > 1)
                         ptx::tma_prefetch_3d(&tmA, kb * (DROW / TR::kElemBytes), mb * DBM, 0);
                     else
                         ptx::tma_prefetch_2d(&tmA, kb * (DROW / TR::kElemBytes), mb * DBM);
                 }
                 for (int kb = 0; kb < a.kblocks; ++kb) {
-                    if (kb + kPrefetch < a.kblocks) {
+                    if (a.a_prefetch && kb + kPrefetch < a.kblocks) {
                         if constexpr (TR::kAPlanes > 1)
                             ptx::tma_prefetch_3d(&tmA, (kb + kPrefetch) * (DROW / TR::kElemBytes),
                                                  mb * DBM, 0);
@@ -1430,6 +1432,8 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
     DevBuf<unsigned> ticket(1, s);
     VXQ_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), s));
     a.ticket = ticket.get();
+    a.a_prefetch = 1;
+    if (const char* e = getenv("VXQ_DENSE_APF")) a.a_prefetch = atoi(e) != 0;
     a.timeout_ns = 10ull * 1000 * 1000 * 1000;
     if (const char* e = getenv("VXQ_WAIT_TIMEOUT_S"))
         a.timeout_ns = (uint64_t)std::max(1, atoi(e)) * 1000ull * 1000 * 1000;
