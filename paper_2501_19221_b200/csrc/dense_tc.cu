@@ -1435,8 +1435,9 @@ void launch_run(const CUtensorMap& tmA, const CUtensorMap& tmB0, const CUtensorM
     // no A-panel L2 prefetch by default: the operands are L2-resident, and the prefetches
     // were a quarter of the L2 tag-stage traffic that bounds the kernel (cfg2 PA 156 -> 173
     // Grv/s, tensor pipe 46 -> 56 %; SBM +4 %; profiles/r02/ab_aprefetch/)
-    // (general-J kinds keep it: their 400 MB J planes stream from DRAM)
-    a.a_prefetch = (KD == Kind::kJ16x2 || KD == Kind::kJQ16) ? 1 : 0;
+    // (the general-J kinds, whose 400 MB J planes stream from DRAM, gain without it too:
+    // PA 17.7 -> 19.6, SBM 12.0 -> 12.7 Grv/s at n = 10^4)
+    a.a_prefetch = 0;
     if (const char* e = getenv("VXQ_DENSE_APF")) a.a_prefetch = atoi(e) != 0;
     a.timeout_ns = 10ull * 1000 * 1000 * 1000;
     if (const char* e = getenv("VXQ_WAIT_TIMEOUT_S"))
