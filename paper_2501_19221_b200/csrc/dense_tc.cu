@@ -610,7 +610,9 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                            : PAIR ? A_BYTES + TR::kPlanes * 128 * DROW : stage_bytes<KD>();
     constexpr int XMS = (RING_BYTES - STAGES * SBYTES) / XM_SLOT_BYTES;  // x/m slots
     static_assert(STAGES * SBYTES <= RING_BYTES, "smem ring");
-    static_assert((KD != Kind::kFp8 && KD != Kind::kJ16x2) || XMS >= 2, "x/m staging slots");
+    // x/m staging needs two slots (one per epilogue half); a ring too deep to leave them
+    // runs the register x/m path (xm_on false)
+    const bool xm_on = XMS >= 2 && a.xm != 0;
     // x/m slots are split between the two epilogue halves (chunk c goes to half c & 1) so
     // each half waits on every phase of its own slots in order: with shared slots a half
     // could wait on a slot two phases ahead of the loader and pass the parity check on a
@@ -652,7 +654,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         // ticket consumers (all arrive on the leader's qempty): per CTA 8 epilogue warps
         // and the x/m loader (PA with staging), the MMA issuer(s) (pair: the leader's
         // only), and every non-leader producer
-        const uint32_t xmc = (a.xm && a.mode == 0) ? 1u : 0u;
+        const uint32_t xmc = (xm_on && a.mode == 0) ? 1u : 0u;
         const uint32_t qcons =
             NCTA * (8u + xmc) + (PAIR ? (uint32_t)CL : (uint32_t)NCTA) + (NCTA - 1u);
         for (int s = 0; s < QN; ++s) {
@@ -934,7 +936,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     mma_done:;
     } else if (warp == 10) {
         // ---------------- x/m loader (PA steps): chunk c of every tile this CTA owns
-        if (a.xm && a.mode == 0 && ptx::elect_one()) {
+        if (xm_on && a.mode == 0 && ptx::elect_one()) {
             const uint64_t pol = ptx::policy_evict_first();
             const int nch = a.bn / 16;
             int jh[2] = {0, 0};  // chunks loaded per epilogue half
@@ -1016,7 +1018,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     mo[jj] = ok ? ptx::ld_stream(mg + base + (int64_t)jj * a.ld, stream) : 0.f;
                 }
             };
-            const bool xm = a.xm && a.mode == 0;
+            const bool xm = xm_on && a.mode == 0;
             if (a.mode == 0 && !xm && half < nch) {
                 // x/m of step t are written by the step-(t-1) tiles of this replica block
                 // (possibly on other CTAs): acquire their counter before the early load
