@@ -1915,7 +1915,10 @@ void dense_pa_general_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t 
     a.m = m.get();
     a.b_buf[0] = reinterpret_cast<uint8_t*>(s0.get());
     a.b_buf[1] = reinterpret_cast<uint8_t*>(s1.get());
-    a.group = pick_group(a.n_tiles);
+    // pairs of replica blocks per row panel: the J-plane panel (not L2-resident: 400 MB at
+    // n = 10^4) is re-used once from L2 (n = 10^4: 19.2 -> 22.3 Grv/s; all 4 blocks 21.7;
+    // profiles/r02/ab_general_group/); VXQ_DENSE_GROUP overrides
+    a.group = getenv("VXQ_DENSE_GROUP") ? pick_group(a.n_tiles) : std::min(2, a.n_tiles);
     a.mode = 0;
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
@@ -2043,7 +2046,11 @@ void dense_sbm_loop(Problem* p, int64_t R, int64_t R_pad, int V, int64_t W,
     // re-used from L2 instead of re-read from DRAM per replica block: 1.48 GB -> less
     // DRAM per step, more of the 1 kW budget for the SMs; cfg2 SBM 324 -> 280 ms per solve,
     // profiles/r02/ab_sbm_group/); VXQ_DENSE_GROUP overrides
-    a.group = (exact && !getenv("VXQ_DENSE_GROUP")) ? a.n_tiles : pick_group(a.n_tiles);
+    // general J (two fp16 J planes, DRAM-streamed): pairs of replica blocks (12.6 -> 13.3)
+    a.group = getenv("VXQ_DENSE_GROUP") ? pick_group(a.n_tiles)
+              : exact                    ? a.n_tiles
+              : general                  ? std::min(2, a.n_tiles)
+                                         : 1;
     a.mode = 0;
     DevBuf<unsigned> done(std::max<int64_t>(T, 1) * a.n_tiles, s);
     VXQ_CUDA(cudaMemsetAsync(done.get(), 0, std::max<int64_t>(T, 1) * a.n_tiles * sizeof(unsigned), s));
