@@ -40,6 +40,27 @@ __device__ __forceinline__ int64_t lane_base(int64_t i, int64_t R_pad, int c, in
     return i * R_pad + (int64_t)c * 32 * V + (int64_t)lane * V;
 }
 
+// Random spin-word gather of the R <= 32 step (A/B knob VXQ_GATHER_LD: 0 = ld.global.nc,
+// 1 = ld.global.cg, 2 = ld.global.nc.L1::no_allocate, 3 = ld.global.nc.L2::64B)
+#ifndef VXQ_GATHER_LD
+#define VXQ_GATHER_LD 0
+#endif
+__device__ __forceinline__ uint32_t gather_word(const uint32_t* p) {
+#if VXQ_GATHER_LD == 1
+    return __ldcg(p);
+#elif VXQ_GATHER_LD == 2
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#elif VXQ_GATHER_LD == 3
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ int64_t pos_of(int64_t r, int V) {
     int64_t ch = 32 * V;
     int64_t c = r / ch, rem = r % ch;
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(256, MULTI ? 4 : VXQ_COOP_MINB) k_pa_step_coop
     const int j0 = v0 ? __ldcs(op.indices + k0) : 0, j1 = v1 ? __ldcs(op.indices + k1) : 0;
     const T a0 = v0 ? O::mul(op.sign, __ldcs(op.data + k0)) : (T)0;
     const T a1 = v1 ? O::mul(op.sign, __ldcs(op.data + k1)) : (T)0;
-    const uint32_t w0 = v0 ? __ldg(sb_in + j0) : 0u, w1 = v1 ? __ldg(sb_in + j1) : 0u;
+    const uint32_t w0 = v0 ? gather_word(sb_in + j0) : 0u, w1 = v1 ? gather_word(sb_in + j1) : 0u;
 #pragma unroll
     for (int u = 0; u < RPW; ++u) {
         if (u >= nr) break;
