@@ -40,10 +40,11 @@ __device__ __forceinline__ int64_t lane_base(int64_t i, int64_t R_pad, int c, in
     return i * R_pad + (int64_t)c * 32 * V + (int64_t)lane * V;
 }
 
-// Random spin-word gather of the R <= 32 step (A/B knob VXQ_GATHER_LD: 0 = ld.global.nc,
+// Random spin-word gather of the R <= 32 step: 64-byte L2 fetch hint, cfg5 PA +4.8 %
+// (profiles/r02/ab_gather_ld; A/B knob VXQ_GATHER_LD: 0 = ld.global.nc,
 // 1 = ld.global.cg, 2 = ld.global.nc.L1::no_allocate, 3 = ld.global.nc.L2::64B)
 #ifndef VXQ_GATHER_LD
-#define VXQ_GATHER_LD 0
+#define VXQ_GATHER_LD 3
 #endif
 __device__ __forceinline__ uint32_t gather_word(const uint32_t* p) {
 #if VXQ_GATHER_LD == 1
@@ -59,6 +60,46 @@ __device__ __forceinline__ uint32_t gather_word(const uint32_t* p) {
 #else
     return __ldg(p);
 #endif
+}
+
+// f[b] += t[b] for b < N.  With VXQ_PACKED=1 fp32 pairs go through the packed f32x2 add
+// (FADD2, sm_100): each half rounds like __fadd_rn, so the sums are bit-identical with half
+// the add issue slots -- measured +1.2 % on cfg3 PA, -0.6 % on cfg4 PA (HBM-bound), so the
+// scalar adds stay the default (profiles/r02/ab_packed)
+#ifndef VXQ_PACKED
+#define VXQ_PACKED 0
+#endif
+template <typename T, int N>
+__device__ __forceinline__ void addv(T* f, const T* t) {
+    if constexpr (VXQ_PACKED && sizeof(T) == 4 && N % 2 == 0) {
+#pragma unroll
+        for (int b = 0; b < N; b += 2) {
+            asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+                "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+                "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+                : "=f"(f[b]), "=f"(f[b + 1])
+                : "f"(f[b]), "f"(f[b + 1]), "f"(t[b]), "f"(t[b + 1]));
+        }
+    } else {
+#pragma unroll
+        for (int b = 0; b < N; ++b) f[b] = Ops<T>::add(f[b], t[b]);
+    }
+}
+// t[b] = a * q[b]: scalar FMULs on purpose -- ptxas (12.9) contracts mul.rn.f32x2 followed by
+// add.rn.f32x2 into FFMA2 (one rounding instead of two) even with --fmad=false, which breaks
+// parity; scalar products feeding the packed add stay unfused
+template <typename T, int N>
+__device__ __forceinline__ void mulv(T* t, T a, const T* q) {
+#pragma unroll
+    for (int b = 0; b < N; ++b) t[b] = Ops<T>::mul(a, q[b]);
+}
+// f[b] += (bit `lane` of w[b]) ? a : -a
+template <typename T, int N>
+__device__ __forceinline__ void add_pm(T* f, const uint32_t* w, T a, int lane) {
+    T t[N];
+#pragma unroll
+    for (int b = 0; b < N; ++b) t[b] = ((w[b] >> lane) & 1u) ? a : -a;
+    addv<T, N>(f, t);
 }
 
 __device__ __forceinline__ int64_t pos_of(int64_t r, int V) {
@@ -251,11 +292,7 @@ __global__ void __launch_bounds__(256, MULTI ? 4 : VXQ_PA_MINB) k_pa_step(int64_
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int g = 0; g < CPW; ++g)
-#pragma unroll
-                for (int b = 0; b < V; ++b)
-                    f[g * V + b] = O::add(f[g * V + b],
-                                          ((w[u][g].v[b] >> lane) & 1u) ? a[u] : -a[u]);
+            for (int g = 0; g < CPW; ++g) add_pm<T, V>(f + g * V, w[u][g].v, a[u], lane);
     }
     for (; k < k1; ++k) {
         const int j = __ldg(op.indices + k);
@@ -264,9 +301,7 @@ __global__ void __launch_bounds__(256, MULTI ? 4 : VXQ_PA_MINB) k_pa_step(int64_
         for (int g = 0; g < CPW; ++g) {
             Vec<uint32_t, V> w =
                 *reinterpret_cast<const Vec<uint32_t, V>*>(sbc + (int64_t)j * W + g * V);
-#pragma unroll
-            for (int b = 0; b < V; ++b)
-                f[g * V + b] = O::add(f[g * V + b], ((w.v[b] >> lane) & 1u) ? a : -a);
+            add_pm<T, V>(f + g * V, w.v, a, lane);
         }
     }
 
@@ -388,6 +423,166 @@ __global__ void __launch_bounds__(256, MULTI ? 4 : VXQ_COOP_MINB) k_pa_step_coop
     }
 }
 
+// ------------------------------------------------------------------ PA cluster (medium n)
+// A thread-block cluster of C CTAs owns one replica chunk (32 V replicas) for a run of
+// steps.  Every CTA of the cluster holds the chunk's spin words of ALL n rows in shared
+// memory (double-buffered, n V words each), so a neighbour gather is a shared-memory
+// broadcast instead of an L2 round trip; CTA k updates rows [k n / C, (k+1) n / C) (x/m
+// stream from HBM as in k_pa_step), stores each new row's V words into all C tables
+// (DSMEM), and one cluster barrier separates the steps.  The CSR entries of the next row and
+// its x/m are loaded while the current row sums.  Per (row, replica): the same operations in
+// the same CSR order as k_pa_step -- bit-identical.
+#ifndef VXQ_PA_CLUSTER_THREADS
+#define VXQ_PA_CLUSTER_THREADS 1024
+#endif
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+template <int V>
+__device__ __forceinline__ void cl_store(uint32_t addr, const uint32_t (&w)[V]) {
+    if constexpr (V == 4)
+        asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]),
+                     "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
+    else if constexpr (V == 2)
+        asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(w[0]),
+                     "r"(w[1]) : "memory");
+    else
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(w[0]) : "memory");
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(VXQ_PA_CLUSTER_THREADS, 1) k_pa_cluster(
+    int64_t n, int64_t R_pad, int C, Operator<T> op, const T* __restrict__ h,
+    const T* __restrict__ lam_sched, int64_t t0, int64_t nsteps, T eta, T alpha,
+    T* __restrict__ x, T* __restrict__ m, const uint32_t* __restrict__ sb_in,
+    uint32_t* __restrict__ sb_out) {
+    using O = Ops<T>;
+    extern __shared__ __align__(16) uint32_t tab[];  // [2][n][V], then this CTA's indptr
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int rank = (int)cl_rank();
+    const int64_t c = blockIdx.x / C, W = R_pad / 32, nV = n * V;
+    const int64_t rb = rank * n / C, re = (rank + 1) * n / C;
+    int64_t* ptr_s = reinterpret_cast<int64_t*>(tab + 2 * nV);  // indptr[rb .. re]
+    for (int64_t e = threadIdx.x; e < nV; e += blockDim.x)
+        tab[e] = __ldg(sb_in + (e / V) * W + c * V + (e % V));
+    for (int64_t r = rb + threadIdx.x; r <= re; r += blockDim.x) ptr_s[r - rb] = __ldg(op.indptr + r);
+    const uint32_t peer = lane < C ? cl_map(tab, (uint32_t)lane) : 0u;  // lane q -> CTA q
+    cl_sync();  // every CTA of the cluster is running and holds table 0
+    for (int64_t s = 0; s < nsteps; ++s) {
+        const T lam = lam_sched[t0 + s];
+        const uint32_t* cur = tab + (s & 1) * nV;
+        const int64_t nxt = ((s + 1) & 1) * nV;
+        const bool last = s == nsteps - 1;
+        int64_t i = rb + warp;
+        // current row: CSR bounds, first 32 entries (lane-parallel), x/m
+        int64_t kb = 0, ke = 0;
+        int jl = 0;
+        T al = (T)0;
+        Vec<T, V> xv, mv;
+        if (i < re) {
+            kb = ptr_s[i - rb];
+            ke = ptr_s[i - rb + 1];
+            if (kb + lane < ke) {
+                jl = __ldg(op.indices + kb + lane);
+                al = O::mul(op.sign, __ldg(op.data + kb + lane));
+            }
+            xv = ld_cs<T, V>(x + lane_base(i, R_pad, (int)c, lane, V));
+            mv = ld_cs<T, V>(m + lane_base(i, R_pad, (int)c, lane, V));
+        }
+        for (; i < re; i += nw) {
+            // next row's loads in flight while this row sums
+            const int64_t in = i + nw;
+            int64_t kbn = 0, ken = 0;
+            int jn = 0;
+            T an = (T)0;
+            Vec<T, V> xn_, mn_;
+            if (in < re) {
+                kbn = ptr_s[in - rb];
+                ken = ptr_s[in - rb + 1];
+                if (kbn + lane < ken) {
+                    jn = __ldg(op.indices + kbn + lane);
+                    an = O::mul(op.sign, __ldg(op.data + kbn + lane));
+                }
+                xn_ = ld_cs<T, V>(x + lane_base(in, R_pad, (int)c, lane, V));
+                mn_ = ld_cs<T, V>(m + lane_base(in, R_pad, (int)c, lane, V));
+            }
+            T f[V];
+#pragma unroll
+            for (int b = 0; b < V; ++b) f[b] = (T)0;
+            const int d0 = ke - kb < 32 ? (int)(ke - kb) : 32;
+            int k = 0;
+            for (; k + 4 <= d0; k += 4) {
+                int j[4];
+                T a[4];
+                Vec<uint32_t, V> w[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    j[u] = __shfl_sync(0xffffffffu, jl, k + u);
+                    a[u] = __shfl_sync(0xffffffffu, al, k + u);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    w[u] = *reinterpret_cast<const Vec<uint32_t, V>*>(cur + (int64_t)j[u] * V);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) add_pm<T, V>(f, w[u].v, a[u], lane);
+            }
+            for (; k < d0; ++k) {
+                const int j = __shfl_sync(0xffffffffu, jl, k);
+                const T a = __shfl_sync(0xffffffffu, al, k);
+                const Vec<uint32_t, V> w = *reinterpret_cast<const Vec<uint32_t, V>*>(cur + (int64_t)j * V);
+                add_pm<T, V>(f, w.v, a, lane);
+            }
+            for (int64_t kk = kb + 32; kk < ke; ++kk) {  // rows longer than 32 entries
+                const int j = __ldg(op.indices + kk);
+                const T a = O::mul(op.sign, __ldg(op.data + kk));
+                const Vec<uint32_t, V> w = *reinterpret_cast<const Vec<uint32_t, V>*>(cur + (int64_t)j * V);
+                add_pm<T, V>(f, w.v, a, lane);
+            }
+            const T hi = __ldg(h + i);
+            uint32_t words[V];
+#pragma unroll
+            for (int b = 0; b < V; ++b) {
+                const T xo = xv.v[b];
+                const T grad = O::add(O::add(O::mul(lam, xo), f[b]), hi);
+                const T mn = O::sub(O::mul(alpha, mv.v[b]), O::mul(eta, grad));
+                T xn = O::add(xo, mn);
+                xn = xn < (T)-1 ? (T)-1 : (xn > (T)1 ? (T)1 : xn);
+                xv.v[b] = xn;
+                mv.v[b] = mn;
+                words[b] = __ballot_sync(0xffffffffu, xn >= (T)0);
+            }
+            st_cs<T, V>(x + lane_base(i, R_pad, (int)c, lane, V), xv);
+            st_cs<T, V>(m + lane_base(i, R_pad, (int)c, lane, V), mv);
+            if (lane < C) cl_store<V>(peer + (uint32_t)((nxt + i * V) * 4), words);
+            if (last && lane < V) {
+                uint32_t wv = words[0];
+#pragma unroll
+                for (int b = 1; b < V; ++b)
+                    if (lane == b) wv = words[b];
+                sb_out[i * W + c * V + lane] = wv;
+            }
+            kb = kbn;
+            ke = ken;
+            jl = jn;
+            al = an;
+            xv = xn_;
+            mv = mn_;
+        }
+        cl_sync();  // the step's words are in every table; table s & 1 is free again
+    }
+}
+
 // ------------------------------------------------------------------ SBM step (sparse)
 template <typename T>
 struct SbmScalars {
@@ -430,9 +625,11 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         for (int u = 0; u < 4; ++u)
             qv[u] = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j[u] * R_pad + off);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a[u], qv[u].v[b]));
+        for (int u = 0; u < 4; ++u) {
+            T t[V];
+            mulv<T, V>(t, a[u], qv[u].v);
+            addv<T, V>(f, t);
+        }
     }
 #if VXQ_SBM_PTAIL
     // the 1-3 remaining entries: one round of index loads, one of gathers (predicated)
@@ -452,9 +649,11 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
             if (u < rem) qv[u] = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j[u] * R_pad + off);
 #pragma unroll
         for (int u = 0; u < 3; ++u)
-            if (u < rem)
-#pragma unroll
-                for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a[u], qv[u].v[b]));
+            if (u < rem) {
+                T t[V];
+                mulv<T, V>(t, a[u], qv[u].v);
+                addv<T, V>(f, t);
+            }
     }
 #else
     for (; k < k1; ++k) {
@@ -813,6 +1012,107 @@ void launch_pa_step(const Layout& L, const Operator<T>& op, const T* h, T lam, T
     launch_pa_step<T>(L, op, h, lam, eta, alpha, x, m, sbi, one_dest(sbo), s);
 }
 
+// ---- PA cluster path (k_pa_cluster): plan + launch
+constexpr size_t kPaClusterSmemMax = 200 * 1024;
+
+int sm_count() {
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return nsm;
+}
+
+struct PaClusterPlan {
+    int C = 0;
+    int64_t chunks = 0;
+    size_t smem = 0;
+};
+
+template <typename T, int V>
+cudaLaunchConfig_t pa_cluster_config(const PaClusterPlan& pl, cudaLaunchAttribute* at,
+                                     cudaStream_t s) {
+    auto kern = k_pa_cluster<T, V>;
+    VXQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)pl.smem));
+    if (pl.C > 8)
+        VXQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(pl.chunks * pl.C));
+    cfg.blockDim = dim3(VXQ_PA_CLUSTER_THREADS);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = s;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pl.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+template <typename T, int V>
+bool pa_cluster_fits(const PaClusterPlan& pl, cudaStream_t s) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = pa_cluster_config<T, V>(pl, at, s);
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k_pa_cluster<T, V>, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return nc >= 1;
+}
+
+// The cluster kernel serves full-row solves whose chunk spin table (2 n V words) fits
+// shared memory.  Opt-in (VXQ_PA_CLUSTER: 0 = never (default), 1 = when chunks x C clusters
+// cover 2/3 of the SMs, 2 = whenever it fits; VXQ_PA_CLUSTER_C overrides C): on cfg 3 it
+// measured 111 us/step against the step kernel's 99 (profiles/r02/ab_pa_cluster) -- the
+// step is instruction-issue bound (~3 instructions per +-a term), not gather-latency bound,
+// and the cluster runs on 128 of the 148 SMs.
+template <typename T>
+bool pa_cluster_plan(const Layout& L, PaClusterPlan* pl, cudaStream_t s) {
+    const char* e = getenv("VXQ_PA_CLUSTER");
+    const int mode = e ? atoi(e) : 0;
+    if (mode == 0 || L.row0 != 0 || L.nrows != L.n) return false;
+    pl->chunks = L.R_pad / (32 * L.V);
+    const int nsm = sm_count();
+    int C = (int)std::max<int64_t>(1, std::min<int64_t>(8, nsm / pl->chunks));
+    if (const char* ce = getenv("VXQ_PA_CLUSTER_C")) C = std::max(1, atoi(ce));
+    pl->C = (int)std::min<int64_t>(C, L.n);
+    // two spin tables + the largest CTA's indptr slice (ceil(n / C) + 1 int64)
+    pl->smem = (size_t)2 * L.n * L.V * sizeof(uint32_t) +
+               (size_t)(ceil_div(L.n, pl->C) + 2) * sizeof(int64_t);
+    if (pl->smem > kPaClusterSmemMax) return false;
+    if (mode == 1 && pl->chunks * pl->C < (2 * nsm) / 3) return false;
+    switch (L.V) {
+        case 1: return pa_cluster_fits<T, 1>(*pl, s);
+        case 2: return pa_cluster_fits<T, 2>(*pl, s);
+        default:
+            if constexpr (sizeof(T) == 4) return pa_cluster_fits<T, 4>(*pl, s);
+            return false;
+    }
+}
+
+template <typename T>
+void launch_pa_cluster(const PaClusterPlan& pl, const Layout& L, const Operator<T>& op,
+                       const T* h, const T* lam_sched, int64_t t0, int64_t nsteps, T eta,
+                       T alpha, T* x, T* m, const uint32_t* sbi, uint32_t* sbo, cudaStream_t s) {
+    cudaLaunchAttribute at[1];
+#define VXQ_PA_CL(VV)                                                                        \
+    {                                                                                        \
+        cudaLaunchConfig_t cfg = pa_cluster_config<T, VV>(pl, at, s);                        \
+        VXQ_CUDA(cudaLaunchKernelEx(&cfg, k_pa_cluster<T, VV>, L.n, L.R_pad, pl.C, op, h,    \
+                                    lam_sched, t0, nsteps, eta, alpha, x, m, sbi, sbo));     \
+    }
+    switch (L.V) {
+        case 1: VXQ_PA_CL(1); break;
+        case 2: VXQ_PA_CL(2); break;
+        default:
+            if constexpr (sizeof(T) == 4) VXQ_PA_CL(4);
+            break;
+    }
+#undef VXQ_PA_CL
+}
+
 template <typename T, bool MULTI>
 void launch_sbm_step_t(const Layout& L, const Operator<T>& op, const T* g, SbmScalars<T> sc,
                        const T* qi, const Dests<T>& qo, T* p, cudaStream_t s) {
@@ -1117,13 +1417,33 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     } else {
         launch_pack<T>(L, x.get(), sbA.get(), s);  // s_0 = sign(x_0)
         ++launches;
-        tm.start();
         uint32_t* bufs[2] = {sbA.get(), sbB.get()};
-        for (int64_t t = 0; t < T_; ++t) {
-            trk.observe(p, bufs[t & 1], t, T_, s);  // E(s_t): exact, bit-packed spins
-            launch_pa_step<T>(L, op, h, (T)sched[t], eta, alpha, x.get(), m.get(), bufs[t & 1],
-                              bufs[(t + 1) & 1], s);
+        PaClusterPlan pl;
+        const bool cl = T_ > 0 && pa_cluster_plan<T>(L, &pl, s);
+        DevBuf<T> ds;
+        if (cl) {  // lambda_t on the device for the multi-step launch
+            ds = DevBuf<T>(T_, s);
+            std::vector<T> st(T_);
+            for (int64_t t = 0; t < T_; ++t) st[t] = (T)sched[t];
+            VXQ_CUDA(cudaMemcpyAsync(ds.get(), st.data(), T_ * sizeof(T), cudaMemcpyHostToDevice, s));
+            VXQ_CUDA(cudaStreamSynchronize(s));
+        }
+        tm.start();
+        if (cl && !trk.trace && !trk.best) {  // all T steps in one launch
+            launch_pa_cluster<T>(pl, L, op, h, ds.get(), 0, T_, eta, alpha, x.get(), m.get(),
+                                 bufs[0], bufs[T_ & 1], s);
             ++launches;
+        } else {
+            for (int64_t t = 0; t < T_; ++t) {
+                trk.observe(p, bufs[t & 1], t, T_, s);  // E(s_t): exact, bit-packed spins
+                if (cl)
+                    launch_pa_cluster<T>(pl, L, op, h, ds.get(), t, 1, eta, alpha, x.get(),
+                                         m.get(), bufs[t & 1], bufs[(t + 1) & 1], s);
+                else
+                    launch_pa_step<T>(L, op, h, (T)sched[t], eta, alpha, x.get(), m.get(),
+                                      bufs[t & 1], bufs[(t + 1) & 1], s);
+                ++launches;
+            }
         }
         VXQ_CHECK_LAUNCH();
         tm.stop();
