@@ -57,6 +57,10 @@ constexpr int QN = 8;  // tile-ticket ring depth (dynamic tile queue, see k_dens
 #endif
 constexpr uint8_t FP8_P1 = 0x38, FP8_M1 = 0xB8;  // E4M3 +1 / -1
 
+#ifndef VXQ_I8_MERGED
+#define VXQ_I8_MERGED 1
+#endif
+
 enum class Kind : int { kFp8 = 0, kBf16x3 = 1, kF16x2 = 2, kJ16x2 = 3, kJQ16 = 4, kI8x3 = 5, kI8x4 = 6 };
 
 template <Kind K>
@@ -847,9 +851,14 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         {
         // mxf4 (block-scaled descriptor): E2M1 = 1 for A and B, UE8M0 scales (bit 23),
         // K = 64 per MMA, scale-factor ids 0; no accumulator-format field
+        // int8 digit planes (VXQ_I8_MERGED): one MMA of N = planes x bn covers all planes --
+        // their B rows sit back to back in each CTA's stage, so K (A) is read from shared
+        // memory once per k-block instead of once per plane
+        const uint32_t n_mma = (is_i8(KD) && VXQ_I8_MERGED) ? (uint32_t)(TR::kPlanes * a.bn)
+                                                             : (uint32_t)a.bn;
         const uint32_t idesc =
             (MX ? ((1u << 7) | (1u << 10) | (1u << 23)) : (TR::kIdescBase | a.idesc_extra)) |
-            ((uint32_t)(a.bn >> 3) << 17) | ((uint32_t)((PAIR ? 2 * DBM : DBM) >> 4) << 24);
+            ((n_mma >> 3) << 17) | ((uint32_t)((PAIR ? 2 * DBM : DBM) >> 4) << 24);
         int stage = 0;
         uint32_t ph = 0;
         int lt = 0;
@@ -875,7 +884,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                     const uint32_t sa = ptx::smem_u32(smem + stage * SBYTES);
                     const uint64_t da = ptx::sw128_kmajor_desc(sa);
 #pragma unroll
-                    for (int pl = 0; pl < TR::kPlanes; ++pl) {
+                    for (int pl = 0; pl < ((is_i8(KD) && VXQ_I8_MERGED) ? 1 : TR::kPlanes); ++pl) {
                         const uint64_t db =
                             ptx::sw128_kmajor_desc(sa + A_BYTES + pl * b_plane_bytes);
 #pragma unroll
@@ -1072,13 +1081,31 @@ __global__ void __launch_bounds__(DTHREADS, 1)
                 const float hi = row_ok ? __ldg(a.h + i) : 0.f;
                 auto process = [&](int c, const float* xo, const float* mo) {
                     uint32_t v[16], v1[16], v2[16], v3[16];
-                    ptx::tmem_ld_32x32b_x16(tbase + c * 16, v);
-                    if constexpr (is_i8(KD)) {  // the digit planes' accumulators
-                        ptx::tmem_ld_32x32b_x16(tbase + (uint32_t)a.bn + c * 16, v1);
-                        ptx::tmem_ld_32x32b_x16(tbase + 2u * (uint32_t)a.bn + c * 16, v2);
+                    if constexpr (is_i8(KD) && VXQ_I8_MERGED) {
+                        // merged MMA: replica j of the block, plane pl sits in column
+                        // h P bn/2 + pl bn/2 + (j - h bn/2), h = (j >= bn/2); 8-column pieces
+                        // never straddle the halves (bn is a multiple of 16)
+                        const uint32_t hb = (uint32_t)a.bn / 2;
+#pragma unroll
+                        for (int piece = 0; piece < 2; ++piece) {
+                            const uint32_t j = (uint32_t)(c * 16 + piece * 8);
+                            const uint32_t h = j >= hb ? 1u : 0u;
+                            const uint32_t col = h * (uint32_t)TR::kPlanes * hb + (j - h * hb);
+                            ptx::tmem_ld_32x32b_x8(tbase + col, v + piece * 8);
+                            ptx::tmem_ld_32x32b_x8(tbase + col + hb, v1 + piece * 8);
+                            ptx::tmem_ld_32x32b_x8(tbase + col + 2 * hb, v2 + piece * 8);
+                            if constexpr (KD == Kind::kI8x4)
+                                ptx::tmem_ld_32x32b_x8(tbase + col + 3 * hb, v3 + piece * 8);
+                        }
+                    } else {
+                        ptx::tmem_ld_32x32b_x16(tbase + c * 16, v);
+                        if constexpr (is_i8(KD)) {  // the digit planes' accumulators
+                            ptx::tmem_ld_32x32b_x16(tbase + (uint32_t)a.bn + c * 16, v1);
+                            ptx::tmem_ld_32x32b_x16(tbase + 2u * (uint32_t)a.bn + c * 16, v2);
+                        }
+                        if constexpr (KD == Kind::kI8x4)  // K s_t (the spin plane)
+                            ptx::tmem_ld_32x32b_x16(tbase + 3u * (uint32_t)a.bn + c * 16, v3);
                     }
-                    if constexpr (KD == Kind::kI8x4)  // K s_t (the spin plane)
-                        ptx::tmem_ld_32x32b_x16(tbase + 3u * (uint32_t)a.bn + c * 16, v3);
                     const int r0 = nb * a.bn + c * 16;
                     const int64_t base = (int64_t)r0 * a.ld + i;
                     ptx::tmem_ld_wait();
