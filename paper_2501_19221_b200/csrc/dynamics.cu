@@ -102,6 +102,45 @@ __device__ __forceinline__ void add_pm(T* f, const uint32_t* w, T a, int lane) {
     addv<T, N>(f, t);
 }
 
+// SBM q table accesses with L2 eviction hints (A/B knob VXQ_SBM_L2HINT): the neighbour
+// gathers of q_t keep their lines (evict_last) while the freshly written q_{t+1} streams
+// (evict_first); 0 = plain accesses
+#ifndef VXQ_SBM_L2HINT
+#define VXQ_SBM_L2HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+template <typename T, int V>
+__device__ __forceinline__ Vec<T, V> ld_hint(const T* p, uint64_t pol) {
+    if constexpr (VXQ_SBM_L2HINT && sizeof(T) == 4 && V == 4) {
+        Vec<T, V> v;
+        asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=f"(v.v[0]), "=f"(v.v[1]), "=f"(v.v[2]), "=f"(v.v[3])
+                     : "l"(p), "l"(pol));
+        return v;
+    } else {
+        return *reinterpret_cast<const Vec<T, V>*>(p);
+    }
+}
+template <typename T, int V>
+__device__ __forceinline__ void st_hint(T* p, const Vec<T, V>& v, uint64_t pol) {
+    if constexpr (VXQ_SBM_L2HINT && sizeof(T) == 4 && V == 4) {
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                     "f"(v.v[0]), "f"(v.v[1]), "f"(v.v[2]), "f"(v.v[3]), "l"(pol)
+                     : "memory");
+    } else {
+        *reinterpret_cast<Vec<T, V>*>(p) = v;
+    }
+}
+
 __device__ __forceinline__ int64_t pos_of(int64_t r, int V) {
     int64_t ch = 32 * V;
     int64_t c = r / ch, rem = r % ch;
@@ -610,6 +649,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
     T f[V];
 #pragma unroll
     for (int b = 0; b < V; ++b) f[b] = (T)0;
+    const uint64_t pol_keep = VXQ_SBM_L2HINT ? l2_policy_last() : 0;
     const int64_t k0 = __ldg(op.indptr + i), k1 = __ldg(op.indptr + i + 1);
     int64_t k = k0;
     for (; k + 4 <= k1; k += 4) {
@@ -623,7 +663,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            qv[u] = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j[u] * R_pad + off);
+            qv[u] = ld_hint<T, V>(q_in + (int64_t)j[u] * R_pad + off, pol_keep);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             T t[V];
@@ -646,7 +686,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
             }
 #pragma unroll
         for (int u = 0; u < 3; ++u)
-            if (u < rem) qv[u] = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j[u] * R_pad + off);
+            if (u < rem) qv[u] = ld_hint<T, V>(q_in + (int64_t)j[u] * R_pad + off, pol_keep);
 #pragma unroll
         for (int u = 0; u < 3; ++u)
             if (u < rem) {
@@ -659,7 +699,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
     for (; k < k1; ++k) {
         int j = __ldg(op.indices + k);
         T a = O::mul(op.sign, __ldg(op.data + k));
-        Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(q_in + (int64_t)j * R_pad + off);
+        Vec<T, V> qv = ld_hint<T, V>(q_in + (int64_t)j * R_pad + off, pol_keep);
 #pragma unroll
         for (int b = 0; b < V; ++b) f[b] = O::add(f[b], O::mul(a, qv.v[b]));
     }
@@ -686,7 +726,7 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
         for (int d = 0; d < kMaxDests; ++d)
             if (d < q_out.n) *reinterpret_cast<Vec<T, V>*>(q_out.p[d] + base) = qv;
     } else {
-        *reinterpret_cast<Vec<T, V>*>(q_one + base) = qv;
+        st_hint<T, V>(q_one + base, qv, VXQ_SBM_L2HINT ? l2_policy_first() : 0);
     }
     st_cs<T, V>(p + pbase, pv);
 }
