@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(VXQ_PA_CLUSTER_THREADS, 1) k_pa_cluster(
             int64_t kbn = 0, ken = 0;
             int jn = 0;
             T an = (T)0;
-            Vec<T, V> xn_, mn_;
+            Vec<T, V> xn_ = xv, mn_ = mv;  // (unused past the last row)
             if (in < re) {
                 kbn = ptr_s[in - rb];
                 ken = ptr_s[in - rb + 1];
