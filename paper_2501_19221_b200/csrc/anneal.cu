@@ -37,6 +37,9 @@ constexpr int kSaSmemMax = 200 * 1024;
 #endif
 constexpr int kPf = VXQ_SA_PF;  // field / spin-word prefetch depth (spins ahead)
 constexpr int kB = 8;   // neighbour updates per batch
+#ifndef VXQ_SA_BATCH
+#define VXQ_SA_BATCH 1
+#endif
 
 __global__ void k_sa_init_spins(int64_t n, int64_t W, int64_t R_pad, uint64_t seed,
                                 int64_t rbegin, uint32_t* __restrict__ sb) {
@@ -221,12 +224,35 @@ __global__ void __launch_bounds__(32) k_sa_run(SaArgs a) {
                 };
                 int64_t e = e0;
                 if constexpr (!SMEM) {  // fire-and-forget reductions at L2
+#if VXQ_SA_BATCH
+                    // all index / value loads of a batch before its reductions (the asm
+                    // memory clobber of a reduction would otherwise order every later load
+                    // behind it: one L2 round trip per neighbour)
+                    for (; e < e1; e += kB) {
+                        int j[kB];
+                        T v[kB];
+#pragma unroll
+                        for (int u = 0; u < kB; ++u) {
+                            const bool ok = e + u < e1;
+                            j[u] = ok ? __ldg(indices + e + u) : -1;
+                            v[u] = ok ? O::mul(d2, __ldg(data + e + u)) : (T)0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < kB; ++u) {
+                            if (j[u] >= 0) {
+                                red_add_global(Fb + (int64_t)j[u] * fs, v[u]);
+                                patch(j[u], v[u]);
+                            }
+                        }
+                    }
+#else
                     for (; e < e1; ++e) {
                         const int j = indices[e];
                         const T v = O::mul(d2, data[e]);
                         red_add_global(Fb + (int64_t)j * fs, v);
                         patch(j, v);
                     }
+#endif
                 }
                 for (; e + kB <= e1; e += kB) {
                     int j[kB];
