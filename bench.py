@@ -638,11 +638,13 @@ def run_ours(args):
     else:
         B = bytes_per_update(args.solver, dbar, R)
         achieved = B * R * n / (mean_step_kernel_ms / 1e3) / 1e9
-        kname = f"k_{args.solver}_step"
-        if info.get("path") == "resident":
-            kname = f"k_{args.solver}_resident"
-        elif args.solver == "pa" and R <= 32 and info.get("path") in ("sparse", "rowpart"):
-            kname = "k_pa_step_coop"  # one sign word per row: cooperative warp-CSR variant
+        kname = info.get("kernel")  # the dynamics kernel the library reports (ABI 5)
+        if not kname:
+            kname = f"k_{args.solver}_step"
+            if info.get("path") == "resident":
+                kname = f"k_{args.solver}_resident"
+            elif args.solver == "pa" and R <= 32 and info.get("path") in ("sparse", "rowpart"):
+                kname = "k_pa_step_coop"  # one sign word per row: cooperative warp-CSR variant
         tr, tsrc = measured_traffic(kname, args.config)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": tr, "traffic_unit": "bytes/step",

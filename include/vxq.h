@@ -46,7 +46,7 @@ extern "C" {
 #define VXQ_API
 #endif
 
-#define VXQ_ABI_VERSION 4  /* 4: eig_info, dense_eligible, outputs.dense_kind, session snapshots */
+#define VXQ_ABI_VERSION 5  /* 5: outputs.step_kernel; 4: eig_info, dense_eligible, outputs.dense_kind, session snapshots */
 
 #define VXQ_OK 0
 #define VXQ_ERR_INVALID 1     /* -> ValidationError */
@@ -132,7 +132,21 @@ typedef struct {
     int64_t launches;    /* kernels launched by this call                    */
     int32_t path_used;   /* VXQ_PATH_* actually run                          */
     int32_t dense_kind;  /* VXQ_DENSE_KIND_*: operand scheme of the tensor-core path */
+    int32_t step_kernel; /* VXQ_KERNEL_*: the dynamics kernel that ran (ABI 5)       */
+    int32_t reserved;
 } vxq_outputs;
+
+/* dynamics kernels (vxq_outputs.step_kernel) */
+#define VXQ_KERNEL_NONE 0
+#define VXQ_KERNEL_PA_STEP 1       /* CSR step over bit-packed spins, one launch per step  */
+#define VXQ_KERNEL_PA_STEP_COOP 2  /* the same for R <= 32 (8 rows per warp)               */
+#define VXQ_KERNEL_PA_CLUSTER 3    /* thread-block clusters, spin tables in shared memory   */
+#define VXQ_KERNEL_PA_RESIDENT 4   /* small n: state + CSR in shared memory, one launch     */
+#define VXQ_KERNEL_SBM_STEP 5      /* CSR step over fp32/fp64 q, one launch per step        */
+#define VXQ_KERNEL_SBM_BLOCK 6     /* row blocks: distinct neighbours' q staged in smem     */
+#define VXQ_KERNEL_SBM_RESIDENT 7
+#define VXQ_KERNEL_DENSE_RUN 8     /* tcgen05 persistent dense kernel (see dense_kind)      */
+#define VXQ_KERNEL_SA_RUN 9
 
 /* tensor-core operand schemes (vxq_outputs.dense_kind) */
 #define VXQ_DENSE_KIND_NONE 0

@@ -24,6 +24,9 @@ VXQ_OK, VXQ_ERR_INVALID, VXQ_ERR_OOM, VXQ_ERR_CUDA, VXQ_ERR_UNSUPPORTED = 0, 1, 
 FP32, FP64 = 0, 1
 PATHS = {"auto": 0, "resident": 1, "sparse": 2, "dense": 3}
 PATH_NAMES = {v: k for k, v in PATHS.items()}
+STEP_KERNELS = {0: None, 1: "k_pa_step", 2: "k_pa_step_coop", 3: "k_pa_cluster",
+                4: "k_pa_resident", 5: "k_sbm_step", 6: "k_sbm_block", 7: "k_sbm_resident",
+                8: "k_dense_run", 9: "k_sa_run"}
 DENSE_KINDS = {0: None, 1: "mxf4", 2: "f8f6f4", 3: "i8x3", 4: "f16x2", 5: "bf16x3", 6: "j16x2",
                7: "jq16"}
 
@@ -67,7 +70,8 @@ class RunOptsC(ctypes.Structure):
 class OutputsC(ctypes.Structure):
     _fields_ = [("states", P), ("energies", P), ("x", P), ("m", P), ("order", P),
                 ("energy_trace", P), ("lambda0_used", f64), ("c0_used", f64), ("loop_ms", f64),
-                ("launches", i64), ("path_used", i32), ("dense_kind", i32)]
+                ("launches", i64), ("path_used", i32), ("dense_kind", i32),
+                ("step_kernel", i32), ("reserved", i32)]
 
 
 _lib = None

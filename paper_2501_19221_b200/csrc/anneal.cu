@@ -392,6 +392,7 @@ void sa_solve_t(Problem* p, const vxq_sa_params* prm, const vxq_run_opts* opts,
     ++launches;
     out->loop_ms = tm.ms();
     out->path_used = resident ? VXQ_PATH_RESIDENT : VXQ_PATH_SPARSE;
+    out->step_kernel = VXQ_KERNEL_SA_RUN;
     finish_from_bits(p, R, W, best_sb.get(), opts, out, s);
     out->launches = launches + 4;
 }

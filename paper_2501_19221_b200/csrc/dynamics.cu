@@ -21,6 +21,8 @@
 //   one 16-byte vector access and the V sign words of the chunk come out of V ballots.
 //   sign bits sb[i][W], W = R_pad / 32: bit (r % 32) of word r / 32 (natural order).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -731,6 +733,144 @@ __global__ void __launch_bounds__(256) k_sbm_step(int64_t row0, int64_t nrows, i
     st_cs<T, V>(p + pbase, pv);
 }
 
+// ------------------------------------------------------------------ SBM step, row blocks
+// Structured sparse graphs (Pegasus / Chimera numbering) give consecutive rows common
+// neighbours: 64 rows of P16 touch ~302 distinct rows through ~920 entries.  One CTA owns
+// (row block b of kSbmBlockRows rows, replica chunk c of 32 V replicas): it stages the q_t
+// chunk rows of the block's distinct neighbours (slot lists built once per problem) and the
+// block's CSR entries in shared memory, then each warp sums its rows from there -- a
+// neighbour row crosses L2 -> SM once per block instead of once per entry.  Per (row,
+// replica) the same operations in the same CSR order as k_sbm_step: bit-identical.
+constexpr int kSbmBlockRows = 64;
+constexpr int kSbmBlockThreads = 512;
+constexpr int kSbmBlockMaxEnt = 4096;  // CSR entries of one block staged in shared memory
+#ifndef VXQ_SBM_BLOCK_V
+#define VXQ_SBM_BLOCK_V 2
+#endif
+constexpr int kSbmBlockV = VXQ_SBM_BLOCK_V;  // replicas per lane of the block path's layout
+template <int BYTES>  // 4, 8 or 16
+__device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(gsrc), "n"(BYTES)
+                     : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(kSbmBlockThreads) k_sbm_block(
+    int64_t n, int64_t R_pad, const int32_t* __restrict__ u_ptr,
+    const int32_t* __restrict__ u_idx, const uint16_t* __restrict__ slot, Operator<T> op,
+    const T* __restrict__ g, SbmScalars<T> sc, const T* __restrict__ q_in,
+    T* __restrict__ q_out, T* __restrict__ p, int ent_cap) {
+    using O = Ops<T>;
+    constexpr int NW = kSbmBlockThreads / 32;
+    constexpr int RPW = kSbmBlockRows / NW;  // rows per warp
+    extern __shared__ __align__(16) unsigned char sbm_blk_smem[];
+    __shared__ int32_t s_ptr[kSbmBlockRows + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b = blockIdx.x;
+    const int64_t off = (int64_t)blockIdx.y * 32 * V + (int64_t)lane * V;
+    const int64_t r0 = (int64_t)b * kSbmBlockRows;
+    const int nr = n - r0 < kSbmBlockRows ? (int)(n - r0) : kSbmBlockRows;
+    // this warp's rows: own q, p, g first (their latency overlaps the staging)
+    Vec<T, V> qo[RPW], po[RPW];
+    T go[RPW];
+#pragma unroll
+    for (int k = 0; k < RPW; ++k) {
+        const int rl = warp + k * NW;
+        if (rl < nr) {
+            const int64_t base = (r0 + rl) * R_pad + off;
+            qo[k] = *reinterpret_cast<const Vec<T, V>*>(q_in + base);
+            po[k] = ld_cs<T, V>(p + base);
+            go[k] = __ldg(g + r0 + rl);
+        }
+    }
+    const int u0 = __ldg(u_ptr + b), nu = __ldg(u_ptr + b + 1) - u0;
+    const int64_t e0 = __ldg(op.indptr + r0);
+    const int ne = (int)(__ldg(op.indptr + r0 + nr) - e0);
+    T* qs = reinterpret_cast<T*>(sbm_blk_smem);                                   // [nu][32 V]
+    T* s_val = qs + (size_t)nu * 32 * V;                                          // [ne]
+    uint16_t* s_slot = reinterpret_cast<uint16_t*>(s_val + ent_cap);              // [ne]
+    // stage the neighbours' chunk rows (16 B per lane per row)
+    for (int s0 = warp * 32; s0 < nu; s0 += NW * 32) {
+        const int jl = s0 + lane < nu ? __ldg(u_idx + u0 + s0 + lane) : 0;
+        const int cnt = min(32, nu - s0);
+        for (int t = 0; t < cnt; ++t) {
+            const int j = __shfl_sync(0xffffffffu, jl, t);
+            const T* src = q_in + (int64_t)j * R_pad + off;
+            T* dst = qs + (size_t)(s0 + t) * 32 * V + (size_t)lane * V;
+            constexpr int VB = (int)(V * sizeof(T));  // bytes per lane: 4, 8, 16 (fp32) / 8, 16 (fp64)
+            if constexpr (VB <= 16) {
+                cp_async_n<VB>(dst, src);
+            } else {
+#pragma unroll
+                for (int h = 0; h < VB / 16; ++h)
+                    cp_async_n<16>(dst + h * 16 / sizeof(T), src + h * 16 / sizeof(T));
+            }
+        }
+    }
+    // the block's CSR entries (slot, sign * value) and row offsets
+    for (int e = threadIdx.x; e < ne; e += kSbmBlockThreads) {
+        s_val[e] = O::mul(op.sign, __ldg(op.data + e0 + e));
+        s_slot[e] = __ldg(slot + e0 + e);
+    }
+    for (int r = threadIdx.x; r <= nr; r += kSbmBlockThreads)
+        s_ptr[r] = (int32_t)(__ldg(op.indptr + r0 + r) - e0);
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < RPW; ++k) {
+        const int rl = warp + k * NW;
+        if (rl >= nr) break;
+        const int kb = s_ptr[rl], ke = s_ptr[rl + 1];
+        T f[V];
+#pragma unroll
+        for (int bb = 0; bb < V; ++bb) f[bb] = (T)0;
+        int kk = kb;
+        for (; kk + 4 <= ke; kk += 4) {
+            Vec<T, V> qv[4];
+            T a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a[u] = s_val[kk + u];
+                qv[u] = *reinterpret_cast<const Vec<T, V>*>(qs + (size_t)s_slot[kk + u] * 32 * V + (size_t)lane * V);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int bb = 0; bb < V; ++bb) f[bb] = O::add(f[bb], O::mul(a[u], qv[u].v[bb]));
+        }
+        for (; kk < ke; ++kk) {
+            const T a = s_val[kk];
+            const Vec<T, V> qv = *reinterpret_cast<const Vec<T, V>*>(qs + (size_t)s_slot[kk] * 32 * V + (size_t)lane * V);
+#pragma unroll
+            for (int bb = 0; bb < V; ++bb) f[bb] = O::add(f[bb], O::mul(a, qv.v[bb]));
+        }
+        const int64_t base = (r0 + rl) * R_pad + off;
+#pragma unroll
+        for (int bb = 0; bb < V; ++bb) {
+            const T qi = qo[k].v[bb];
+            const T inner = -O::sub(O::add(O::mul(qi, qi), sc.a0), sc.a_t);
+            const T force = O::add(O::mul(inner, qi), O::mul(sc.c0, O::add(f[bb], go[k])));
+            T pn = O::add(po[k].v[bb], O::mul(sc.dt, force));
+            T qn = O::add(qi, O::mul(sc.dta0, pn));
+            if (fabs(qn) > sc.q_cap) {
+                qn = qn < -sc.q_cap ? -sc.q_cap : sc.q_cap;
+                pn = (T)0;
+            }
+            qo[k].v[bb] = qn;
+            po[k].v[bb] = pn;
+        }
+        *reinterpret_cast<Vec<T, V>*>(q_out + base) = qo[k];
+        st_cs<T, V>(p + base, po[k]);
+    }
+}
+
 // ------------------------------------------------------------------ resident (small n)
 // One CTA owns RG replicas for all T steps: their state and the whole CSR (row pointers,
 // indices, values) live in shared memory, so the only per-step synchronisation is one
@@ -1280,6 +1420,150 @@ struct Tracker {
     }
 };
 
+// ---- blocked sparse SBM (k_sbm_block): per-problem neighbour slots, plan, launch
+// VXQ_SBM_BLOCK: 0 = never (default), 1 = when sampled blocks show >= 2 entries per staged
+// row, 2 = whenever the slots fit shared memory.  Opt-in: on cfg 3 the blocked step cuts
+// L2 -> SM gather bytes 3x but measured 174 us against the step kernel's 142
+// (profiles/r02/ab_sbm_block): its staging and summing phases do not overlap at 2 CTAs/SM.
+int sbm_block_mode() {
+    const char* e = getenv("VXQ_SBM_BLOCK");
+    return e ? atoi(e) : 0;
+}
+
+}  // namespace
+
+struct NbrBlocks {
+    int nb = 0, max_u = 0, max_e = 0;
+    int64_t total_u = 0;
+    double reuse = 0.0;                // entries per staged neighbour row
+    int32_t* u_ptr = nullptr;          // [nb + 1]
+    int32_t* u_idx = nullptr;          // [total_u] distinct neighbours of each block, ascending
+    uint16_t* slot = nullptr;          // [nnz] CSR entry -> slot in its block's list
+};
+
+void nbr_blocks_destroy(NbrBlocks* b) {
+    if (!b) return;
+    if (b->u_ptr) cudaFree(b->u_ptr);
+    if (b->u_idx) cudaFree(b->u_idx);
+    if (b->slot) cudaFree(b->slot);
+    delete b;
+}
+
+namespace {
+
+constexpr size_t kSbmBlockSmemMax = (kSbmBlockV >= 4 ? 200 : 110) * 1024;  // 2 CTAs/SM when V <= 2
+constexpr double kSbmBlockMinReuse = 2.0;
+
+// Distinct-neighbour lists of every kSbmBlockRows-row block (host, once per problem; the
+// CSR is tiny for the graphs this serves).  Cheap rejection first: a sample of blocks must
+// show reuse >= kSbmBlockMinReuse and fit shared memory.
+NbrBlocks* nbr_blocks_get(Problem* p, int mode, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(p->mu);
+    if (p->nbr_blocks_state != 0) return p->nbr_blocks_state > 0 ? p->nbr_blocks : nullptr;
+    const int64_t n = p->n, nnz = p->nnz;
+    const int64_t nb = ceil_div(n, kSbmBlockRows);
+    if (n < 2 * kSbmBlockRows || nnz == 0 || nnz > ((int64_t)1 << 26) || nb > ((int64_t)1 << 30)) {
+        p->nbr_blocks_state = -1;
+        return nullptr;
+    }
+    std::vector<int64_t> ip(n + 1);
+    VXQ_CUDA(cudaMemcpyAsync(ip.data(), p->indptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> ix(nnz);
+    VXQ_CUDA(cudaMemcpyAsync(ix.data(), p->indices, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    VXQ_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> tmp;
+    auto uniq = [&](int64_t b) {
+        const int64_t r0 = b * kSbmBlockRows, r1 = std::min(n, r0 + kSbmBlockRows);
+        tmp.assign(ix.begin() + ip[r0], ix.begin() + ip[r1]);
+        std::sort(tmp.begin(), tmp.end());
+        tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+        return (int64_t)tmp.size();
+    };
+    const size_t row_bytes = 32 * kSbmBlockV * sizeof(float);  // one fp32 chunk row
+    const size_t ent_b = sizeof(float) + sizeof(uint16_t);  // per staged CSR entry
+    if (mode == 1) {  // sample 16 blocks spread over the rows
+        int64_t ent = 0, un = 0;
+        for (int k = 0; k < 16; ++k) {
+            const int64_t b = (nb - 1) * k / 15;
+            const int64_t r0 = b * kSbmBlockRows, r1 = std::min(n, r0 + kSbmBlockRows);
+            ent += ip[r1] - ip[r0];
+            const int64_t u = uniq(b);
+            un += u;
+            if ((size_t)u * row_bytes + (size_t)(ip[r1] - ip[r0] + 8) * ent_b > kSbmBlockSmemMax ||
+                ip[r1] - ip[r0] > kSbmBlockMaxEnt) {
+                p->nbr_blocks_state = -1;
+                return nullptr;
+            }
+        }
+        if (un == 0 || (double)ent / (double)un < kSbmBlockMinReuse) {
+            p->nbr_blocks_state = -1;
+            return nullptr;
+        }
+    }
+    NbrBlocks* B = new NbrBlocks;
+    B->nb = (int)nb;
+    std::vector<int32_t> uptr(nb + 1, 0), uidx;
+    std::vector<uint16_t> sl(nnz);
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t u = uniq(b);
+        const int64_t r0b = b * kSbmBlockRows, r1b = std::min(n, r0b + kSbmBlockRows);
+        if ((size_t)u * row_bytes + (size_t)(ip[r1b] - ip[r0b] + 8) * ent_b > kSbmBlockSmemMax ||
+            u > 65535 || ip[r1b] - ip[r0b] > kSbmBlockMaxEnt) {
+            delete B;
+            p->nbr_blocks_state = -1;
+            return nullptr;
+        }
+        B->max_u = std::max<int>(B->max_u, (int)u);
+        B->max_e = std::max<int>(B->max_e, (int)(ip[r1b] - ip[r0b]));
+        const int64_t r0 = b * kSbmBlockRows, r1 = std::min(n, r0 + kSbmBlockRows);
+        for (int64_t e = ip[r0]; e < ip[r1]; ++e)
+            sl[e] = (uint16_t)(std::lower_bound(tmp.begin(), tmp.end(), ix[e]) - tmp.begin());
+        uidx.insert(uidx.end(), tmp.begin(), tmp.end());
+        uptr[b + 1] = (int32_t)uidx.size();
+    }
+    B->total_u = (int64_t)uidx.size();
+    B->reuse = (double)nnz / (double)std::max<int64_t>(1, B->total_u);
+    if (mode == 1 && B->reuse < kSbmBlockMinReuse) {
+        delete B;
+        p->nbr_blocks_state = -1;
+        return nullptr;
+    }
+    VXQ_CUDA(cudaMalloc(&B->u_ptr, (nb + 1) * sizeof(int32_t)));
+    VXQ_CUDA(cudaMalloc(&B->u_idx, std::max<int64_t>(1, B->total_u) * sizeof(int32_t)));
+    VXQ_CUDA(cudaMalloc(&B->slot, nnz * sizeof(uint16_t)));
+    VXQ_CUDA(cudaMemcpyAsync(B->u_ptr, uptr.data(), (nb + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    VXQ_CUDA(cudaMemcpyAsync(B->u_idx, uidx.data(), B->total_u * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    VXQ_CUDA(cudaMemcpyAsync(B->slot, sl.data(), nnz * sizeof(uint16_t), cudaMemcpyHostToDevice, s));
+    VXQ_CUDA(cudaStreamSynchronize(s));
+    p->nbr_blocks = B;
+    p->nbr_blocks_state = 1;
+    return B;
+}
+
+template <typename T>
+void launch_sbm_block(const NbrBlocks& B, const Layout& L, const Operator<T>& op, const T* g,
+                      SbmScalars<T> sc, const T* qi, T* qo, T* p, cudaStream_t s) {
+    const int ent_cap = (B.max_e + 7) / 8 * 8;
+    const size_t smem = (size_t)B.max_u * 32 * L.V * sizeof(T) +
+                        (size_t)ent_cap * (sizeof(T) + sizeof(uint16_t));
+    dim3 grid((unsigned)B.nb, (unsigned)(L.R_pad / (32 * L.V)));
+#define VXQ_SBM_BLK(VV)                                                                      \
+    {                                                                                        \
+        VXQ_CUDA(cudaFuncSetAttribute(k_sbm_block<T, VV>,                                    \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        k_sbm_block<T, VV><<<grid, kSbmBlockThreads, smem, s>>>(L.n, L.R_pad, B.u_ptr, B.u_idx, \
+                                                               B.slot, op, g, sc, qi, qo, p, ent_cap); \
+    }
+    switch (L.V) {
+        case 1: VXQ_SBM_BLK(1); break;
+        case 2: VXQ_SBM_BLK(2); break;
+        default:
+            if constexpr (sizeof(T) == 4) VXQ_SBM_BLK(4);
+            break;
+    }
+#undef VXQ_SBM_BLK
+}
+
 // Common tail: sign bits -> exact energies -> states / order / analog exports.
 template <typename T>
 void finish_outputs(Problem* p, const Layout& L, const uint32_t* sb, const T* xa, const T* ma,
@@ -1418,6 +1702,7 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     if (!dense && !dense_gen) trk.init(p, L, T_, want_trace, want_best, s);
     EventTimer tm(s);
     const uint32_t* sb_final = nullptr;
+    bool used_cluster = false;
     DevBuf<long long> q2;
     DevBuf<uint32_t> sb_best;
     if (dense) {
@@ -1460,6 +1745,7 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
         uint32_t* bufs[2] = {sbA.get(), sbB.get()};
         PaClusterPlan pl;
         const bool cl = T_ > 0 && pa_cluster_plan<T>(L, &pl, s);
+        used_cluster = cl;
         DevBuf<T> ds;
         if (cl) {  // lambda_t on the device for the multi-step launch
             ds = DevBuf<T>(T_, s);
@@ -1495,6 +1781,11 @@ void pa_solve_t(Problem* p, const vxq_pa_params* prm, const vxq_run_opts* opts, 
     }
     out->path_used = (dense || dense_gen) ? VXQ_PATH_DENSE : path;
     out->dense_kind = (dense || dense_gen) ? dense_last_kind() : VXQ_DENSE_KIND_NONE;
+    out->step_kernel = (dense || dense_gen)          ? VXQ_KERNEL_DENSE_RUN
+                       : path == VXQ_PATH_RESIDENT   ? VXQ_KERNEL_PA_RESIDENT
+                       : used_cluster                ? VXQ_KERNEL_PA_CLUSTER
+                       : L.R_pad == 32               ? VXQ_KERNEL_PA_STEP_COOP
+                                                     : VXQ_KERNEL_PA_STEP;
     // q2 (coupling energy counts of the final spins) only describes sb_final without tracking
     finish_outputs<T>(p, L, sb_final, x.get(), m.get(), opts, out, s,
                       dense && !want_best ? q2.get() : nullptr);
@@ -1506,7 +1797,8 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
                   const std::vector<double>& a_sched, double dt, double a0, double c0,
                   double q_cap, int requested_path, int64_t nnz, T* q, T* qalt, T* pm,
                   vxq_outputs* out, int64_t& launches, cudaStream_t s, T** q_final,
-                  Tracker* trk = nullptr, uint32_t* sb_scratch = nullptr) {
+                  Tracker* trk = nullptr, uint32_t* sb_scratch = nullptr,
+                  const NbrBlocks* nbrb = nullptr) {
     const int64_t n = L.n, T_ = (int64_t)a_sched.size();
     SbmScalars<T> sc;
     sc.a_t = 0;
@@ -1517,7 +1809,7 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
     sc.q_cap = (T)q_cap;
     int RG = resident_rg(L);
     size_t smem = resident_smem_sbm(L, RG, sizeof(T), nnz);
-    int path = choose_path(requested_path, L, smem, nnz);
+    int path = nbrb ? VXQ_PATH_SPARSE : choose_path(requested_path, L, smem, nnz);
     const bool tracking = trk && (trk->trace || trk->best);
     if (tracking && path == VXQ_PATH_RESIDENT) {
         if (requested_path == VXQ_PATH_RESIDENT)
@@ -1551,7 +1843,8 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
                 trk->observe(p, sb_scratch, t, T_, s);
             }
             sc.a_t = (T)a_sched[t];
-            launch_sbm_step<T>(L, op, g, sc, qs[t & 1], qs[(t + 1) & 1], pm, s);
+            if (nbrb) launch_sbm_block<T>(*nbrb, L, op, g, sc, qs[t & 1], qs[(t + 1) & 1], pm, s);
+            else launch_sbm_step<T>(L, op, g, sc, qs[t & 1], qs[(t + 1) & 1], pm, s);
             ++launches;
         }
         VXQ_CHECK_LAUNCH();
@@ -1562,6 +1855,9 @@ void sbm_run_core(Problem* p, const Layout& L, const Operator<T>& op, const T* g
     if (out) {
         out->path_used = path;
         out->dense_kind = VXQ_DENSE_KIND_NONE;
+        out->step_kernel = path == VXQ_PATH_RESIDENT ? VXQ_KERNEL_SBM_RESIDENT
+                           : nbrb                    ? VXQ_KERNEL_SBM_BLOCK
+                                                     : VXQ_KERNEL_SBM_STEP;
     }
 }
 
@@ -1569,19 +1865,6 @@ template <typename T>
 void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts,
                  vxq_outputs* out, cudaStream_t s) {
     const int64_t n = p->n, R = prm->replicas, T_ = prm->steps;
-    Layout L = make_layout(n, R, sizeof(T) == 8);
-    double c0 = std::isnan(prm->c0) ? problem_c0(p, s) : prm->c0;
-    out->c0_used = c0;
-    std::vector<double> sched(T_);
-    sbm_schedule(prm->a0, T_, sched.data());
-    const int64_t rbegin = opts ? opts->replica_begin : 0;
-    DevBuf<T> q(n * L.R_pad, s), q2(n * L.R_pad, s), pm(n * L.R_pad, s);
-    DevBuf<uint32_t> sb(n * L.W, s);
-    int64_t launches = 0;
-    k_init_sbm<T><<<nblk(((2 * n + 3) / 4) * L.R_pad), TB, 0, s>>>(
-        n, 0, n, L.R_pad, L.V, prm->seed, rbegin, prm->init_noise, q.get(), pm.get());
-    VXQ_CHECK_LAUNCH();
-    ++launches;
     const int req = opts ? opts->path : 0;
     if constexpr (sizeof(T) == 8) {
         if (req == VXQ_PATH_DENSE)
@@ -1598,6 +1881,36 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
                                                                               prm->init_noise);
     const bool dense = sizeof(T) == 4 && !want_best &&
                        (req == VXQ_PATH_DENSE || (req == VXQ_PATH_AUTO && elig));
+    Layout L = make_layout(n, R, sizeof(T) == 8);
+    // blocked sparse step (structured graphs, fp32)
+    const NbrBlocks* nbrb = nullptr;
+    if constexpr (sizeof(T) == 4) {
+        const int bmode = sbm_block_mode();
+        if (!dense && bmode != 0 && (req == VXQ_PATH_AUTO || req == VXQ_PATH_SPARSE)) {
+            const int RG = resident_rg(L);
+            const size_t rsm = resident_smem_sbm(L, RG, sizeof(T), p->nnz);
+            if (choose_path(req, L, rsm, p->nnz) == VXQ_PATH_SPARSE) {
+                nbrb = nbr_blocks_get(p, bmode, s);
+                if (nbrb && L.V > kSbmBlockV) {  // narrower chunks: staged rows fit 2 CTAs/SM
+                    L.V = kSbmBlockV;
+                    L.R_pad = ceil_div(R, 32 * L.V) * 32 * L.V;
+                    L.W = L.R_pad / 32;
+                }
+            }
+        }
+    }
+    double c0 = std::isnan(prm->c0) ? problem_c0(p, s) : prm->c0;
+    out->c0_used = c0;
+    std::vector<double> sched(T_);
+    sbm_schedule(prm->a0, T_, sched.data());
+    const int64_t rbegin = opts ? opts->replica_begin : 0;
+    DevBuf<T> q(n * L.R_pad, s), q2(n * L.R_pad, s), pm(n * L.R_pad, s);
+    DevBuf<uint32_t> sb(n * L.W, s);
+    int64_t launches = 0;
+    k_init_sbm<T><<<nblk(((2 * n + 3) / 4) * L.R_pad), TB, 0, s>>>(
+        n, 0, n, L.R_pad, L.V, prm->seed, rbegin, prm->init_noise, q.get(), pm.get());
+    VXQ_CHECK_LAUNCH();
+    ++launches;
     if (dense) {
         // per-step energies (want_trace): exact on the uniform-|J| exact-field kernel with
         // h = 0 (a spin plane next to the digit planes), NaN on the other dense kinds
@@ -1611,6 +1924,7 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
         }
         out->path_used = VXQ_PATH_DENSE;
         out->dense_kind = dense_last_kind();
+        out->step_kernel = VXQ_KERNEL_DENSE_RUN;
         finish_outputs<T>(p, L, sb.get(), q.get(), pm.get(), opts, out, s,
                           p->uniform_magnitude ? qq.get() : nullptr);
         out->launches = launches + 4;
@@ -1622,7 +1936,7 @@ void sbm_solve_t(Problem* p, const vxq_sbm_params* prm, const vxq_run_opts* opts
     Tracker trk;
     trk.init(p, L, T_, want_trace, want_best, s);
     sbm_run_core<T>(p, L, op, g, sched, prm->dt, prm->a0, c0, prm->q_cap, req, p->nnz,
-                    q.get(), q2.get(), pm.get(), out, launches, s, &qf, &trk, sb.get());
+                    q.get(), q2.get(), pm.get(), out, launches, s, &qf, &trk, sb.get(), nbrb);
     launch_pack<T>(L, qf, sb.get(), s);
     ++launches;
     trk.observe(p, sb.get(), T_, T_, s);
@@ -1928,6 +2242,7 @@ void session_finish_t(Session* S, int64_t T_, vxq_outputs* out, const vxq_run_op
     finish_outputs<T>(S->p, F, sb, xa, ma, opts, out, S->s);
     out->loop_ms = 0;
     out->path_used = VXQ_PATH_SPARSE;
+    out->step_kernel = S->solver == 0 ? VXQ_KERNEL_PA_STEP : VXQ_KERNEL_SBM_STEP;
 }
 }  // namespace
 

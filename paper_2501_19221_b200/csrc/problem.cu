@@ -27,6 +27,8 @@ Problem::~Problem() {
     cudaStreamSynchronize(0);
     extern void dense_destroy(DenseOperand*);
     if (dense) dense_destroy(dense);
+    extern void nbr_blocks_destroy(NbrBlocks*);
+    if (nbr_blocks) nbr_blocks_destroy(nbr_blocks);
     cudaSetDevice(prev);
 }
 

@@ -16,6 +16,7 @@ namespace vxq {
 constexpr int kMaxLimbs = 8;
 
 struct DenseOperand;  // dense tcgen05 path (dense_tc.cu)
+struct NbrBlocks;     // row-block neighbour lists of the blocked sparse SBM step (dynamics.cu)
 
 // lambda_max of the SBM coupling matrix (eigen.cu, eig_extreme "max")
 constexpr int kEigDense = 0;       // n <= 512: full-dimension Lanczos, full reorthogonalisation
@@ -68,6 +69,8 @@ struct Problem {
     EigInfo eig;      // how c0 was obtained (vxq_problem_eig_info)
     int h_zero = -1;  // cached problem_h_zero (-1 = unknown)
     DenseOperand* dense = nullptr;
+    NbrBlocks* nbr_blocks = nullptr;  // built on the first blocked-SBM eligibility check
+    int nbr_blocks_state = 0;         // 0 unknown, 1 built (eligible), -1 not eligible
 
     ~Problem();
 };

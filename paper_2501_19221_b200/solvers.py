@@ -225,7 +225,8 @@ def run_pa(model, params, *, precision="fp32", path="auto", device=0, replica_be
                                         ctypes.byref(out)))
     info = {"lambda0": out.lambda0_used, "loop_ms": out.loop_ms, "launches": out.launches,
             "path": _lib.PATH_NAMES.get(out.path_used, "?"), "precision": precision,
-            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind), "energy_trace": tr,
+            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind),
+            "kernel": _lib.STEP_KERNELS.get(out.step_kernel), "energy_trace": tr,
             "track_best": track_best}
     return RunResult(st, en, order, x, m, info)
 
@@ -244,7 +245,8 @@ def run_sbm(model, params, *, precision="fp32", path="auto", device=0, replica_b
                                          ctypes.byref(out)))
     info = {"c0": out.c0_used, "loop_ms": out.loop_ms, "launches": out.launches,
             "path": _lib.PATH_NAMES.get(out.path_used, "?"), "precision": precision,
-            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind), "energy_trace": tr,
+            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind),
+            "kernel": _lib.STEP_KERNELS.get(out.step_kernel), "energy_trace": tr,
             "track_best": track_best}
     return RunResult(st, en, order, x, m, info)
 
@@ -279,7 +281,7 @@ def run_sa(model, params, *, precision="fp32", path="auto", device=0, replica_be
                                         ctypes.byref(out)))
     info = {"T_init": out.lambda0_used, "T_final": out.c0_used, "loop_ms": out.loop_ms,
             "launches": out.launches, "path": _lib.PATH_NAMES.get(out.path_used, "?"),
-            "precision": precision}
+            "precision": precision, "kernel": _lib.STEP_KERNELS.get(out.step_kernel)}
     return RunResult(st, en, order, None, None, info)
 
 
@@ -310,7 +312,8 @@ def run_device(kind: str, model, params, states_ptr: int, energies_ptr: int, *,
                                    ctypes.byref(out)))
     return {"lambda0": out.lambda0_used, "c0": out.c0_used, "loop_ms": out.loop_ms,
             "launches": out.launches, "path": _lib.PATH_NAMES.get(out.path_used, "?"),
-            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind)}
+            "dense_kind": _lib.DENSE_KINDS.get(out.dense_kind),
+            "kernel": _lib.STEP_KERNELS.get(out.step_kernel)}
 
 
 def sampleset_from(res: RunResult, R: int, seed, wall_time: float, replica_begin: int = 0):

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
-    assert L.vxq_abi_version() == 4
+    assert L.vxq_abi_version() == 5
 
 
 def test_struct_layouts_match_header():
@@ -36,7 +36,8 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.SbmParamsC) == 64
     assert ctypes.sizeof(_lib.SaParamsC) == 48
     assert ctypes.sizeof(_lib.RunOptsC) == 32
-    assert ctypes.sizeof(_lib.OutputsC) == 88
+    assert ctypes.sizeof(_lib.OutputsC) == 96
+    assert _lib.OutputsC.step_kernel.offset == 88  # ABI 5
 
 
 @pytest.mark.parametrize("T", [1, 2, 3, 10, 999, 1000, 10_000])
