@@ -57,6 +57,8 @@ def test_cluster_equals_step_kernel_and_oracle(monkeypatch, n, R, C, deg, hubs):
     a = run(monkeypatch, m, R, T, mode=2, C=C)
     b = run(monkeypatch, m, R, T, mode=0)
     assert a.info["launches"] < b.info["launches"] - T + 5, "cluster kernel did not run"
+    assert a.info["kernel"] == "k_pa_cluster"
+    assert b.info["kernel"] == ("k_pa_step_coop" if R <= 32 else "k_pa_step")
     assert np.array_equal(a.x, b.x) and np.array_equal(a.m, b.m)
     assert np.array_equal(a.states, b.states) and np.array_equal(a.energies, b.energies)
     reps = np.unique(np.r_[0, 1, R // 2, R - 1])
@@ -105,6 +107,7 @@ def test_cfg3_cluster_mode_auto_eligibility(monkeypatch):
     monkeypatch.delenv("VXQ_PA_CLUSTER", raising=False)
     d = vxq.run_pa(m, vxq.PaParams(steps=T, replicas=4096, seed=0), want_state=True)
     assert d.info["path"] == "sparse" and d.info["launches"] >= T
+    assert d.info["kernel"] == "k_pa_step"
     a = run(monkeypatch, m, 4096, T, mode=1, seed=0)
-    assert a.info["launches"] < T
+    assert a.info["launches"] < T and a.info["kernel"] == "k_pa_cluster"
     assert np.array_equal(a.x, d.x) and np.array_equal(a.m, d.m)
