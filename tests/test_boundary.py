@@ -30,6 +30,29 @@ def test_library_exports_every_declared_symbol():
     assert L.vxq_abi_version() == 5
 
 
+def header_constants(prefix):
+    text = open(os.path.join(ROOT, "include", "vxq.h")).read()
+    return {int(v): k for k, v in re.findall(r"#define\s+(" + prefix + r"\w+)\s+(\d+)", text)}
+
+
+def test_kernel_and_kind_codes_match_header():
+    """The names the Python layer reports (info["kernel"], info["dense_kind"]) are the
+    header's VXQ_KERNEL_* / VXQ_DENSE_KIND_* codes."""
+    kernels = header_constants("VXQ_KERNEL_")
+    assert set(kernels) == set(_lib.STEP_KERNELS)
+    for code, macro in kernels.items():
+        name = _lib.STEP_KERNELS[code]
+        if code == 0:
+            assert name is None and macro == "VXQ_KERNEL_NONE"
+        else:  # VXQ_KERNEL_PA_STEP_COOP <-> k_pa_step_coop
+            assert name == "k_" + macro[len("VXQ_KERNEL_"):].lower(), (macro, name)
+    kinds = header_constants("VXQ_DENSE_KIND_")
+    assert set(kinds) == set(_lib.DENSE_KINDS)
+    for code, macro in kinds.items():
+        if code:
+            assert _lib.DENSE_KINDS[code] == macro[len("VXQ_DENSE_KIND_"):].lower()
+
+
 def test_struct_layouts_match_header():
     # field order / sizes of the ctypes mirrors (x86-64 SysV)
     assert ctypes.sizeof(_lib.PaParamsC) == 48
