@@ -675,7 +675,11 @@ def run_ours(args):
 
         (rows, _t0), (cols, _t1), (vals, _t2), (hv, _t3) = (
             pinned(model.rows), pinned(model.cols), pinned(model.values), pinned(model.h))
-        h2d = int(rows.nbytes + cols.nbytes + vals.nbytes + hv.nbytes)
+        # bytes the upload actually moves: a dense (full upper triangle) model crosses PCIe
+        # as values + h only, its indices are generated on the device (vxq_problem_create)
+        from paper_2501_19221_b200.device import full_triangle
+        h2d = int((0 if full_triangle(n, rows, cols) else rows.nbytes + cols.nbytes) +
+                  vals.nbytes + hv.nbytes)
         d2h = int(R * n + 16 * R)
         walls = []
         for k in range(K + 1):

@@ -160,7 +160,10 @@ typedef struct {
 
 /* Build a device problem from the reference's canonical arrays:
  * rows/cols int64 with rows[k] < cols[k], sorted unique (model.py:81-104),
- * values/h fp64, offset. device = CUDA ordinal. Host pointers. */
+ * values/h fp64, offset. device = CUDA ordinal. Host pointers.
+ * Dense models: rows = cols = NULL with num_couplings = n (n - 1) / 2 means the full
+ * upper triangle in canonical (row-major) order -- the only canonical set of that size --
+ * and only the values cross PCIe (the indices are generated on the device). */
 VXQ_API int vxq_problem_create(int64_t n, int64_t num_couplings, const int64_t* rows,
                        const int64_t* cols, const double* values, const double* h,
                        double offset, int device, vxq_problem** out);

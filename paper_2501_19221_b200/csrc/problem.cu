@@ -74,6 +74,24 @@ __global__ void k_row_total(int64_t n, const int32_t* up, const int32_t* lo, int
     if (i == n) tot[i] = 0;
 }
 
+// (rows[k], cols[k]) of the full upper triangle in canonical order: row i starts at
+// i (n - 1) - i (i - 1) / 2; binary search for the row of k
+__global__ void k_triangle_coo(int64_t n, int64_t m, int64_t* __restrict__ rows,
+                               int64_t* __restrict__ cols) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    int64_t lo = 0, hi = n - 2;  // the row i with start(i) <= k < start(i + 1)
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        const int64_t st = mid * (n - 1) - mid * (mid - 1) / 2;
+        if (st <= k) lo = mid;
+        else hi = mid - 1;
+    }
+    const int64_t st = lo * (n - 1) - lo * (lo - 1) / 2;
+    rows[k] = lo;
+    cols[k] = lo + 1 + (k - st);
+}
+
 __global__ void k_iota(int64_t m, int32_t* v) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k < m) v[k] = (int32_t)k;
@@ -342,7 +360,11 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
     VXQ_REQUIRE(n >= 1, "model needs at least one variable");
     VXQ_REQUIRE(n < (1LL << 31) - 1, "n must be < 2^31");
     VXQ_REQUIRE(m >= 0 && m < (1LL << 31) - 1, "num_couplings must be in [0, 2^31)");
-    VXQ_REQUIRE(m == 0 || (rows && cols && values), "null coupling arrays");
+    // rows = cols = NULL: the full upper triangle (dense model), generated on the device
+    const bool implied = m > 0 && !rows && !cols;
+    VXQ_REQUIRE(!implied || (n >= 2 && m == n * (n - 1) / 2),
+                "rows = cols = NULL needs num_couplings = n (n - 1) / 2");
+    VXQ_REQUIRE(m == 0 || ((implied || (rows && cols)) && values), "null coupling arrays");
     VXQ_REQUIRE(std::isfinite(offset), "offset must be finite");
     int ndev = 0;
     VXQ_CUDA(cudaGetDeviceCount(&ndev));
@@ -424,8 +446,13 @@ Problem* problem_create(int64_t n, int64_t m, const int64_t* rows, const int64_t
         if (m > 0) {
             drows = DevBuf<int64_t>(m, s);
             dcols = DevBuf<int64_t>(m, s);
-            VXQ_CUDA(cudaMemcpyAsync(drows.get(), rows, m * sizeof(int64_t), cudaMemcpyDefault, s));
-            VXQ_CUDA(cudaMemcpyAsync(dcols.get(), cols, m * sizeof(int64_t), cudaMemcpyDefault, s));
+            if (implied) {
+                k_triangle_coo<<<nblk(m), TB, 0, s>>>(n, m, drows.get(), dcols.get());
+                VXQ_CHECK_LAUNCH();
+            } else {
+                VXQ_CUDA(cudaMemcpyAsync(drows.get(), rows, m * sizeof(int64_t), cudaMemcpyDefault, s));
+                VXQ_CUDA(cudaMemcpyAsync(dcols.get(), cols, m * sizeof(int64_t), cudaMemcpyDefault, s));
+            }
             VXQ_CUDA(cudaEventRecord(ev_rc, s));
             VXQ_CUDA(cudaStreamWaitEvent(s2, ev_rc, 0));  // one transfer at a time on PCIe
             VXQ_CUDA(cudaMemcpyAsync(dval.get(), values, m * sizeof(double), cudaMemcpyDefault,

@@ -21,6 +21,33 @@ _cache: dict[tuple[int, int], "DeviceProblem"] = {}
 _cache_lock = threading.Lock()
 
 
+def full_triangle(n: int, rows, cols) -> bool:
+    """True when the canonical COO arrays are the full upper triangle (a dense model):
+    n (n - 1) / 2 sorted unique pairs i < j can only be all of them, so the check is the
+    count plus a strided sample (insurance against non-canonical input).  Such a model is
+    uploaded as values only -- vxq_problem_create generates the indices on the device."""
+    m = len(rows)
+    if n < 2 or m == 0 or m != n * (n - 1) // 2 or len(cols) != m:
+        return False
+    k = np.unique(np.r_[np.linspace(0, m - 1, 4096).astype(np.int64), 0, m - 1])
+    i = np.floor(((2 * n - 1) - np.sqrt((2.0 * n - 1) ** 2 - 8.0 * k)) / 2).astype(np.int64)
+    st = i * (n - 1) - i * (i - 1) // 2
+    i = np.where(st > k, i - 1, i)  # floating-point edge of the closed form
+    st = i * (n - 1) - i * (i - 1) // 2
+    i = np.where(k >= st + (n - 1 - i), i + 1, i)
+    st = i * (n - 1) - i * (i - 1) // 2
+    return bool(np.array_equal(np.asarray(rows)[k], i) and
+                np.array_equal(np.asarray(cols)[k], i + 1 + (k - st)))
+
+
+def upload_bytes(model) -> int:
+    """Host -> device bytes of a problem upload (COO + h)."""
+    n = int(model.n)
+    m = len(model.values)
+    idx = 0 if full_triangle(n, model.rows, model.cols) else 16 * m
+    return idx + 8 * m + 8 * n
+
+
 class DeviceProblem:
     """Owns one vxq_problem handle."""
 
@@ -35,7 +62,9 @@ class DeviceProblem:
         if h.shape != (n,):
             raise ValidationError(f"field vector has shape {h.shape}, expected ({n},)")
         handle = ctypes.c_void_p()
-        _lib.check(L.vxq_problem_create(n, int(vals.shape[0]), _lib.ptr(rows), _lib.ptr(cols),
+        dense = full_triangle(n, rows, cols)  # values only; indices generated on the device
+        _lib.check(L.vxq_problem_create(n, int(vals.shape[0]), None if dense else _lib.ptr(rows),
+                                        None if dense else _lib.ptr(cols),
                                         _lib.ptr(vals), _lib.ptr(h), float(model.offset),
                                         int(device), ctypes.byref(handle)))
         self.handle = handle

@@ -640,3 +640,34 @@ def test_sparse_sbm_r32_irregular_rows_match_oracle():
     Q, P = O.sbm_run(ip, ix, -dv, -m.h, O.sbm_schedule(1.0, 30), 0.05, 1.0, 0.3, 1.0, Q, P,
                      np.float32)
     assert np.array_equal(s.x, Q.astype(np.float64)) and np.array_equal(s.m, P.astype(np.float64))
+
+
+def test_dense_model_values_only_upload_is_identical(monkeypatch):
+    """A full-upper-triangle model crosses PCIe as values only (indices generated on the
+    device by vxq_problem_create): problem, lambda0, c0 and PA / SBM solves equal those of
+    the explicit-index upload bit for bit."""
+    from paper_2501_19221_b200 import device
+    rng = np.random.default_rng(3)
+    n = 700
+    iu, ju = np.triu_indices(n, 1)
+    m = vxq.IsingModel.from_arrays(n, iu, ju, rng.normal(size=len(iu)) / np.sqrt(n),
+                                   h=rng.uniform(-1, 1, n), canonical=True)
+    assert device.full_triangle(n, m.rows, m.cols)
+
+    def solve(model):
+        dp = device.DeviceProblem(model)
+        info = dp.info()
+        lam, c0 = dp.lambda0(), dp.c0()
+        r = vxq.run_pa(model, vxq.PaParams(steps=30, replicas=128, seed=1), want_state=True,
+                       cache=False)
+        s = vxq.run_sbm(model, vxq.SbmParams(steps=30, dt=0.05, replicas=128, seed=1),
+                        want_state=True, cache=False)
+        return info, lam, c0, r, s
+
+    a = solve(m)
+    monkeypatch.setattr(device, "full_triangle", lambda *args: False)
+    b = solve(m)
+    assert a[0] == b[0] and a[1] == b[1] and a[2] == b[2]
+    for ra, rb in ((a[3], b[3]), (a[4], b[4])):
+        assert np.array_equal(ra.x, rb.x) and np.array_equal(ra.energies, rb.energies)
+        assert np.array_equal(ra.states, rb.states)

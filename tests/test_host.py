@@ -131,3 +131,23 @@ def test_run_opts_stream_mapping():
     assert _opts("fp32", "auto", 0).stream is None
     assert _opts("fp32", "auto", 0, stream=0).stream == 0x1
     assert _opts("fp32", "auto", 0, stream=0x7f00).stream == 0x7f00
+
+
+def test_full_triangle_detection():
+    """Dense models upload values only (vxq_problem_create with rows = cols = NULL): the
+    detection accepts exactly the canonical full upper triangle."""
+    from paper_2501_19221_b200.device import full_triangle, upload_bytes
+    for n in (2, 3, 17, 300, 2049):
+        iu, ju = np.triu_indices(n, 1)
+        assert full_triangle(n, iu.astype(np.int64), ju.astype(np.int64))
+        assert not full_triangle(n + 1, iu, ju)
+        if len(iu) > 1:
+            assert not full_triangle(n, iu[:-1], ju[:-1])
+    iu, ju = np.triu_indices(300, 1)
+    bad = ju.copy()
+    bad[-1] = 0  # the last pair is always sampled
+    assert not full_triangle(300, iu, bad)
+    sk = vxq.IsingModel.from_arrays(300, iu, ju, np.ones(len(iu)), canonical=True)
+    assert upload_bytes(sk) == 8 * len(iu) + 8 * 300
+    sparse = vxq.IsingModel.from_arrays(300, iu[:10], ju[:10], np.ones(10), canonical=True)
+    assert upload_bytes(sparse) == 24 * 10 + 8 * 300
