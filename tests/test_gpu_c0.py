@@ -87,3 +87,20 @@ def test_c0_sbm_solve_uses_it():
     m = instances.maxcut3(100_000)
     s = vxq.run_sbm(m, vxq.SbmParams(steps=3, dt=0.05, replicas=32, seed=0))
     assert s.info["c0"] == vxq.resolve_c0(m)
+
+
+def test_c0_dense_int8_spmv_matches_csr_spmv(monkeypatch):
+    """Dense uniform-|J| problems run the Lanczos SpMV over an int8 K (n^2 bytes) instead of
+    the CSR (12 bytes per entry): the returned c0 agrees with the CSR-SpMV value and with
+    the exact lambda_max of -A (numpy eigvalsh) to the ARPACK-level tolerance."""
+    n = 2500
+    m = instances.sk(n)
+    a = get_problem(m, cache=False).c0()
+    monkeypatch.setenv("VXQ_EIG_DENSE", "0")
+    b = get_problem(m, cache=False).c0()
+    A = np.zeros((n, n))
+    A[m.rows, m.cols] = m.values
+    A[m.cols, m.rows] = m.values
+    lam = np.linalg.eigvalsh(-A)[-1]
+    assert abs(a - b) <= 1e-7 * abs(b)
+    assert abs(1.0 / a - lam) <= 1e-7 * abs(lam)
