@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(TB) k_spmv_dot_rows(int64_t n, const int64_t* 
 // then streams K as int8 (n^2 bytes: 100 MB at n = 10^4) instead of the CSR's 12 bytes per
 // entry (1.2 GB): w_i = (sign c) * sum_j K_ij v_j, one warp per row, 4 columns per lane per
 // pass (coalesced K bytes and v words; zero entries skipped), fixed reduction order
-// (deterministic).  (A 16-column unrolled, branch-free variant measured slower: 80 vs 33 ms.)
+// (deterministic).
 __global__ void k_build_dense_k8(int64_t n, int64_t ld, const int64_t* __restrict__ indptr,
                                  const int32_t* __restrict__ indices,
                                  const double* __restrict__ data, int8_t* __restrict__ K) {
@@ -275,37 +275,36 @@ __global__ void k_build_dense_k8(int64_t n, int64_t ld, const int64_t* __restric
         K[row * ld + indices[k]] = data[k] > 0.0 ? 1 : -1;
 }
 
-__global__ void __launch_bounds__(TB) k_dense_spmv_dot(int64_t n, int64_t ld,
-                                                       const int8_t* __restrict__ K,
-                                                       double scale, const double* v, double* w,
-                                                       double* part) {
-    __shared__ double sh[TB / 32];
+// one CTA of kDenseSpmvThreads per row (a warp per row left each warp ~80 dependent passes
+// over its 10 KB row); partial sums combined in a fixed order; part[b] = row b's v_i w_i
+constexpr int kDenseSpmvThreads = 128;
+__global__ void __launch_bounds__(kDenseSpmvThreads) k_dense_spmv_dot(
+    int64_t n, int64_t ld, const int8_t* __restrict__ K, double scale, const double* v,
+    double* w, double* part) {
+    __shared__ double sh[kDenseSpmvThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double dsum = 0.0;
-    const int64_t row = (int64_t)blockIdx.x * (TB / 32) + wid;
-    if (row < n) {
-        const int8_t* kr = K + row * ld;
-        double acc = 0.0;
-        for (int64_t j = (int64_t)lane * 4; j < ld; j += 128) {
-            const char4 k4 = *reinterpret_cast<const char4*>(kr + j);
-            if (k4.x) acc += k4.x > 0 ? v[j] : -v[j];
-            if (k4.y) acc += k4.y > 0 ? v[j + 1] : -v[j + 1];
-            if (k4.z) acc += k4.z > 0 ? v[j + 2] : -v[j + 2];
-            if (k4.w) acc += k4.w > 0 ? v[j + 3] : -v[j + 3];
-        }
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        acc *= scale;
-        if (lane == 0) {
-            w[row] = acc;
-            dsum = v[row] * acc;
-        }
+    const int64_t row = blockIdx.x;
+    const int8_t* kr = K + row * ld;
+    double acc = 0.0;
+    // 4 K bytes per thread per pass: the threads' v reads stay within a few lines per
+    // instruction (16 bytes per thread spread them over 32 lines: 88 ms instead of 27 for
+    // the SK n = 10^4 c0); zero entries (incl. the row padding past n) never touch v
+    for (int64_t j = (int64_t)threadIdx.x * 4; j < ld; j += 4 * kDenseSpmvThreads) {
+        const char4 k4 = *reinterpret_cast<const char4*>(kr + j);
+        if (k4.x) acc += k4.x > 0 ? v[j] : -v[j];
+        if (k4.y) acc += k4.y > 0 ? v[j + 1] : -v[j + 1];
+        if (k4.z) acc += k4.z > 0 ? v[j + 2] : -v[j + 2];
+        if (k4.w) acc += k4.w > 0 ? v[j + 3] : -v[j + 3];
     }
-    if (lane == 0) sh[wid] = dsum;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sh[wid] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int k = 0; k < TB / 32; ++k) t += sh[k];
-        part[blockIdx.x] = t;
+        for (int k = 0; k < kDenseSpmvThreads / 32; ++k) t += sh[k];
+        t *= scale;
+        w[row] = t;
+        part[row] = v[row] * t;
     }
 }
 
@@ -598,7 +597,8 @@ struct Lanczos {
                 n, ld, p_->indptr, p_->indices, p_->data64, kd.get());
             VXQ_CHECK_LAUNCH();
             kscale = sign * p_->magnitude;
-            spmv_blocks = (unsigned)ceil_div(n * 32, TB);
+            spmv_blocks = (unsigned)n;  // one CTA per row: n partials
+            if (n > (int64_t)part.count) part = DevBuf<double>(n, s_);
         }
     }
 
@@ -617,8 +617,8 @@ struct Lanczos {
     // step k: w = B v_k - alpha_k v_k - beta_{k-1} v_{k-1}; beta_k = ||w||  (4 launches)
     void step(int64_t k, double* alpha, double* beta) {
         if (kd.get())
-            k_dense_spmv_dot<<<spmv_blocks, TB, 0, s>>>(n, ld, kd.get(), kscale, v, w.get(),
-                                                        part.get());
+            k_dense_spmv_dot<<<spmv_blocks, kDenseSpmvThreads, 0, s>>>(n, ld, kd.get(), kscale, v,
+                                                                       w.get(), part.get());
         else if (short_rows)
             k_spmv_dot_rows<<<spmv_blocks, TB, 0, s>>>(n, p->indptr, p->indices, p->data64,
                                                        sign, v, w.get(), part.get());
